@@ -1,0 +1,214 @@
+/*
+ * tileqr.h -- C ABI of the B200-native (sm_100a) FP64 tile Householder QR
+ * library libtileqr.so (package paper_1102_5328_b200).
+ *
+ * The method is the PLASMA-style tile QR of arxiv 1102.5328 (INRIA RR-7526):
+ * "split the initial matrix of order N into NT x NT smaller square pieces of
+ * order NB, called tiles", factored by four serial kernels
+ * "DGEQRT and DTSQRT ... DLARFB and DSSRFB" whose DAG is
+ * executed level by level; (NB, IB) are the tunable parameters of Problem 1
+ * and tileqr_tune applies the paper's Step-1/Step-2
+ * pruning.  Kernel internals follow the compact-WY
+ * formulation adopted by SPEC.md:125 (readings listed in DESIGN.md).
+ *
+ * Conventions (all entry points):
+ *   - Matrices are FP64, column-major.  Pointers are DEVICE pointers on the
+ *     current CUDA device unless the name starts with h_ (host).
+ *   - Work is stream-ordered on `stream` (0 = legacy default stream); the
+ *     library never synchronizes the stream except where stated (tune).
+ *   - The caller owns A, T, B and every batched operand; the library owns a
+ *     workspace (padded tile buffer, task lists, CUDA graphs, NCCL comm)
+ *     cached per (device, shape) and released by tileqr_finalize().
+ *   - Return value: 0 = success; -i = the i-th argument is illegal (LAPACK
+ *     xerbla style, nothing is launched); > 0 = TILEQR_ERR_* (message from
+ *     tileqr_last_error()).  NB must satisfy 1 <= NB <= 512 (the paper bounds
+ *     tiles by 512) and 1 <= IB <= NB with IB dividing NB
+ *     (PAPER.md:366-367).
+ *   - Results are deterministic: bitwise identical run to run (and across
+ *     GPU counts in tileqr_dist_factor) for the same (NB, IB).
+ *   - No CPU fallback exists: without a CUDA device every compute call returns
+ *     TILEQR_ERR_CUDA.
+ */
+#ifndef TILEQR_H_
+#define TILEQR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tileqr_stream_t; /* == cudaStream_t */
+
+enum {
+  TILEQR_OK = 0,
+  TILEQR_ERR_CUDA = 1,     /* a CUDA runtime call or kernel launch failed  */
+  TILEQR_ERR_NCCL = 2,     /* an NCCL call failed                           */
+  TILEQR_ERR_ALLOC = 3,    /* device or host allocation failed              */
+  TILEQR_ERR_NOT_INIT = 4, /* tileqr_dist_* before tileqr_dist_init         */
+  TILEQR_ERR_INTERNAL = 5
+};
+
+/* Library version string, e.g. "tileqr 0.1 sm_100a". */
+const char* tileqr_version(void);
+
+/* Thread-local text of the last error (empty string when none). */
+const char* tileqr_last_error(void);
+
+/* Number of doubles of the T buffer of an M x N factorization:
+ * MT*NT*IB*NB with MT = ceil(M/NB), NT = ceil(N/NB).
+ * T tile (m,k), m >= k, starts at offset (m + k*MT)*IB*NB and is IB x NB with
+ * ld = IB: block p (columns [p*IB,(p+1)*IB)) is the IB x IB upper-triangular
+ * compact-WY factor of inner panel p; its strictly-lower part is 0.
+ * Errors: -1..-4 for M < 0, N < 0, bad NB, bad IB; -5 for n_doubles == NULL. */
+int tileqr_t_size(int64_t M, int64_t N, int NB, int IB, size_t* n_doubles);
+
+/* ------------------------------------------------------------------------
+ * tileqr_factor -- tile QR of the M x N matrix A (Fig. 1).
+ *
+ *   A  [in/out] device, M x N, leading dimension lda >= max(1, M).
+ *      On return (PLASMA convention): R in the upper triangle
+ *      of A[0:min(M,N), 0:N]; V_kk strictly below the diagonal of tile (k,k)
+ *      (unit diagonal implicit); the full V2_mk in tile (m,k), m > k.
+ *      Non-dividing sizes are padded internally (reading R5).
+ *   T  [out] device, tileqr_t_size() doubles (layout above); overwritten.
+ *   d_info [out] device int (may be NULL): 0 = ok, 1 = A held a non-finite
+ *      entry (the factorization still runs; its output is then unspecified).
+ *   Workspace: (MT*NB) x (NT*NB) doubles plus task lists, cached.
+ *   Errors: -1 M<0, -2 N<0, -3 A==NULL (M,N>0), -4 lda<max(1,M), -5 NB,
+ *   -6 IB, -7 T==NULL.  Quick return for M == 0 or N == 0.
+ * ------------------------------------------------------------------------ */
+int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, double* T,
+                  int* d_info, tileqr_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * tileqr_apply_qt -- B <- Q^T B (trans = 'T') or B <- Q B (trans = 'N') with
+ * the Q of a tileqr_factor output:
+ *   'T': k ascending: LARFB(k) on B's row-tile k, then SSRFB(k,m) on row-tiles
+ *        (k, m) for m ascending;
+ *   'N': k descending: SSRFB(k,m) for m descending, then LARFB(k); panels in
+ *        reverse order and T not transposed.
+ *   M x K is the shape that was factored (A, lda, T as returned, same NB/IB);
+ *   B is M x NRHS, ldb >= max(1, M).
+ *   Errors: -1 trans, -2 M, -3 NRHS, -4 K, -5 A, -6 lda, -7 T, -8 NB, -9 IB,
+ *   -10 B, -11 ldb.
+ * ------------------------------------------------------------------------ */
+int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double* A, int64_t lda,
+                    const double* T, int NB, int IB, double* B, int64_t ldb,
+                    tileqr_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Batched tile kernels.  Each takes DEVICE arrays of
+ * `batch` DEVICE pointers; every tile is NB x NB with ld = NB, every T is
+ * IB x NB with ld = IB.  Tiles within one call must not alias (except as
+ * stated).  batch == 0 is a no-op.  Errors: -1 NB, -2 IB, -3 batch < 0,
+ * -4.. NULL arrays (numbered in argument order), -(last) ncols out of range.
+ * ------------------------------------------------------------------------ */
+
+/* GEQRT: QR of each tile A[i] (R upper, V strictly lower), writes T[i]. */
+int tileqr_geqrt_batched(int NB, int IB, int batch, double* const* A, double* const* T,
+                         tileqr_stream_t stream);
+
+/* TSQRT: QR of [R[i]; A2[i]] with R[i] upper triangular: updates the upper
+ * triangle of R[i] only (its strict lower part is neither read nor written),
+ * overwrites A2[i] with V2, writes T[i]. */
+int tileqr_tsqrt_batched(int NB, int IB, int batch, double* const* R, double* const* A2,
+                         double* const* T, tileqr_stream_t stream);
+
+/* LARFB: C[i] <- Q^T C[i] ('T') or Q C[i] ('N') with Q from a GEQRT
+ * (V[i] strictly-lower part read, T[i]); C[i] is NB x ncols (ld = NB),
+ * 1 <= ncols <= NB. */
+int tileqr_larfb_batched(char trans, int NB, int IB, int batch, const double* const* V,
+                         const double* const* T, double* const* C, int ncols,
+                         tileqr_stream_t stream);
+
+/* SSRFB (TSMQR): [C1[i]; C2[i]] <- Q^T [C1; C2] ('T') or Q [C1; C2] ('N')
+ * with Q from a TSQRT (V2[i], T[i]); C1, C2 are NB x ncols (ld = NB),
+ * 1 <= ncols <= NB.  This is the dominant kernel. */
+int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* const* V2,
+                         const double* const* T, double* const* C1, double* const* C2,
+                         int ncols, tileqr_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * tileqr_tune -- the paper's two-step empirical tuning:
+ *   Step 1: time tileqr_ssrfb_batched for every (NB, IB)
+ *     of the grid NB in {64,96,...,256}, IB | NB (IB >= 8 unless
+ *     TILEQR_TUNE_SMALL_IB=1), 50 back-to-back launches on the same buffers
+ *     ("No Flush"); rate = 50*batch*4*NB^3/t.
+ *   Pre-selection: Property 1, upper convex hull (Property 2), then Heuristic
+ *     0/1/2, cap 8.
+ *   Step 2: for N' on a ladder ascending to N, time
+ *     tileqr_factor 6x per surviving candidate (median), then drop NB2 when
+ *     some NB1 > NB2 is strictly faster (Property 3, if payg != 0).
+ *   Returns the best (NB, IB) at N in *h_NB, *h_IB.  Synchronizes the current
+ *   device.  report_json_path (nullable) receives the Step-1 data set, the
+ *   candidate set and every Step-2 sample as JSON.
+ *   Errors: -1 M, -2 N, -3 ngpus (must be 1 here; see tileqr_dist_factor),
+ *   -4 heuristic not in {0,1,2}, -6/-7 NULL outputs.
+ * ------------------------------------------------------------------------ */
+int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h_NB, int* h_IB,
+                const char* report_json_path);
+
+/* Pure host pieces of the tuner (no GPU needed), exported for testing:
+ * Property 1 + upper hull + heuristic on n samples (nb[i], ib[i], gflops[i]);
+ * writes at most `cap` (heuristic 1/2) or n (heuristic 0) selected points to
+ * out_nb/out_ib/out_gflops (capacity n) and their count to *n_out. */
+int tileqr_preselect(int n, const int* h_nb, const int* h_ib, const double* h_gflops, int heuristic,
+                     int cap, int* h_out_nb, int* h_out_ib, double* h_out_gflops, int* n_out);
+/* Property 3 prune: keep[i] = 0 when some j has nb[j] > nb[i] and
+ * gflops[j] > gflops[i]; else 1. */
+int tileqr_payg_prune(int n, const int* h_nb, const double* h_gflops, int* h_keep);
+/* ASAP level of each task kind (G,L,T,S) in the tile DAG: the launcher's
+ * closed form (G(k)=3k, L(k,n)=3k+1, T(k,m)=2k+m, S(k,m,n)=2k+m+1);
+ * returns the number of levels of an MT x NT tile matrix in *n_levels. */
+int tileqr_num_levels(int64_t MT, int64_t NT, int64_t* n_levels);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: one process per GPU, tile columns 1D block-cyclic (tile column
+ * n lives on rank n mod nranks), panel V/T tiles broadcast from the owner of
+ * tile column k with NCCL over NVLink each DAG level.
+ * ------------------------------------------------------------------------ */
+/* h_nccl_unique_id: 128-byte ncclUniqueId from rank 0 (e.g. via
+ * torch.distributed); device: CUDA ordinal this rank uses. */
+int tileqr_dist_init(int nranks, int rank, const void* h_nccl_unique_id, int device);
+/* Writes a fresh ncclUniqueId (128 bytes) into h_id (rank 0 only). */
+int tileqr_dist_unique_id(void* h_id);
+/* Local tile storage of an N x N factorization (square, NB | padded N):
+ * n_local = number of tile columns owned by this rank; A_local holds them in
+ * tile layout: local column j (global n = rank + j*nranks) has its MT tiles
+ * at A_local + (m + j*MT)*NB*NB, column-major within a tile (ld = NB).
+ * T_local: tile (m, j) at (m + j*MT)*IB*NB. */
+int tileqr_dist_local_cols(int64_t N, int NB, int* n_local);
+/* Fill this rank's local tile columns with the synthetic generator below
+ * (global idx = i + j*N), zero/identity padding as tileqr_factor does. */
+int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed,
+                             tileqr_stream_t stream);
+/* Factor the distributed matrix in place; d_info as tileqr_factor. */
+int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
+                       tileqr_stream_t stream);
+void tileqr_dist_finalize(void);
+
+/* ------------------------------------------------------------------------
+ * Utilities.
+ * ------------------------------------------------------------------------ */
+/* Synthetic input generator (same counter-based
+ * generator as synth_inputs.uniform):
+ *   A[i + j*lda] = (splitmix64(splitmix64(seed) + offset + i + j*M) >> 11)
+ *                  * 2^-53 - 0.5 */
+int tileqr_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t seed,
+                       uint64_t offset, tileqr_stream_t stream);
+
+/* Name of the implementation tileqr_ssrfb_batched / tileqr_larfb_batched use
+ * for this (NB, IB): "dmma" (FP64 tensor-core mma.sync path, NB % 32 == 0,
+ * 32 <= NB <= 256) or "simt" (any NB <= 512). */
+const char* tileqr_ssrfb_impl(int NB, int IB);
+
+/* Release all cached workspaces, graphs and communicators. */
+void tileqr_finalize(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TILEQR_H_ */

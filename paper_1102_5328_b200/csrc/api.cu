@@ -1,0 +1,542 @@
+// api.cu -- C ABI of libtileqr (include/tileqr.h): argument checking, error
+// model, per-shape workspaces, and the wavefront (DAG-level) launcher of the
+// tile QR factorization.
+//
+// The DAG of the flat-tree tile QR (Fig. 1b) is executed
+// level by level.  Every task is placed at its ASAP level, which has the
+// closed form (checked against an explicit dependency DP in
+// tests): GEQRT(k) = 3k, LARFB(k,n) = 3k+1, TSQRT(k,m) = 2k+m,
+// SSRFB(k,m,n) = 2k+m+1, so an MT x NT matrix has 3*min(MT,NT)-2 (+ the tail
+// of a tall matrix) levels.  All tasks of one kind at one level are
+// independent and run as ONE batched launch; the panel kernels (GEQRT, TSQRT)
+// and the update kernels (LARFB, SSRFB) of a level run concurrently on two
+// streams.  The whole level sequence is captured once per shape into a CUDA
+// graph and replayed (the GPU counterpart of PLASMA's static schedule,
+// PAPER.md:163-164).
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "internal.h"
+
+namespace tileqr {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+           cudaGetErrorString(e), what, file, line);
+  set_error(buf);
+  return TILEQR_ERR_CUDA;
+}
+
+static int arg_error(int i, const char* fn, const char* what) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: illegal argument %d (%s)", fn, i, what);
+  set_error(buf);
+  return -i;
+}
+
+// ---------------------------------------------------------------------------
+// Level schedule (closed form) and task lists
+// ---------------------------------------------------------------------------
+struct LevelLists {
+  int64_t nlev = 0;
+  // per level: offset/count into each kind's flat arrays
+  std::vector<int64_t> g_off, g_cnt, t_off, t_cnt, l_off, l_cnt, s_off, s_cnt;
+};
+
+static int64_t num_levels(int64_t MT, int64_t NT) {
+  const int64_t KT = std::min(MT, NT);
+  if (KT <= 0) return 0;
+  int64_t last = 0;
+  for (int64_t k = 0; k < KT; ++k) {
+    last = std::max(last, 3 * k);                              // G
+    if (NT > k + 1) last = std::max(last, 3 * k + 1);          // L
+    if (MT > k + 1) last = std::max(last, 2 * k + MT - 1);     // T(k, MT-1)
+    if (MT > k + 1 && NT > k + 1) last = std::max(last, 2 * k + MT);  // S(k, MT-1, .)
+  }
+  return last + 1;
+}
+
+// Host-side task lists in tile-index form; materialised to device pointers.
+struct HostTasks {
+  std::vector<std::vector<int64_t>> G, T, L, S;  // per level: flattened tuples
+};
+
+static void build_tasks(int64_t MT, int64_t NT, HostTasks& h, int64_t nlev) {
+  h.G.assign(nlev, {});
+  h.T.assign(nlev, {});
+  h.L.assign(nlev, {});
+  h.S.assign(nlev, {});
+  const int64_t KT = std::min(MT, NT);
+  for (int64_t k = 0; k < KT; ++k) {
+    h.G[3 * k].push_back(k);
+    for (int64_t n = k + 1; n < NT; ++n) {
+      h.L[3 * k + 1].push_back(k);
+      h.L[3 * k + 1].push_back(n);
+    }
+    for (int64_t m = k + 1; m < MT; ++m) {
+      h.T[2 * k + m].push_back(k);
+      h.T[2 * k + m].push_back(m);
+      for (int64_t n = k + 1; n < NT; ++n) {
+        auto& v = h.S[2 * k + m + 1];
+        v.push_back(k);
+        v.push_back(m);
+        v.push_back(n);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Workspace of one factorization shape
+// ---------------------------------------------------------------------------
+struct FactorWS {
+  int dev = -1;
+  int64_t M = 0, N = 0, MT = 0, NT = 0;
+  int NB = 0, IB = 0;
+  double* tiles = nullptr;  // (MT*NB) x (NT*NB) in tile layout
+  double* Tws = nullptr;    // MT*NT*IB*NB
+  void** dptr = nullptr;    // all pointer arrays
+  LevelLists lv;
+  // device pointer arrays per kind
+  double** gA = nullptr; double** gT = nullptr;
+  double** tR = nullptr; double** tA = nullptr; double** tT = nullptr;
+  double** lV = nullptr; double** lT = nullptr; double** lC = nullptr;
+  double** sV = nullptr; double** sT = nullptr; double** sC1 = nullptr; double** sC2 = nullptr;
+  cudaStream_t s_panel = nullptr, s_update = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaGraphExec_t graph = nullptr;
+  ~FactorWS() {
+    if (graph) cudaGraphExecDestroy(graph);
+    for (auto e : ev) cudaEventDestroy(e);
+    if (s_panel) cudaStreamDestroy(s_panel);
+    if (s_update) cudaStreamDestroy(s_update);
+    cudaFree(tiles);
+    cudaFree(Tws);
+    cudaFree(dptr);
+  }
+};
+
+static std::mutex g_mu;
+static std::map<std::tuple<int, int64_t, int64_t, int, int>, std::unique_ptr<FactorWS>> g_ws;
+
+static bool use_graph() {
+  const char* e = getenv("TILEQR_NO_GRAPH");
+  return !(e && e[0] == '1');
+}
+
+static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** out) {
+  auto ws = std::make_unique<FactorWS>();
+  ws->dev = dev;
+  ws->M = M;
+  ws->N = N;
+  ws->NB = NB;
+  ws->IB = IB;
+  ws->MT = (M + NB - 1) / NB;
+  ws->NT = (N + NB - 1) / NB;
+  const int64_t MT = ws->MT, NT = ws->NT;
+  const size_t tile = (size_t)NB * NB;
+  if (cudaMalloc(&ws->tiles, tile * MT * NT * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ws->Tws, (size_t)MT * NT * IB * NB * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("tileqr_factor: device allocation of the tile workspace failed");
+    return TILEQR_ERR_ALLOC;
+  }
+  const int64_t nlev = num_levels(MT, NT);
+  HostTasks h;
+  build_tasks(MT, NT, h, nlev);
+  LevelLists& lv = ws->lv;
+  lv.nlev = nlev;
+  int64_t nG = 0, nT = 0, nL = 0, nS = 0;
+  for (int64_t t = 0; t < nlev; ++t) {
+    lv.g_off.push_back(nG); lv.g_cnt.push_back((int64_t)h.G[t].size()); nG += h.G[t].size();
+    lv.t_off.push_back(nT); lv.t_cnt.push_back((int64_t)h.T[t].size() / 2); nT += h.T[t].size() / 2;
+    lv.l_off.push_back(nL); lv.l_cnt.push_back((int64_t)h.L[t].size() / 2); nL += h.L[t].size() / 2;
+    lv.s_off.push_back(nS); lv.s_cnt.push_back((int64_t)h.S[t].size() / 3); nS += h.S[t].size() / 3;
+  }
+  const size_t total = 2 * nG + 3 * nT + 3 * nL + 4 * nS;
+  std::vector<void*> hp(std::max<size_t>(total, 1));
+  double* A = ws->tiles;
+  double* T = ws->Tws;
+  auto tp = [&](int64_t m, int64_t n) { return A + (size_t)(m + n * MT) * tile; };
+  auto tt = [&](int64_t m, int64_t k) { return T + (size_t)(m + k * MT) * IB * NB; };
+  size_t o = 0;
+  const size_t oG = o; o += 2 * nG;
+  const size_t oT = o; o += 3 * nT;
+  const size_t oL = o; o += 3 * nL;
+  const size_t oS = o; o += 4 * nS;
+  {
+    size_t i = 0;
+    for (int64_t t = 0; t < nlev; ++t)
+      for (int64_t k : h.G[t]) {
+        hp[oG + i] = tp(k, k);
+        hp[oG + nG + i] = tt(k, k);
+        ++i;
+      }
+    i = 0;
+    for (int64_t t = 0; t < nlev; ++t)
+      for (size_t q = 0; q < h.T[t].size(); q += 2) {
+        const int64_t k = h.T[t][q], m = h.T[t][q + 1];
+        hp[oT + i] = tp(k, k);
+        hp[oT + nT + i] = tp(m, k);
+        hp[oT + 2 * nT + i] = tt(m, k);
+        ++i;
+      }
+    i = 0;
+    for (int64_t t = 0; t < nlev; ++t)
+      for (size_t q = 0; q < h.L[t].size(); q += 2) {
+        const int64_t k = h.L[t][q], n = h.L[t][q + 1];
+        hp[oL + i] = tp(k, k);
+        hp[oL + nL + i] = tt(k, k);
+        hp[oL + 2 * nL + i] = tp(k, n);
+        ++i;
+      }
+    i = 0;
+    for (int64_t t = 0; t < nlev; ++t)
+      for (size_t q = 0; q < h.S[t].size(); q += 3) {
+        const int64_t k = h.S[t][q], m = h.S[t][q + 1], n = h.S[t][q + 2];
+        hp[oS + i] = tp(m, k);
+        hp[oS + nS + i] = tt(m, k);
+        hp[oS + 2 * nS + i] = tp(k, n);
+        hp[oS + 3 * nS + i] = tp(m, n);
+        ++i;
+      }
+  }
+  if (cudaMalloc(&ws->dptr, hp.size() * sizeof(void*)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("tileqr_factor: device allocation of the task lists failed");
+    return TILEQR_ERR_ALLOC;
+  }
+  TQ_CUDA(cudaMemcpy(ws->dptr, hp.data(), hp.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  double** d = reinterpret_cast<double**>(ws->dptr);
+  ws->gA = d + oG; ws->gT = d + oG + nG;
+  ws->tR = d + oT; ws->tA = d + oT + nT; ws->tT = d + oT + 2 * nT;
+  ws->lV = d + oL; ws->lT = d + oL + nL; ws->lC = d + oL + 2 * nL;
+  ws->sV = d + oS; ws->sT = d + oS + nS; ws->sC1 = d + oS + 2 * nS; ws->sC2 = d + oS + 3 * nS;
+  TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_panel, cudaStreamNonBlocking));
+  TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_update, cudaStreamNonBlocking));
+  ws->ev.resize(4);
+  for (auto& e : ws->ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *out = ws.get();
+  g_ws[std::make_tuple(dev, M, N, NB, IB)] = std::move(ws);
+  return 0;
+}
+
+// Issue the level sequence: s_panel runs GEQRT/TSQRT, s_update LARFB/SSRFB.
+static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
+  const LevelLists& lv = ws->lv;
+  const int NB = ws->NB, IB = ws->IB;
+  cudaEvent_t ep = ws->ev[0], eu = ws->ev[1];
+  for (int64_t t = 0; t < lv.nlev; ++t) {
+    if (t > 0) {  // level t depends on everything of level t-1
+      TQ_CUDA(cudaEventRecord(eu, su));
+      TQ_CUDA(cudaStreamWaitEvent(sp, eu, 0));
+      TQ_CUDA(cudaEventRecord(ep, sp));
+      TQ_CUDA(cudaStreamWaitEvent(su, ep, 0));
+    }
+    int rc;
+    if (lv.g_cnt[t] > 0 &&
+        (rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp)))
+      return rc;
+    if (lv.t_cnt[t] > 0 &&
+        (rc = launch_tsqrt(NB, IB, (int)lv.t_cnt[t], ws->tR + lv.t_off[t], ws->tA + lv.t_off[t],
+                           ws->tT + lv.t_off[t], sp)))
+      return rc;
+    if (lv.l_cnt[t] > 0 &&
+        (rc = launch_larfb(true, NB, IB, (int)lv.l_cnt[t], ws->lV + lv.l_off[t], ws->lT + lv.l_off[t],
+                           ws->lC + lv.l_off[t], NB, su)))
+      return rc;
+    if (lv.s_cnt[t] > 0 &&
+        (rc = launch_ssrfb(true, NB, IB, (int)lv.s_cnt[t], ws->sV + lv.s_off[t], ws->sT + lv.s_off[t],
+                           ws->sC1 + lv.s_off[t], ws->sC2 + lv.s_off[t], NB, su)))
+      return rc;
+  }
+  return 0;
+}
+
+// Run the level sequence ordered after `stream` and before subsequent work on it.
+static int run_levels(FactorWS* ws, cudaStream_t stream) {
+  if (use_graph()) {
+    if (!ws->graph) {
+      cudaStream_t cs = ws->s_panel;
+      TQ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+      TQ_CUDA(cudaEventRecord(ws->ev[2], cs));
+      TQ_CUDA(cudaStreamWaitEvent(ws->s_update, ws->ev[2], 0));
+      int rc = issue_levels(ws, cs, ws->s_update);
+      cudaEventRecord(ws->ev[3], ws->s_update);
+      cudaStreamWaitEvent(cs, ws->ev[3], 0);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(cs, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      TQ_CUDA(e);
+      e = cudaGraphInstantiate(&ws->graph, g, 0);
+      cudaGraphDestroy(g);
+      TQ_CUDA(e);
+    }
+    TQ_CUDA(cudaGraphLaunch(ws->graph, stream));
+    return 0;
+  }
+  // eager: fork/join the two internal streams around the caller's stream
+  TQ_CUDA(cudaEventRecord(ws->ev[2], stream));
+  TQ_CUDA(cudaStreamWaitEvent(ws->s_panel, ws->ev[2], 0));
+  TQ_CUDA(cudaStreamWaitEvent(ws->s_update, ws->ev[2], 0));
+  int rc = issue_levels(ws, ws->s_panel, ws->s_update);
+  if (rc) return rc;
+  TQ_CUDA(cudaEventRecord(ws->ev[2], ws->s_panel));
+  TQ_CUDA(cudaStreamWaitEvent(stream, ws->ev[2], 0));
+  TQ_CUDA(cudaEventRecord(ws->ev[3], ws->s_update));
+  TQ_CUDA(cudaStreamWaitEvent(stream, ws->ev[3], 0));
+  return 0;
+}
+
+}  // namespace tileqr
+
+using namespace tileqr;
+
+extern "C" {
+
+const char* tileqr_version(void) { return "tileqr 0.1 sm_100a (FP64 DMMA tile QR)"; }
+
+const char* tileqr_last_error(void) { return g_last_error.c_str(); }
+
+int tileqr_t_size(int64_t M, int64_t N, int NB, int IB, size_t* n_doubles) {
+  if (M < 0) return arg_error(1, "tileqr_t_size", "M < 0");
+  if (N < 0) return arg_error(2, "tileqr_t_size", "N < 0");
+  if (NB < 1 || NB > 512) return arg_error(3, "tileqr_t_size", "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(4, "tileqr_t_size", "IB must divide NB");
+  if (!n_doubles) return arg_error(5, "tileqr_t_size", "NULL output");
+  const int64_t MT = (M + NB - 1) / NB, NT = (N + NB - 1) / NB;
+  *n_doubles = (size_t)(MT * NT) * IB * NB;
+  return 0;
+}
+
+int tileqr_num_levels(int64_t MT, int64_t NT, int64_t* n_levels) {
+  if (MT < 0) return arg_error(1, "tileqr_num_levels", "MT < 0");
+  if (NT < 0) return arg_error(2, "tileqr_num_levels", "NT < 0");
+  if (!n_levels) return arg_error(3, "tileqr_num_levels", "NULL output");
+  *n_levels = num_levels(MT, NT);
+  return 0;
+}
+
+int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, double* T,
+                  int* d_info, tileqr_stream_t stream) {
+  static const char* fn = "tileqr_factor";
+  if (M < 0) return arg_error(1, fn, "M < 0");
+  if (N < 0) return arg_error(2, fn, "N < 0");
+  if (!A && M > 0 && N > 0) return arg_error(3, fn, "A is NULL");
+  if (lda < std::max<int64_t>(1, M)) return arg_error(4, fn, "lda < max(1,M)");
+  if (NB < 1 || NB > 512) return arg_error(5, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(6, fn, "IB must divide NB");
+  if (!T && M > 0 && N > 0) return arg_error(7, fn, "T is NULL");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_info) {
+    int rc = launch_zero_int(d_info, s);
+    if (rc) return rc;
+  }
+  if (M == 0 || N == 0) return 0;
+  int dev;
+  TQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  FactorWS* ws = nullptr;
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  if (it != g_ws.end()) {
+    ws = it->second.get();
+  } else {
+    int rc = create_ws(dev, M, N, NB, IB, &ws);
+    if (rc) return rc;
+  }
+  int rc = launch_layout_to_tiles(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, d_info, s);
+  if (rc) return rc;
+  if ((rc = run_levels(ws, s))) return rc;
+  if ((rc = launch_tiles_to_layout(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, s))) return rc;
+  TQ_CUDA(cudaMemcpyAsync(T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
+                          cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double* A, int64_t lda,
+                    const double* T, int NB, int IB, double* B, int64_t ldb,
+                    tileqr_stream_t stream) {
+  static const char* fn = "tileqr_apply_qt";
+  if (trans != 'T' && trans != 'N' && trans != 't' && trans != 'n')
+    return arg_error(1, fn, "trans not 'T' or 'N'");
+  if (M < 0) return arg_error(2, fn, "M < 0");
+  if (NRHS < 0) return arg_error(3, fn, "NRHS < 0");
+  if (K < 0) return arg_error(4, fn, "K < 0");
+  if (!A && M > 0 && K > 0) return arg_error(5, fn, "A is NULL");
+  if (lda < std::max<int64_t>(1, M)) return arg_error(6, fn, "lda < max(1,M)");
+  if (!T && M > 0 && K > 0) return arg_error(7, fn, "T is NULL");
+  if (NB < 1 || NB > 512) return arg_error(8, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(9, fn, "IB must divide NB");
+  if (!B && M > 0 && NRHS > 0) return arg_error(10, fn, "B is NULL");
+  if (ldb < std::max<int64_t>(1, M)) return arg_error(11, fn, "ldb < max(1,M)");
+  if (M == 0 || NRHS == 0 || K == 0) return 0;
+  const bool tr = (trans == 'T' || trans == 't');
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t MT = (M + NB - 1) / NB, KTt = (K + NB - 1) / NB, BT = (NRHS + NB - 1) / NB;
+  const int64_t KT = std::min(MT, KTt);
+  const size_t tile = (size_t)NB * NB;
+  double *Vt = nullptr, *Bt = nullptr;
+  void** dp = nullptr;
+  // per launch: LARFB tasks (k, n) n < BT; SSRFB tasks (k, m, n) n < BT
+  const int64_t nlaunch_s = KT * MT;  // upper bound
+  const size_t nptr = (size_t)KT * BT * 3 + (size_t)nlaunch_s * BT * 4;
+  TQ_CUDA(cudaMallocAsync(&Vt, tile * MT * KT * sizeof(double), s));
+  TQ_CUDA(cudaMallocAsync(&Bt, tile * MT * BT * sizeof(double), s));
+  TQ_CUDA(cudaMallocAsync(&dp, nptr * sizeof(void*), s));
+  int rc = launch_v_to_tiles(M, K, A, lda, NB, MT, KT, Vt, s);
+  if (!rc) rc = launch_layout_to_tiles(M, NRHS, B, ldb, NB, MT, BT, Bt, nullptr, s);
+  std::vector<void*> hp(nptr);
+  auto vt = [&](int64_t m, int64_t k) { return (void*)(Vt + (size_t)(m + k * MT) * tile); };
+  auto bt = [&](int64_t m, int64_t n) { return (void*)(Bt + (size_t)(m + n * MT) * tile); };
+  auto tt = [&](int64_t m, int64_t k) { return (void*)(T + (size_t)(m + k * MT) * IB * NB); };
+  struct L { bool larfb; size_t off; int64_t cnt; };
+  std::vector<L> seq;
+  size_t o = 0;
+  for (int64_t kk = 0; kk < KT; ++kk) {
+    const int64_t k = tr ? kk : KT - 1 - kk;
+    auto add_larfb = [&]() {
+      seq.push_back({true, o, BT});
+      for (int64_t n = 0; n < BT; ++n) {
+        hp[o + n] = vt(k, k);
+        hp[o + BT + n] = tt(k, k);
+        hp[o + 2 * BT + n] = bt(k, n);
+      }
+      o += 3 * BT;
+    };
+    if (tr) add_larfb();
+    for (int64_t mm = k + 1; mm < MT; ++mm) {
+      const int64_t m = tr ? mm : MT - 1 - (mm - (k + 1));
+      seq.push_back({false, o, BT});
+      for (int64_t n = 0; n < BT; ++n) {
+        hp[o + n] = vt(m, k);
+        hp[o + BT + n] = tt(m, k);
+        hp[o + 2 * BT + n] = bt(k, n);
+        hp[o + 3 * BT + n] = bt(m, n);
+      }
+      o += 4 * BT;
+    }
+    if (!tr) add_larfb();
+  }
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(dp, hp.data(), o * sizeof(void*), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync", __FILE__, __LINE__);
+  }
+  double** d = reinterpret_cast<double**>(dp);
+  for (const L& l : seq) {
+    if (rc) break;
+    if (l.larfb)
+      rc = launch_larfb(tr, NB, IB, (int)l.cnt, (const double* const*)(d + l.off),
+                        (const double* const*)(d + l.off + l.cnt), d + l.off + 2 * l.cnt, NB, s);
+    else
+      rc = launch_ssrfb(tr, NB, IB, (int)l.cnt, (const double* const*)(d + l.off),
+                        (const double* const*)(d + l.off + l.cnt), d + l.off + 2 * l.cnt,
+                        d + l.off + 3 * l.cnt, NB, s);
+  }
+  if (!rc) rc = launch_tiles_to_layout(M, NRHS, B, ldb, NB, MT, BT, Bt, s);
+  cudaFreeAsync(Vt, s);
+  cudaFreeAsync(Bt, s);
+  cudaFreeAsync(dp, s);
+  return rc;
+}
+
+static int check_batched(const char* fn, int NB, int IB, int batch) {
+  if (NB < 1 || NB > 512) return arg_error(1, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(2, fn, "IB must divide NB");
+  if (batch < 0) return arg_error(3, fn, "batch < 0");
+  return 0;
+}
+
+int tileqr_geqrt_batched(int NB, int IB, int batch, double* const* A, double* const* T,
+                         tileqr_stream_t stream) {
+  static const char* fn = "tileqr_geqrt_batched";
+  if (int rc = check_batched(fn, NB, IB, batch)) return rc;
+  if (batch == 0) return 0;
+  if (!A) return arg_error(4, fn, "A is NULL");
+  if (!T) return arg_error(5, fn, "T is NULL");
+  return launch_geqrt(NB, IB, batch, A, T, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tileqr_tsqrt_batched(int NB, int IB, int batch, double* const* R, double* const* A2,
+                         double* const* T, tileqr_stream_t stream) {
+  static const char* fn = "tileqr_tsqrt_batched";
+  if (int rc = check_batched(fn, NB, IB, batch)) return rc;
+  if (batch == 0) return 0;
+  if (!R) return arg_error(4, fn, "R is NULL");
+  if (!A2) return arg_error(5, fn, "A2 is NULL");
+  if (!T) return arg_error(6, fn, "T is NULL");
+  return launch_tsqrt(NB, IB, batch, R, A2, T, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tileqr_larfb_batched(char trans, int NB, int IB, int batch, const double* const* V,
+                         const double* const* T, double* const* C, int ncols,
+                         tileqr_stream_t stream) {
+  static const char* fn = "tileqr_larfb_batched";
+  if (trans != 'T' && trans != 'N' && trans != 't' && trans != 'n')
+    return arg_error(1, fn, "trans not 'T' or 'N'");
+  if (NB < 1 || NB > 512) return arg_error(2, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(3, fn, "IB must divide NB");
+  if (batch < 0) return arg_error(4, fn, "batch < 0");
+  if (batch == 0) return 0;
+  if (!V) return arg_error(5, fn, "V is NULL");
+  if (!T) return arg_error(6, fn, "T is NULL");
+  if (!C) return arg_error(7, fn, "C is NULL");
+  if (ncols < 1 || ncols > NB) return arg_error(8, fn, "ncols not in [1, NB]");
+  return launch_larfb(trans == 'T' || trans == 't', NB, IB, batch, V, T, C, ncols,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* const* V2,
+                         const double* const* T, double* const* C1, double* const* C2, int ncols,
+                         tileqr_stream_t stream) {
+  static const char* fn = "tileqr_ssrfb_batched";
+  if (trans != 'T' && trans != 'N' && trans != 't' && trans != 'n')
+    return arg_error(1, fn, "trans not 'T' or 'N'");
+  if (NB < 1 || NB > 512) return arg_error(2, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(3, fn, "IB must divide NB");
+  if (batch < 0) return arg_error(4, fn, "batch < 0");
+  if (batch == 0) return 0;
+  if (!V2) return arg_error(5, fn, "V2 is NULL");
+  if (!T) return arg_error(6, fn, "T is NULL");
+  if (!C1) return arg_error(7, fn, "C1 is NULL");
+  if (!C2) return arg_error(8, fn, "C2 is NULL");
+  if (ncols < 1 || ncols > NB) return arg_error(9, fn, "ncols not in [1, NB]");
+  return launch_ssrfb(trans == 'T' || trans == 't', NB, IB, batch, V2, T, C1, C2, ncols,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tileqr_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t seed,
+                       uint64_t offset, tileqr_stream_t stream) {
+  static const char* fn = "tileqr_rng_uniform";
+  if (M < 0) return arg_error(1, fn, "M < 0");
+  if (N < 0) return arg_error(2, fn, "N < 0");
+  if (!A && M > 0 && N > 0) return arg_error(3, fn, "A is NULL");
+  if (lda < std::max<int64_t>(1, M)) return arg_error(4, fn, "lda < max(1,M)");
+  return launch_rng_uniform(M, N, A, lda, seed, offset, reinterpret_cast<cudaStream_t>(stream));
+}
+
+const char* tileqr_ssrfb_impl(int NB, int IB) { return ssrfb_impl_name(NB, IB); }
+
+void tileqr_finalize(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_ws.clear();
+}
+
+}  // extern "C"

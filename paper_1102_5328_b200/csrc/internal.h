@@ -1,0 +1,62 @@
+// internal.h -- shared declarations of libtileqr's CUDA kernels and host runtime.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md "Boundary").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/tileqr.h"
+
+namespace tileqr {
+
+// ---- error plumbing (api.cu) --------------------------------------------
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define TQ_CUDA(call)                                                         \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) return ::tileqr::cuda_fail(e_, #call, __FILE__, __LINE__); \
+  } while (0)
+#define TQ_LAUNCH_CHECK()                                                     \
+  do {                                                                        \
+    cudaError_t e_ = cudaGetLastError();                                      \
+    if (e_ != cudaSuccess) return ::tileqr::cuda_fail(e_, "kernel launch", __FILE__, __LINE__); \
+  } while (0)
+
+// ---- argument validation shared by entry points ---------------------------
+inline bool valid_nb_ib(int NB, int IB) {
+  return NB >= 1 && NB <= 512 && IB >= 1 && IB <= NB && NB % IB == 0;
+}
+
+// ---- layout / utility kernels (kernels_layout.cu) --------------------------
+// A (M x N, lda) -> padded tile buffer (MT*NT tiles of NB*NB, tile (m,n) at
+// (m + n*MT)*NB*NB); sets *d_info = 1 when A holds a non-finite value.
+int launch_layout_to_tiles(int64_t M, int64_t N, const double* A, int64_t lda, int NB, int64_t MT,
+                           int64_t NT, double* tiles, int* d_info, cudaStream_t s);
+int launch_tiles_to_layout(int64_t M, int64_t N, double* A, int64_t lda, int NB, int64_t MT,
+                           int64_t NT, const double* tiles, cudaStream_t s);
+// Copy the V part of A (M x K) into a tile buffer (rows >= M zero, columns >= K zero).
+int launch_v_to_tiles(int64_t M, int64_t K, const double* A, int64_t lda, int NB, int64_t MT,
+                      int64_t KT, double* tiles, cudaStream_t s);
+int launch_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t seed, uint64_t offset,
+                       cudaStream_t s);
+int launch_zero_int(int* p, cudaStream_t s);
+
+// ---- tile kernels ---------------------------------------------------------
+// All take device arrays of device pointers (tiles NB x NB, ld NB; T IB x NB, ld IB).
+int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s);
+int launch_tsqrt(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
+                 cudaStream_t s);
+int launch_larfb(bool trans, int NB, int IB, int batch, const double* const* V,
+                 const double* const* T, double* const* C, int ncols, cudaStream_t s);
+int launch_ssrfb(bool trans, int NB, int IB, int batch, const double* const* V2,
+                 const double* const* T, double* const* C1, double* const* C2, int ncols,
+                 cudaStream_t s);
+
+// Which SSRFB implementation a (NB, IB) pair uses ("dmma" or "simt").
+const char* ssrfb_impl_name(int NB, int IB);
+
+}  // namespace tileqr

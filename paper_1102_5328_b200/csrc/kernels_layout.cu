@@ -1,0 +1,172 @@
+// kernels_layout.cu -- HBM-bound data movement of the tile QR (SURVEY §8(a)
+// rows a1/a7): LAPACK column-major <-> padded tile layout, the non-finite
+// flag, and the device copy of the synthetic input generator.
+//
+// Tile layout ("split the initial matrix ... into NT x NT
+// smaller square pieces of order NB, called tiles"): tile (m,n) is a
+// contiguous NB x NB column-major block at offset (m + n*MT)*NB*NB.  A column
+// segment of NB rows is contiguous in BOTH layouts, so each warp moves whole
+// 256-B runs: one thread per element pair, grid-stride, 16-B accesses on the
+// tile side when NB is even.
+#include <math.h>
+
+#include "internal.h"
+
+namespace tileqr {
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t work) {
+  int64_t blocks = (work + kThreads - 1) / kThreads;
+  // 148 SMs x 8 resident 256-thread CTAs; grid-stride beyond that.
+  const int64_t cap = 148 * 8 * 4;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+// Padded value of element (i, j) of the (MT*NB) x (NT*NB) matrix
+// (reading R5: rows >= M are 0; a padded column j >= N is e_j when
+// M <= j < MT*NB, else 0).
+__device__ __forceinline__ double padded_value(int64_t i, int64_t j, int64_t M, int64_t N,
+                                               const double* __restrict__ A, int64_t lda,
+                                               int* bad) {
+  if (i < M && j < N) {
+    double v = __ldg(A + i + j * lda);
+    if (!isfinite(v)) *bad = 1;
+    return v;
+  }
+  return (j >= N && i == j && j >= M) ? 1.0 : 0.0;
+}
+
+__global__ void __launch_bounds__(kThreads)
+layout_to_tiles_kernel(int64_t M, int64_t N, const double* __restrict__ A, int64_t lda, int NB,
+                       int64_t MT, int64_t NT, double* __restrict__ tiles, int* d_info) {
+  // work item = (global column j, tile row m, row pair within the tile)
+  const int64_t half = (NB + 1) / 2;
+  const int64_t ncols = NT * NB;
+  const int64_t per_col = MT * half;
+  const int64_t total = ncols * per_col;
+  int bad = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = w / per_col;
+    const int64_t rem = w - j * per_col;
+    const int64_t m = rem / half;
+    const int64_t il = 2 * (rem - m * half);
+    const int64_t n = j / NB, jl = j - n * NB;
+    const int64_t i = m * NB + il;
+    double* dst = tiles + (m + n * MT) * (int64_t)NB * NB + il + jl * NB;
+    double v0 = padded_value(i, j, M, N, A, lda, &bad);
+    if (il + 1 < NB) {
+      double v1 = padded_value(i + 1, j, M, N, A, lda, &bad);
+      if ((NB & 1) == 0) {
+        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+      } else {
+        dst[0] = v0;
+        dst[1] = v1;
+      }
+    } else {
+      dst[0] = v0;
+    }
+  }
+  if (bad && d_info) *d_info = 1;  // benign race: every writer stores 1
+}
+
+__global__ void __launch_bounds__(kThreads)
+tiles_to_layout_kernel(int64_t M, int64_t N, double* __restrict__ A, int64_t lda, int NB,
+                       int64_t MT, const double* __restrict__ tiles) {
+  const int64_t total = M * N;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = w / M, i = w - j * M;
+    const int64_t m = i / NB, il = i - m * NB, n = j / NB, jl = j - n * NB;
+    A[i + j * lda] = tiles[(m + n * MT) * (int64_t)NB * NB + il + jl * NB];
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+v_to_tiles_kernel(int64_t M, int64_t K, const double* __restrict__ A, int64_t lda, int NB,
+                  int64_t MT, int64_t KT, double* __restrict__ tiles) {
+  const int64_t rows = MT * NB, total = rows * KT * NB;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = w / rows, i = w - j * rows;
+    const int64_t m = i / NB, il = i - m * NB, n = j / NB, jl = j - n * NB;
+    tiles[(m + n * MT) * (int64_t)NB * NB + il + jl * NB] =
+        (i < M && j < K) ? A[i + j * lda] : 0.0;
+  }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void __launch_bounds__(kThreads)
+rng_uniform_kernel(int64_t M, int64_t N, double* __restrict__ A, int64_t lda, uint64_t key,
+                   uint64_t offset) {
+  const int64_t total = M * N;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = w / M, i = w - j * M;
+    const uint64_t bits = splitmix64(key + offset + (uint64_t)w) >> 11;
+    A[i + j * lda] = (double)bits * 0x1.0p-53 - 0.5;
+  }
+}
+
+__global__ void zero_int_kernel(int* p) { *p = 0; }
+
+uint64_t host_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+}  // namespace
+
+int launch_layout_to_tiles(int64_t M, int64_t N, const double* A, int64_t lda, int NB, int64_t MT,
+                           int64_t NT, double* tiles, int* d_info, cudaStream_t s) {
+  const int64_t work = NT * NB * MT * ((NB + 1) / 2);
+  layout_to_tiles_kernel<<<grid_for(work), kThreads, 0, s>>>(M, N, A, lda, NB, MT, NT, tiles,
+                                                              d_info);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_tiles_to_layout(int64_t M, int64_t N, double* A, int64_t lda, int NB, int64_t MT,
+                           int64_t NT, const double* tiles, cudaStream_t s) {
+  (void)NT;
+  tiles_to_layout_kernel<<<grid_for(M * N), kThreads, 0, s>>>(M, N, A, lda, NB, MT, tiles);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_v_to_tiles(int64_t M, int64_t K, const double* A, int64_t lda, int NB, int64_t MT,
+                      int64_t KT, double* tiles, cudaStream_t s) {
+  v_to_tiles_kernel<<<grid_for(MT * NB * KT * NB), kThreads, 0, s>>>(M, K, A, lda, NB, MT, KT,
+                                                                      tiles);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t seed,
+                       uint64_t offset, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return 0;
+  rng_uniform_kernel<<<grid_for(M * N), kThreads, 0, s>>>(M, N, A, lda, host_splitmix64(seed),
+                                                          offset);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_zero_int(int* p, cudaStream_t s) {
+  zero_int_kernel<<<1, 1, 0, s>>>(p);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace tileqr

@@ -1,0 +1,306 @@
+// kernels_panel.cu -- the panel kernels of the tile QR: GEQRT (QR of a
+// diagonal tile) and TSQRT (QR of a triangle stacked on a square tile)
+// ("DGEQRT and DTSQRT serial kernels").
+//
+// One CTA per task (a batch of independent tasks per launch).  For each inner
+// panel p of IB columns (inner blocking):
+//   1. the panel columns are staged in shared memory (ld = NB+1, odd, so the
+//      column-strided accesses of one warp hit distinct banks) when they fit,
+//      else they are addressed in global memory (same code, generic pointer);
+//   2. columns are factored one by one.  ONE reduction pass per column
+//      computes sigma = ||x2||^2 and every dot d_c = x2 . P(:,c) of the
+//      remaining panel columns at once (warp-shuffle trees), because
+//      v2 = x2 / (alpha - beta) makes w_c = R(j,c) + d_c/(alpha - beta);
+//      the rank-1 panel update follows: 2 CTA barriers per column;
+//   3. T_p (IB x IB upper triangular, R3) is built by the
+//      forward-columnwise recurrence T[0:i,i] = -tau_i T[0:i,0:i] (V^T v_i);
+//   4. Q_p^T is applied to the trailing columns of the tile (pair).
+// Reflector rule: DESIGN.md reading R1 (LAPACK larfg sign convention, no
+// rescaling loop).  TSQRT never writes the strict lower part of R, which the
+// LARFB of the same DAG level reads.
+#include <math.h>
+
+#include "internal.h"
+
+namespace tileqr {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr size_t kSmemBudget = 200 * 1024;
+
+struct Mat {
+  double* p;
+  int ld;
+  __device__ __forceinline__ double& operator()(int r, int c) const {
+    return p[r + (size_t)c * ld];
+  }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+struct PanelSmem {
+  double* tau;  // [IB]
+  double* dots; // [IB]
+  double* rj;   // [IB]  row j of R restricted to the panel columns
+  double* G;    // [IB*IB] Gram matrix of the panel's reflectors (IB <= 64) or [IB] column
+  double* W;    // [IB*CW] trailing-update workspace
+  double* P;    // [(NB+1)*IB] staged panel, or nullptr
+};
+
+__host__ __device__ inline int trailing_cw(int IB) {
+  int cw = 4096 / IB;
+  if (cw > 64) cw = 64;
+  if (cw < 1) cw = 1;
+  return cw;
+}
+
+inline size_t panel_smem_bytes(int NB, int IB, bool stage) {
+  size_t g = (IB <= 64) ? (size_t)IB * IB : (size_t)IB;
+  size_t n = 3 * (size_t)IB + g + (size_t)IB * trailing_cw(IB);
+  if (stage) n += (size_t)(NB + 1) * IB;
+  return n * sizeof(double);
+}
+
+inline bool panel_stage(int NB, int IB) { return panel_smem_bytes(NB, IB, true) <= kSmemBudget; }
+
+// TS = true: TSQRT on (R = Rp[b] upper triangle, B = Bp[b]); false: GEQRT on A = Rp[b].
+template <bool TS>
+__global__ void __launch_bounds__(kThreads)
+panel_kernel(int NB, int IB, double* const* Rp, double* const* Bp, double* const* Tp, int stage) {
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* const Rg = Rp[blockIdx.x];
+  double* const Bg = TS ? Bp[blockIdx.x] : Rg;
+  double* const Tg = Tp[blockIdx.x];
+  const Mat R{Rg, NB};
+  const Mat B{Bg, NB};
+  const Mat Tm{Tg, IB};
+  const int CW = trailing_cw(IB);
+  const bool fullG = IB <= 64;
+
+  PanelSmem s;
+  s.tau = smem;
+  s.dots = s.tau + IB;
+  s.rj = s.dots + IB;
+  s.G = s.rj + IB;
+  s.W = s.G + (fullG ? IB * IB : IB);
+  s.P = stage ? s.W + IB * CW : nullptr;
+
+  for (int c0 = 0; c0 < NB; c0 += IB) {
+    // P(r, c) = panel column c0 + c, rows 0..NB-1 (B for TSQRT, A for GEQRT)
+    Mat P = stage ? Mat{s.P, NB + 1} : Mat{&B(0, c0), NB};
+    if (stage) {
+      for (int idx = tid; idx < NB * IB; idx += kThreads) {
+        const int c = idx / NB, r = idx - c * NB;
+        P(r, c) = B(r, c0 + c);
+      }
+      __syncthreads();
+    }
+
+    // ---- 2. factor the panel column by column --------------------------
+    for (int jj = 0; jj < IB; ++jj) {
+      const int j = c0 + jj;
+      // rows of the reflector tail: TSQRT all NB rows of B; GEQRT rows j+1..NB-1
+      const int r0 = TS ? 0 : j + 1;
+      // (a) one pass: dots[c] = sum_r P(r,jj) P(r,c), c = jj..IB-1; rj[c] = R(j, c0+c)
+      for (int c = jj + warp; c < IB; c += kWarps) {
+        double acc = 0.0;
+        for (int r = r0 + lane; r < NB; r += 32) acc = fma(P(r, jj), P(r, c), acc);
+        acc = warp_sum(acc);
+        if (lane == 0) {
+          s.dots[c] = acc;
+          s.rj[c] = TS ? R(j, c0 + c) : P(j, c);
+        }
+      }
+      __syncthreads();
+      // (b) reflector (every thread computes the same scalars)
+      const double sigma = s.dots[jj];
+      const double alpha = s.rj[jj];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (sigma != 0.0) {
+        const double nrm = sqrt(alpha * alpha + sigma);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      // (c) rank-1 update of the remaining panel columns, then scale v2
+      if (sigma != 0.0) {
+        for (int r = r0 + tid; r < NB; r += kThreads) {
+          const double v = P(r, jj) * scal;
+          for (int c = jj + 1; c < IB; ++c) {
+            const double w = fma(scal, s.dots[c], s.rj[c]);
+            P(r, c) = fma(-tau * v, w, P(r, c));
+          }
+          P(r, jj) = v;
+        }
+      }
+      // row j of R (TSQRT: global R; GEQRT: row j of the staged panel)
+      if (tid > jj && tid < IB && sigma != 0.0) {
+        const double w = fma(scal, s.dots[tid], s.rj[tid]);
+        if (TS) R(j, c0 + tid) = s.rj[tid] - tau * w;
+        else P(j, tid) = s.rj[tid] - tau * w;
+      }
+      if (tid == 0) {
+        if (TS) R(j, j) = beta;
+        else P(j, jj) = beta;
+        s.tau[jj] = tau;
+      }
+      __syncthreads();
+    }
+
+    // ---- write the factored panel back ------------------------------------
+    if (stage) {
+      for (int idx = tid; idx < NB * IB; idx += kThreads) {
+        const int c = idx / NB, r = idx - c * NB;
+        B(r, c0 + c) = P(r, c);
+      }
+    }
+
+    // ---- 3. T_p -----------------------------------------------------------
+    // z_l(i) = v_l . v_i.  TSQRT: the top parts e_j are distinct unit
+    // vectors, so z = V2_l . V2_i.  GEQRT: v_l(c0+i) * 1 + sum_{r > c0+i}.
+    auto vdot = [&](int l, int i) -> double {  // warp-cooperative, l < i
+      double acc = 0.0;
+      const int rs = TS ? 0 : c0 + i + 1;
+      for (int r = rs + lane; r < NB; r += 32) acc = fma(P(r, l), P(r, i), acc);
+      acc = warp_sum(acc);
+      if (!TS) acc += P(c0 + i, l);
+      return acc;
+    };
+    Mat Tp{&Tm(0, c0), IB};
+    if (fullG) {
+      for (int idx = warp; idx < IB * IB; idx += kWarps) {
+        const int i = idx / IB, l = idx - i * IB;
+        if (l < i) {
+          const double z = vdot(l, i);
+          if (lane == 0) s.G[l + i * IB] = z;
+        }
+      }
+      __syncthreads();
+      // thread r owns row r of T_p: T(r,i) = -tau_i sum_{l=r}^{i-1} T(r,l) z_l(i)
+      if (tid < IB) {
+        const int r = tid;
+        for (int i = 0; i < IB; ++i) {
+          double v;
+          if (i < r) {
+            v = 0.0;
+          } else if (i == r) {
+            v = s.tau[i];
+          } else {
+            double acc = 0.0;
+            for (int l = r; l < i; ++l) acc = fma(Tp(r, l), s.G[l + i * IB], acc);
+            v = -s.tau[i] * acc;
+          }
+          Tp(r, i) = v;
+        }
+      }
+    } else {
+      for (int i = 0; i < IB; ++i) {
+        for (int l = warp; l < i; l += kWarps) {
+          const double z = vdot(l, i);
+          if (lane == 0) s.G[l] = z;
+        }
+        __syncthreads();
+        for (int r = tid; r < IB; r += kThreads) {
+          double v;
+          if (i < r) {
+            v = 0.0;
+          } else if (i == r) {
+            v = s.tau[i];
+          } else {
+            double acc = 0.0;
+            for (int l = r; l < i; ++l) acc = fma(Tp(r, l), s.G[l], acc);
+            v = -s.tau[i] * acc;
+          }
+          Tp(r, i) = v;
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+
+    // ---- 4. trailing columns c >= c0+IB: W = V^T C; W = T^T W; C -= V W ---
+    for (int cb = c0 + IB; cb < NB; cb += CW) {
+      const int nc = min(CW, NB - cb);
+      for (int idx = tid; idx < IB * nc; idx += kThreads) {
+        const int cc = idx / IB, i = idx - cc * IB;
+        const int c = cb + cc;
+        double acc;
+        if (TS) {
+          acc = R(c0 + i, c);
+          for (int r = 0; r < NB; ++r) acc = fma(P(r, i), B(r, c), acc);
+        } else {
+          acc = B(c0 + i, c);
+          for (int r = c0 + i + 1; r < NB; ++r) acc = fma(P(r, i), B(r, c), acc);
+        }
+        s.W[i + cc * IB] = acc;
+      }
+      __syncthreads();
+      for (int cc = tid; cc < nc; cc += kThreads) {  // W(:,cc) <- T_p^T W(:,cc), bottom-up
+        double* w = s.W + cc * IB;
+        for (int i = IB - 1; i >= 0; --i) {
+          double acc = 0.0;
+          for (int l = 0; l <= i; ++l) acc = fma(Tp(l, i), w[l], acc);
+          w[i] = acc;
+        }
+      }
+      __syncthreads();
+      if (TS) {
+        for (int idx = tid; idx < IB * nc; idx += kThreads) {
+          const int cc = idx / IB, i = idx - cc * IB;
+          R(c0 + i, cb + cc) -= s.W[i + cc * IB];
+        }
+        for (int idx = tid; idx < NB * nc; idx += kThreads) {
+          const int cc = idx / NB, r = idx - cc * NB;
+          double acc = 0.0;
+          for (int i = 0; i < IB; ++i) acc = fma(P(r, i), s.W[i + cc * IB], acc);
+          B(r, cb + cc) -= acc;
+        }
+      } else {
+        for (int idx = tid; idx < (NB - c0) * nc; idx += kThreads) {
+          const int cc = idx / (NB - c0), r = c0 + (idx - cc * (NB - c0));
+          // V(r,i) = P(r,i) for r > c0+i, 1 for r == c0+i, 0 above
+          const int d = r - c0, iend = min(d, IB);
+          double acc = 0.0;
+          for (int i = 0; i < iend; ++i) acc = fma(P(r, i), s.W[i + cc * IB], acc);
+          if (d < IB) acc += s.W[d + cc * IB];
+          B(r, cb + cc) -= acc;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <bool TS>
+int launch_panel(int NB, int IB, int batch, double* const* R, double* const* B, double* const* T,
+                 cudaStream_t s) {
+  if (batch <= 0) return 0;
+  const bool stage = panel_stage(NB, IB);
+  const size_t bytes = panel_smem_bytes(NB, IB, stage);
+  auto kern = panel_kernel<TS>;
+  if (bytes > 48 * 1024) {
+    TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  }
+  kern<<<batch, kThreads, bytes, s>>>(NB, IB, R, B, T, stage ? 1 : 0);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace
+
+int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s) {
+  return launch_panel<false>(NB, IB, batch, A, nullptr, T, s);
+}
+
+int launch_tsqrt(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
+                 cudaStream_t s) {
+  return launch_panel<true>(NB, IB, batch, R, A2, T, s);
+}
+
+}  // namespace tileqr

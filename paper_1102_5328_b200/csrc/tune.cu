@@ -1,0 +1,346 @@
+// tune.cu -- tileqr_tune: the paper's two-step empirical tuning of (NB, IB)
+// on the GPU.
+//
+//   Step 1: benchmark the dominant kernel, SSRFB, for every
+//     (NB, IB) of the grid: one warm-up then 50 back-to-back batched launches
+//     on the same buffers ("No Flush"), timed at once with
+//     CUDA events; rate = 50 * batch * 4 NB^3 / t (nominal flops).
+//   Pre-selection: Property 1 (orthogonal pruning), upper
+//     convex hull (Property 2 / Heuristic 0), Heuristic 1
+//     (steepness) or 2 (iso-segments), cap 8.
+//   Step 2: factorizations on a ladder of matrix orders
+//     ascending to N, 6 runs per candidate (median), P =
+//     4/3 N^3 / t; after each rung Property 3 ("prune as you go") drops NB2
+//     when some NB1 > NB2 is strictly faster.
+// Readings of the unclear points (tie rules, first hull point, iso-segment
+// count) are DESIGN.md R13/R14.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace tileqr {
+namespace {
+
+struct Pt {
+  int nb, ib;
+  double g;
+};
+
+std::vector<Pt> orthogonal_prune(const std::vector<Pt>& in) {
+  std::map<int, Pt> best;
+  for (const Pt& p : in) {
+    auto it = best.find(p.nb);
+    if (it == best.end() || p.g > it->second.g || (p.g == it->second.g && p.ib > it->second.ib))
+      best[p.nb] = p;
+  }
+  std::vector<Pt> out;
+  for (auto& kv : best) out.push_back(kv.second);
+  return out;  // sorted by nb
+}
+
+// upper hull, strictly decreasing slopes (collinear interior points dropped)
+std::vector<Pt> upper_hull(const std::vector<Pt>& pts) {
+  std::vector<Pt> h;
+  for (const Pt& q : pts) {
+    while (h.size() >= 2) {
+      const Pt& o = h[h.size() - 2];
+      const Pt& a = h[h.size() - 1];
+      const long double cross = (long double)(a.nb - o.nb) * ((long double)q.g - o.g) -
+                                ((long double)a.g - o.g) * (long double)(q.nb - o.nb);
+      if (cross >= 0) h.pop_back();
+      else break;
+    }
+    h.push_back(q);
+  }
+  return h;
+}
+
+long double slope_in(const std::vector<Pt>& h, size_t i) {
+  return ((long double)h[i].g - h[i - 1].g) / (long double)(h[i].nb - h[i - 1].nb);
+}
+
+std::vector<Pt> heuristic1(const std::vector<Pt>& h, int cap) {
+  if (h.size() <= 1) return h;
+  std::vector<size_t> idx;
+  for (size_t i = 1; i < h.size(); ++i) idx.push_back(i);
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) {
+    const long double sx = slope_in(h, x), sy = slope_in(h, y);
+    if (sx != sy) return sx > sy;
+    return h[x].nb < h[y].nb;
+  });
+  if ((int)idx.size() > cap) idx.resize(cap);
+  std::sort(idx.begin(), idx.end());
+  std::vector<Pt> out;
+  for (size_t i : idx) out.push_back(h[i]);
+  return out;
+}
+
+std::vector<Pt> heuristic2(const std::vector<Pt>& h, int cap) {
+  if (h.size() <= 1) return h;
+  const long double x0 = h.front().nb, x1 = h.back().nb;
+  const long double width = (x1 - x0) / cap;
+  std::map<int, size_t> best;  // segment -> hull index
+  for (size_t i = 1; i < h.size(); ++i) {
+    int seg = (h[i].nb == h.back().nb) ? cap - 1 : (int)((h[i].nb - x0) / width);
+    if (seg >= cap) seg = cap - 1;
+    auto it = best.find(seg);
+    if (it == best.end() || slope_in(h, i) > slope_in(h, it->second)) best[seg] = i;
+  }
+  std::vector<size_t> idx;
+  for (auto& kv : best) idx.push_back(kv.second);
+  std::sort(idx.begin(), idx.end());
+  std::vector<Pt> out;
+  for (size_t i : idx) out.push_back(h[i]);
+  return out;
+}
+
+std::vector<Pt> preselect(const std::vector<Pt>& samples, int heuristic, int cap) {
+  std::vector<Pt> hull = upper_hull(orthogonal_prune(samples));
+  if (heuristic == 1) return heuristic1(hull, cap);
+  if (heuristic == 2) return heuristic2(hull, cap);
+  return hull;
+}
+
+std::string pts_json(const std::vector<Pt>& v) {
+  std::string s = "[";
+  char buf[128];
+  for (size_t i = 0; i < v.size(); ++i) {
+    snprintf(buf, sizeof buf, "%s{\"nb\": %d, \"ib\": %d, \"gflops\": %.6f}", i ? ", " : "", v[i].nb,
+             v[i].ib, v[i].g);
+    s += buf;
+  }
+  return s + "]";
+}
+
+#define TQ_TRY(call)                 \
+  do {                               \
+    int rc_ = (call);                \
+    if (rc_) { cleanup(); return rc_; } \
+  } while (0)
+
+}  // namespace
+}  // namespace tileqr
+
+using namespace tileqr;
+
+extern "C" {
+
+int tileqr_preselect(int n, const int* h_nb, const int* h_ib, const double* h_gflops, int heuristic,
+                     int cap, int* h_out_nb, int* h_out_ib, double* h_out_gflops, int* n_out) {
+  if (n < 1) { set_error("tileqr_preselect: empty dataset"); return -1; }
+  if (!h_nb) return -2;
+  if (!h_ib) return -3;
+  if (!h_gflops) return -4;
+  if (heuristic < 0 || heuristic > 2) return -5;
+  if (cap < 1) return -6;
+  if (!h_out_nb || !h_out_ib || !h_out_gflops || !n_out) return -7;
+  std::vector<Pt> s;
+  for (int i = 0; i < n; ++i) s.push_back({h_nb[i], h_ib[i], h_gflops[i]});
+  std::vector<Pt> out = preselect(s, heuristic, cap);
+  for (size_t i = 0; i < out.size(); ++i) {
+    h_out_nb[i] = out[i].nb;
+    h_out_ib[i] = out[i].ib;
+    h_out_gflops[i] = out[i].g;
+  }
+  *n_out = (int)out.size();
+  return 0;
+}
+
+int tileqr_payg_prune(int n, const int* h_nb, const double* h_gflops, int* h_keep) {
+  if (n < 0) return -1;
+  if (!h_nb && n) return -2;
+  if (!h_gflops && n) return -3;
+  if (!h_keep && n) return -4;
+  for (int i = 0; i < n; ++i) {
+    h_keep[i] = 1;
+    for (int j = 0; j < n; ++j)
+      if (h_nb[j] > h_nb[i] && h_gflops[j] > h_gflops[i]) h_keep[i] = 0;
+  }
+  return 0;
+}
+
+int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h_NB, int* h_IB,
+                const char* report_json_path) {
+  static const char* fn = "tileqr_tune";
+  char msg[256];
+  if (M < 1) { snprintf(msg, sizeof msg, "%s: M < 1", fn); set_error(msg); return -1; }
+  if (N < 1) { snprintf(msg, sizeof msg, "%s: N < 1", fn); set_error(msg); return -2; }
+  if (ngpus != 1) { snprintf(msg, sizeof msg, "%s: ngpus must be 1 (per-rank tuning)", fn); set_error(msg); return -3; }
+  if (heuristic < 0 || heuristic > 2) { set_error("tileqr_tune: heuristic not in {0,1,2}"); return -4; }
+  if (!h_NB) return -6;
+  if (!h_IB) return -7;
+
+  const char* e_batch = getenv("TILEQR_TUNE_BATCH");
+  const int batch = e_batch ? atoi(e_batch) : 4096;
+  const char* e_small = getenv("TILEQR_TUNE_SMALL_IB");
+  const int ib_min = (e_small && e_small[0] == '1') ? 1 : 8;
+  const char* e_reps = getenv("TILEQR_TUNE_REPS");
+  const int reps = e_reps ? atoi(e_reps) : 50;
+  const int nb_grid[] = {64, 96, 128, 160, 192, 224, 256};
+  const int nbmax = 256;
+
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  double* buf = nullptr;
+  double** ptrs = nullptr;
+  double* A0 = nullptr;
+  double* A = nullptr;
+  double* T = nullptr;
+  int* dinfo = nullptr;
+  auto cleanup = [&]() {
+    if (s) cudaStreamSynchronize(s);
+    cudaFree(buf); cudaFree(ptrs); cudaFree(A0); cudaFree(A); cudaFree(T); cudaFree(dinfo);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+  };
+  TQ_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+  TQ_TRY(cudaEventCreate(&e0) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+  TQ_TRY(cudaEventCreate(&e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+
+  // ---- Step 1: SSRFB sweep ---------------------------------------------------
+  const size_t tile_max = (size_t)nbmax * nbmax;
+  if (cudaMalloc(&buf, (size_t)batch * (4 * tile_max + tile_max) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ptrs, (size_t)batch * 5 * sizeof(double*)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("tileqr_tune: step-1 allocation failed");
+    cleanup();
+    return TILEQR_ERR_ALLOC;
+  }
+  std::vector<Pt> samples;
+  std::vector<double*> hp(5 * (size_t)batch);
+  for (int nb : nb_grid) {
+    const size_t tile = (size_t)nb * nb;
+    for (int i = 0; i < batch; ++i) {
+      double* base = buf + (size_t)i * 5 * tile;
+      hp[i] = base;                        // R (top)
+      hp[batch + i] = base + tile;         // V2 (TSQRT bottom)
+      hp[2 * batch + i] = base + 2 * tile; // C1
+      hp[3 * batch + i] = base + 3 * tile; // C2
+      hp[4 * batch + i] = base + 4 * tile; // T (IB x NB <= NB x NB)
+    }
+    TQ_TRY(cudaMemcpy(ptrs, hp.data(), hp.size() * sizeof(double*), cudaMemcpyHostToDevice) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+    TQ_TRY(launch_rng_uniform((int64_t)tile, (int64_t)batch * 5, buf, (int64_t)tile, 2, 0, s));
+    for (int ib = ib_min; ib <= nb; ++ib) {
+      if (nb % ib) continue;
+      // V2, T from a TSQRT of (top, bottom); fresh bottoms each time are not
+      // needed for timing: the reflector values only scale the data.
+      TQ_TRY(launch_tsqrt(nb, ib, batch, ptrs, ptrs + batch, ptrs + 4 * batch, s));
+      TQ_TRY(launch_ssrfb(true, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, ptrs + 2 * batch,
+                          ptrs + 3 * batch, nb, s));  // warm-up
+      TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+      for (int r = 0; r < reps; ++r)
+        TQ_TRY(launch_ssrfb(true, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, ptrs + 2 * batch,
+                            ptrs + 3 * batch, nb, s));
+      TQ_TRY(cudaEventRecord(e1, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+      TQ_TRY(cudaEventSynchronize(e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double g = (double)reps * batch * 4.0 * nb * nb * (double)nb / (ms * 1e-3) / 1e9;
+      samples.push_back({nb, ib, g});
+      // keep magnitudes bounded across the repeated in-place updates
+      TQ_TRY(launch_rng_uniform((int64_t)tile, (int64_t)batch * 5, buf, (int64_t)tile, 2, 0, s));
+    }
+  }
+  cudaFree(buf);
+  buf = nullptr;
+  std::vector<Pt> cand = preselect(samples, heuristic, 8);
+
+  // ---- Step 2: factorizations on a ladder ascending to N --------------------
+  std::vector<int64_t> ladder;
+  for (int64_t d : {4, 2, 1}) {
+    const int64_t n = std::max<int64_t>(64, N / d);
+    if (ladder.empty() || n > ladder.back()) ladder.push_back(n);
+  }
+  const double ratio = (double)M / (double)N;
+  std::string step2 = "[";
+  std::vector<Pt> alive = cand;
+  std::vector<Pt> last;
+  for (size_t li = 0; li < ladder.size(); ++li) {
+    const int64_t n = ladder[li];
+    const int64_t m = std::max<int64_t>(1, (int64_t)(ratio * n + 0.5));
+    cudaFree(A0); cudaFree(A); cudaFree(T); cudaFree(dinfo);
+    A0 = A = T = nullptr;
+    dinfo = nullptr;
+    size_t tn = 0;
+    tileqr_t_size(m, n, 8, 8, &tn);
+    size_t tmax = 0;
+    for (const Pt& p : alive) {
+      size_t t = 0;
+      tileqr_t_size(m, n, p.nb, p.ib, &t);
+      tmax = std::max(tmax, t);
+    }
+    if (cudaMalloc(&A0, (size_t)m * n * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&A, (size_t)m * n * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&T, std::max<size_t>(tmax, 1) * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&dinfo, sizeof(int)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("tileqr_tune: step-2 allocation failed");
+      cleanup();
+      return TILEQR_ERR_ALLOC;
+    }
+    TQ_TRY(launch_rng_uniform(m, n, A0, m, 3, 0, s));
+    std::vector<Pt> res;
+    for (const Pt& p : alive) {
+      std::vector<float> times;
+      for (int r = 0; r < 7; ++r) {  // 1 warm-up + 6 timed runs
+        TQ_TRY(cudaMemcpyAsync(A, A0, (size_t)m * n * sizeof(double), cudaMemcpyDeviceToDevice, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        TQ_TRY(tileqr_factor(m, n, A, m, p.nb, p.ib, T, dinfo, (tileqr_stream_t)s));
+        TQ_TRY(cudaEventRecord(e1, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        TQ_TRY(cudaEventSynchronize(e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0) times.push_back(ms);
+      }
+      std::sort(times.begin(), times.end());
+      const double med = 0.5 * (times[2] + times[3]);
+      const double flops = (m >= n) ? 2.0 * m * (double)n * n - 2.0 * (double)n * n * n / 3.0
+                                    : 2.0 * n * (double)m * m - 2.0 * (double)m * m * m / 3.0;
+      const double g = flops / (med * 1e-3) / 1e9;
+      res.push_back({p.nb, p.ib, g});
+      char b[192];
+      snprintf(b, sizeof b, "%s{\"n\": %lld, \"nb\": %d, \"ib\": %d, \"median_ms\": %.4f, \"gflops\": %.3f}",
+               step2.size() > 1 ? ", " : "", (long long)n, p.nb, p.ib, med, g);
+      step2 += b;
+    }
+    last = res;
+    if (payg) {  // Property 3
+      std::vector<Pt> keep;
+      for (const Pt& q : res) {
+        bool drop = false;
+        for (const Pt& o : res)
+          if (o.nb > q.nb && o.g > q.g) drop = true;
+        if (!drop) keep.push_back(q);
+      }
+      alive = keep;
+    }
+  }
+  step2 += "]";
+  Pt best = last.front();
+  for (const Pt& p : last)
+    if (p.g > best.g) best = p;
+  *h_NB = best.nb;
+  *h_IB = best.ib;
+  if (report_json_path) {
+    FILE* f = fopen(report_json_path, "w");
+    if (f) {
+      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d,\n",
+              (long long)M, (long long)N, heuristic, payg, batch, reps);
+      fprintf(f, " \"step1\": %s,\n \"candidates\": %s,\n \"step2\": %s,\n \"best\": {\"nb\": %d, \"ib\": %d, \"gflops\": %.3f}}\n",
+              pts_json(samples).c_str(), pts_json(cand).c_str(), step2.c_str(), best.nb, best.ib, best.g);
+      fclose(f);
+    }
+  }
+  cleanup();
+  return 0;
+}
+
+}  // extern "C"

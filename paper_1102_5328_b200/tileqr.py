@@ -1,0 +1,226 @@
+"""Thin ctypes binding of libtileqr.so (include/tileqr.h).
+
+Argument marshalling only: every step of the factorization runs in the CUDA
+kernels of libtileqr.so.  PyTorch supplies device memory, streams and process
+groups.  There is no CPU fallback: if the library is missing, importing this
+module raises.
+
+Names follow the C ABI (tileqr_factor -> factor, ...).  Matrices are FP64
+column-major; torch tensors are passed as Fortran-ordered views, i.e. a
+torch tensor ``A`` of shape (N, M) row-major IS the column-major M x N matrix
+``A.T``.  The helpers :func:`colmajor_empty` / :func:`to_colmajor` /
+:func:`from_colmajor` do that bookkeeping.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libtileqr.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"libtileqr.so not built ({_LIB_PATH}); run `python -m paper_1102_5328_b200.build`")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+
+_i, _i64, _u64, _c, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_char, ctypes.c_double
+_p, _sz = ctypes.c_void_p, ctypes.c_size_t
+_PI = ctypes.POINTER(ctypes.c_int)
+_PD = ctypes.POINTER(ctypes.c_double)
+
+_SIGS = {
+    "tileqr_version": ([], ctypes.c_char_p),
+    "tileqr_last_error": ([], ctypes.c_char_p),
+    "tileqr_t_size": ([_i64, _i64, _i, _i, ctypes.POINTER(_sz)], _i),
+    "tileqr_factor": ([_i64, _i64, _p, _i64, _i, _i, _p, _p, _p], _i),
+    "tileqr_apply_qt": ([_c, _i64, _i64, _i64, _p, _i64, _p, _i, _i, _p, _i64, _p], _i),
+    "tileqr_geqrt_batched": ([_i, _i, _i, _p, _p, _p], _i),
+    "tileqr_tsqrt_batched": ([_i, _i, _i, _p, _p, _p, _p], _i),
+    "tileqr_larfb_batched": ([_c, _i, _i, _i, _p, _p, _p, _i, _p], _i),
+    "tileqr_ssrfb_batched": ([_c, _i, _i, _i, _p, _p, _p, _p, _i, _p], _i),
+    "tileqr_tune": ([_i64, _i64, _i, _i, _i, _PI, _PI, ctypes.c_char_p], _i),
+    "tileqr_preselect": ([_i, _PI, _PI, _PD, _i, _i, _PI, _PI, _PD, _PI], _i),
+    "tileqr_payg_prune": ([_i, _PI, _PD, _PI], _i),
+    "tileqr_num_levels": ([_i64, _i64, ctypes.POINTER(_i64)], _i),
+    "tileqr_dist_init": ([_i, _i, _p, _i], _i),
+    "tileqr_dist_unique_id": ([_p], _i),
+    "tileqr_dist_local_cols": ([_i64, _i, _PI], _i),
+    "tileqr_dist_fill_uniform": ([_i64, _i, _p, _u64, _p], _i),
+    "tileqr_dist_factor": ([_i64, _p, _i, _i, _p, _p, _p], _i),
+    "tileqr_dist_finalize": ([], None),
+    "tileqr_rng_uniform": ([_i64, _i64, _p, _i64, _u64, _u64, _p], _i),
+    "tileqr_ssrfb_impl": ([_i, _i], ctypes.c_char_p),
+    "tileqr_finalize": ([], None),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+LIB_PATH = _LIB_PATH
+
+
+class TileQRError(RuntimeError):
+    pass
+
+
+def _check(rc: int, fn: str):
+    if rc != 0:
+        msg = _lib.tileqr_last_error().decode()
+        raise TileQRError(f"{fn} returned {rc}: {msg}")
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def version() -> str:
+    return _lib.tileqr_version().decode()
+
+
+def last_error() -> str:
+    return _lib.tileqr_last_error().decode()
+
+
+def t_size(m: int, n: int, nb: int, ib: int) -> int:
+    out = _sz()
+    _check(_lib.tileqr_t_size(m, n, nb, ib, ctypes.byref(out)), "tileqr_t_size")
+    return out.value
+
+
+def num_levels(mt: int, nt: int) -> int:
+    out = _i64()
+    _check(_lib.tileqr_num_levels(mt, nt, ctypes.byref(out)), "tileqr_num_levels")
+    return out.value
+
+
+def ssrfb_impl(nb: int, ib: int) -> str:
+    return _lib.tileqr_ssrfb_impl(nb, ib).decode()
+
+
+# ---------------------------------------------------------------------------
+# column-major helpers
+# ---------------------------------------------------------------------------
+def colmajor_empty(m: int, n: int, device="cuda") -> torch.Tensor:
+    """Storage of a column-major m x n FP64 matrix: a (n, m) row-major tensor."""
+    return torch.empty((n, m), dtype=torch.float64, device=device)
+
+
+def to_colmajor(x, device="cuda") -> torch.Tensor:
+    """numpy/torch m x n matrix -> device storage (n, m) holding it column-major."""
+    t = torch.as_tensor(x, dtype=torch.float64)
+    return t.t().contiguous().to(device)
+
+
+def from_colmajor(buf: torch.Tensor):
+    """device storage (n, m) -> numpy m x n matrix (Fortran order)."""
+    import numpy as np
+    return np.asfortranarray(buf.detach().cpu().numpy().T)
+
+
+# ---------------------------------------------------------------------------
+# entry points
+# ---------------------------------------------------------------------------
+def factor(A: torch.Tensor, m: int, n: int, nb: int, ib: int, T: torch.Tensor | None = None,
+           info: torch.Tensor | None = None, lda: int | None = None, stream=None):
+    """tileqr_factor on the column-major m x n matrix stored in A (in place).
+
+    Returns (T, info) device tensors."""
+    assert A.dtype == torch.float64 and A.is_cuda and A.is_contiguous()
+    if T is None:
+        T = torch.empty(max(1, t_size(m, n, nb, ib)), dtype=torch.float64, device=A.device)
+    if info is None:
+        info = torch.zeros(1, dtype=torch.int32, device=A.device)
+    rc = _lib.tileqr_factor(m, n, A.data_ptr(), lda if lda is not None else max(1, m), nb, ib,
+                            T.data_ptr(), info.data_ptr(), _stream(stream))
+    _check(rc, "tileqr_factor")
+    return T, info
+
+
+def apply_qt(trans: str, A: torch.Tensor, m: int, k: int, T: torch.Tensor, nb: int, ib: int,
+             B: torch.Tensor, nrhs: int, lda: int | None = None, ldb: int | None = None,
+             stream=None):
+    """B <- Q^T B ('T') or Q B ('N') in place (B column-major m x nrhs)."""
+    rc = _lib.tileqr_apply_qt(trans.encode(), m, nrhs, k, A.data_ptr(),
+                              lda if lda is not None else max(1, m), T.data_ptr(), nb, ib,
+                              B.data_ptr(), ldb if ldb is not None else max(1, m), _stream(stream))
+    _check(rc, "tileqr_apply_qt")
+    return B
+
+
+def _ptrs(tiles) -> torch.Tensor:
+    return torch.tensor([t.data_ptr() for t in tiles], dtype=torch.int64, device="cuda")
+
+
+def geqrt_batched(nb: int, ib: int, A_ptrs: torch.Tensor, T_ptrs: torch.Tensor, stream=None):
+    _check(_lib.tileqr_geqrt_batched(nb, ib, A_ptrs.numel(), A_ptrs.data_ptr(), T_ptrs.data_ptr(),
+                                     _stream(stream)), "tileqr_geqrt_batched")
+
+
+def tsqrt_batched(nb: int, ib: int, R_ptrs, A2_ptrs, T_ptrs, stream=None):
+    _check(_lib.tileqr_tsqrt_batched(nb, ib, R_ptrs.numel(), R_ptrs.data_ptr(), A2_ptrs.data_ptr(),
+                                     T_ptrs.data_ptr(), _stream(stream)), "tileqr_tsqrt_batched")
+
+
+def larfb_batched(trans: str, nb: int, ib: int, V_ptrs, T_ptrs, C_ptrs, ncols: int, stream=None):
+    _check(_lib.tileqr_larfb_batched(trans.encode(), nb, ib, V_ptrs.numel(), V_ptrs.data_ptr(),
+                                     T_ptrs.data_ptr(), C_ptrs.data_ptr(), ncols, _stream(stream)),
+           "tileqr_larfb_batched")
+
+
+def ssrfb_batched(trans: str, nb: int, ib: int, V2_ptrs, T_ptrs, C1_ptrs, C2_ptrs, ncols: int,
+                  stream=None):
+    _check(_lib.tileqr_ssrfb_batched(trans.encode(), nb, ib, V2_ptrs.numel(), V2_ptrs.data_ptr(),
+                                     T_ptrs.data_ptr(), C1_ptrs.data_ptr(), C2_ptrs.data_ptr(),
+                                     ncols, _stream(stream)), "tileqr_ssrfb_batched")
+
+
+def rng_uniform(A: torch.Tensor, m: int, n: int, seed: int, offset: int = 0, lda: int | None = None,
+                stream=None):
+    _check(_lib.tileqr_rng_uniform(m, n, A.data_ptr(), lda if lda is not None else max(1, m), seed,
+                                   offset, _stream(stream)), "tileqr_rng_uniform")
+    return A
+
+
+def tune(m: int, n: int, ngpus: int = 1, heuristic: int = 2, payg: bool = True,
+         report_json_path: str | None = None):
+    nb, ib = ctypes.c_int(), ctypes.c_int()
+    rc = _lib.tileqr_tune(m, n, ngpus, heuristic, int(payg), ctypes.byref(nb), ctypes.byref(ib),
+                          report_json_path.encode() if report_json_path else None)
+    _check(rc, "tileqr_tune")
+    return nb.value, ib.value
+
+
+def preselect(samples, heuristic: int = 2, cap: int = 8):
+    """Host-only Step-1 pre-selection; samples [(nb, ib, gflops)]."""
+    n = len(samples)
+    nb = (ctypes.c_int * n)(*[s[0] for s in samples])
+    ib = (ctypes.c_int * n)(*[s[1] for s in samples])
+    g = (ctypes.c_double * n)(*[s[2] for s in samples])
+    onb, oib, og = (ctypes.c_int * n)(), (ctypes.c_int * n)(), (ctypes.c_double * n)()
+    cnt = ctypes.c_int()
+    _check(_lib.tileqr_preselect(n, nb, ib, g, heuristic, cap, onb, oib, og, ctypes.byref(cnt)),
+           "tileqr_preselect")
+    return [(onb[i], oib[i], og[i]) for i in range(cnt.value)]
+
+
+def payg_prune(results):
+    """Host-only Property-3 prune; results [(nb, ib, gflops)] -> survivors."""
+    n = len(results)
+    nb = (ctypes.c_int * n)(*[r[0] for r in results])
+    g = (ctypes.c_double * n)(*[r[2] for r in results])
+    keep = (ctypes.c_int * n)()
+    _check(_lib.tileqr_payg_prune(n, nb, g, keep), "tileqr_payg_prune")
+    return [r for r, k in zip(results, keep) if k]
+
+
+def finalize():
+    _lib.tileqr_finalize()

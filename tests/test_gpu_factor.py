@@ -1,0 +1,174 @@
+"""GPU parity of the whole tile QR (tileqr_factor / tileqr_apply_qt through the
+C ABI) against the oracle, with BASELINE.json north_star's tolerances:
+
+    ||A - QR||_F / (||A||_F N eps) < 10,  ||Q^T Q - I||_F / (N eps) < 10,
+    sign-normalised R within 1e-10 (normwise relative, R10) of the
+    oracle's R.
+
+Q is formed on the GPU (apply_qt('N') of the identity).  Sizes span several
+tiles and ragged tails; config [0] (256^2, NB=64, IB=16) and config [2]
+(2048^2) run in full; config [3] (10000^2) checks the outputs the oracle can
+compute cheaply (the first block row of R and panel 0, oracle kmax=1) plus
+residual / orthogonality properties on random vectors.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth_inputs as si
+from _tq import EPS, nrel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tq():
+    from paper_1102_5328_b200 import tileqr
+    return tileqr
+
+
+def gpu_factor(tq, a, nb, ib):
+    m, n = a.shape
+    A = tq.to_colmajor(a)
+    T, info = tq.factor(A, m, n, nb, ib)
+    torch.cuda.synchronize()
+    return A, T, info
+
+
+def gpu_q(tq, A, T, m, k, nb, ib):
+    Q = tq.to_colmajor(np.eye(m))
+    tq.apply_qt("N", A, m, k, T, nb, ib, Q, m)
+    torch.cuda.synchronize()
+    return tq.from_colmajor(Q)
+
+
+def check_against_oracle(tq, m, n, nb, ib, seed):
+    a = si.uniform(m, n, seed)
+    A, T, info = gpu_factor(tq, a, nb, ib)
+    assert int(info.item()) == 0
+    f = tq.from_colmajor(A)
+    fo, to, _ = oracle.tileqr_factor(a, nb, ib)
+    # primary: sign-normalised R (north_star) -- 1e-10 normwise relative
+    assert nrel(oracle.sign_normalised_r(f), oracle.sign_normalised_r(fo)) < 1e-10
+    # secondary: same (NB, IB) and convention => same V and T (R12)
+    assert nrel(f, fo) < 1e-10
+    assert nrel(T.cpu().numpy(), to) < 1e-10
+    k = min(m, n)
+    q = gpu_q(tq, A, T, m, n, nb, ib)
+    r = np.triu(f[:k, :])
+    assert np.linalg.norm(a - q[:, :k] @ r) / (np.linalg.norm(a) * max(m, n) * EPS) < 10
+    assert np.linalg.norm(q.T @ q - np.eye(m)) / (m * EPS) < 10
+    return A, T
+
+
+CASES = [
+    (256, 256, 64, 16, 1),     # config [0]
+    (250, 250, 64, 16, 11),    # ragged: padded to 4 x 4 tiles
+    (300, 300, 96, 12, 12),
+    (520, 520, 128, 32, 13),   # 5 x 5 tiles, ragged tail of 8
+    (700, 300, 128, 32, 14),   # tall
+    (300, 700, 128, 16, 15),   # wide
+    (600, 600, 256, 256, 16),  # IB = NB (no inner blocking)
+    (480, 480, 224, 7, 17),    # odd IB
+    (256, 256, 64, 1, 18),     # IB = 1
+    (512, 512, 160, 40, 19),
+    (384, 384, 192, 64, 20),
+    (200, 200, 48, 6, 21),     # SIMT path (NB % 32 != 0)
+    (64, 64, 64, 16, 22),      # single tile
+    (1, 1, 32, 8, 23),
+    (37, 5, 32, 4, 24),
+]
+
+
+@pytest.mark.parametrize("m,n,nb,ib,seed", CASES)
+def test_factor_matches_oracle(tq, m, n, nb, ib, seed):
+    check_against_oracle(tq, m, n, nb, ib, seed)
+
+
+@pytest.mark.parametrize("nb,ib", [(64, 16), (128, 32), (256, 64)])
+def test_factor_config2_full(tq, nb, ib):  # BASELINE.json configs[2], 2048^2
+    check_against_oracle(tq, 2048, 2048, nb, ib, 3)
+
+
+def test_factor_is_deterministic_and_graph_equals_eager(tq, monkeypatch):
+    a = si.uniform(640, 640, 30)
+    A1, T1, _ = gpu_factor(tq, a, 128, 32)
+    A2, T2, _ = gpu_factor(tq, a, 128, 32)
+    assert torch.equal(A1, A2) and torch.equal(T1, T2)
+    monkeypatch.setenv("TILEQR_NO_GRAPH", "1")
+    A3, T3, _ = gpu_factor(tq, a, 128, 32)
+    assert torch.equal(A1, A3) and torch.equal(T1, T3)
+
+
+def test_nonfinite_sets_info(tq):
+    a = si.uniform(128, 128, 31)
+    a[17, 90] = np.nan
+    _, _, info = gpu_factor(tq, a, 64, 16)
+    assert int(info.item()) == 1
+    a[17, 90] = 0.5
+    _, _, info = gpu_factor(tq, a, 64, 16)
+    assert int(info.item()) == 0
+
+
+def test_apply_round_trip_and_qt_a_is_r(tq):
+    m, n, nb, ib = 500, 300, 128, 32
+    a = si.uniform(m, n, 32)
+    A, T, _ = gpu_factor(tq, a, nb, ib)
+    f = tq.from_colmajor(A)
+    b = si.uniform(m, 7, 33)
+    B = tq.to_colmajor(b)
+    tq.apply_qt("N", A, m, n, T, nb, ib, B, 7)
+    tq.apply_qt("T", A, m, n, T, nb, ib, B, 7)
+    torch.cuda.synchronize()
+    assert nrel(tq.from_colmajor(B), b) < 1e-13
+    Aq = tq.to_colmajor(a)
+    tq.apply_qt("T", A, m, n, T, nb, ib, Aq, n)
+    torch.cuda.synchronize()
+    qta = tq.from_colmajor(Aq)
+    assert nrel(qta[:n], np.triu(f[:n])) < 1e-13 and np.linalg.norm(qta[n:]) < 1e-12
+
+
+def test_empty_is_quick_return(tq):
+    A = torch.zeros(1, dtype=torch.float64, device="cuda")
+    T, info = tq.factor(A, 0, 5, 4, 2, T=torch.zeros(1, dtype=torch.float64, device="cuda"))
+    assert int(info.item()) == 0
+
+
+@pytest.mark.slow
+def test_factor_config3_sampled(tq):
+    """BASELINE.json configs[3] (10000^2) in the bench's launch configuration:
+    first block row of R and panel 0 (V, T) against the oracle (kmax=1), and
+    residual / orthogonality on random vectors (hold at any size)."""
+    n = 10000
+    nb, ib = int(os.environ.get("TILEQR_BENCH_NB", 128)), int(os.environ.get("TILEQR_BENCH_IB", 32))
+    a = si.uniform(n, n, 4)
+    A = tq.to_colmajor(a)
+    T, info = tq.factor(A, n, n, nb, ib)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    fo, to, _ = oracle.tileqr_factor(a, nb, ib, kmax=1)
+    f_row = A[:, :nb].cpu().numpy().T  # rows 0..nb-1 of the column-major result
+    assert nrel(f_row, fo[:nb, :]) < 1e-10
+    f_col = A[:nb, :].cpu().numpy().T  # panel 0 (columns 0..nb-1)
+    assert nrel(f_col, fo[:, :nb]) < 1e-10
+    mt = -(-n // nb)
+    assert nrel(T[: mt * ib * nb].cpu().numpy(), to[: mt * ib * nb]) < 1e-10
+    # residual ||A x - Q R x|| and orthogonality ||Q^T Q y - y|| on random vectors
+    x = si.uniform(n, 4, 40)
+    Rx = torch.triu(A.t()) @ torch.from_numpy(x).cuda()  # A.t() is the matrix (column-major storage)
+    QRx = Rx.t().contiguous()  # column-major storage of the n x 4 matrix R x
+    tq.apply_qt("N", A, n, n, T, nb, ib, QRx, 4)
+    Ax = torch.from_numpy(a).cuda() @ torch.from_numpy(x).cuda()
+    torch.cuda.synchronize()
+    res = torch.linalg.norm(Ax - QRx.t()) / (torch.linalg.norm(torch.from_numpy(a).cuda()) *
+                                             torch.linalg.norm(torch.from_numpy(x).cuda()) * n * EPS)
+    assert float(res) < 10
+    y = tq.to_colmajor(si.uniform(n, 4, 41))
+    y0 = y.clone()
+    tq.apply_qt("N", A, n, n, T, nb, ib, y, 4)
+    tq.apply_qt("T", A, n, n, T, nb, ib, y, 4)
+    torch.cuda.synchronize()
+    assert float(torch.linalg.norm(y - y0) / (torch.linalg.norm(y0) * n * EPS)) < 10
