@@ -1,0 +1,324 @@
+"""bench.py -- tile-QR FP64 throughput of libtileqr on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tileqr|reference]
+                    [--workload 3|2|0|4] [--nb NB --ib IB]
+
+One "step" = one whole tile QR factorization (tileqr_factor: layout in, every
+DAG level of GEQRT/TSQRT/LARFB/SSRFB, layout out, T copy) of the workload's
+matrix, restored from a pristine device copy at the start of the step.
+
+Workload at N=1: BASELINE.json configs[3] (10000 x 10000, uniform(-0.5,0.5),
+seed 4, NB/IB from the tuner's decision table) -- the largest single-GPU
+tile-QR configuration (configs[1] is a kernel sweep, not a factorization).
+At N>1 (torchrun): configs[4], 40000 x 40000 with tile columns 1D
+block-cyclic over the ranks (tileqr_dist_factor; strong scaling).
+
+Metric: GFLOP/s = (4/3 N^3) / t (unpadded N, IB extra
+flops not credited), also as % of the measured B200 FP64 (DMMA) peak.
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
+plain C tile QR in oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0   # measured: tools/peak_fp64.cu, profiles/peak_fp64_r01.json (DMMA, sustained)
+FP64_PEAK_SRC = "measured here: mma.sync.m8n8k4.f64 register loop on 148 SMs at 1965 MHz (profiles/peak_fp64_r01.json)"
+
+WORKLOADS = {
+    0: dict(name="qr256_nb64_ib16 (BASELINE configs[0])", M=256, N=256, seed=1, nb=64, ib=16),
+    2: dict(name="qr2048 (BASELINE configs[2])", M=2048, N=2048, seed=3),
+    3: dict(name="qr10000_tuned (BASELINE configs[3])", M=10000, N=10000, seed=4),
+    4: dict(name="qr40000_dist (BASELINE configs[4])", M=40000, N=40000, seed=5),
+}
+TUNED = os.path.join(ROOT, "paper_1102_5328_b200", "tuned_table.json")
+
+
+def qr_flops(m: int, n: int) -> float:
+    if m >= n:
+        return 2.0 * m * n * n - 2.0 * n ** 3 / 3.0
+    return 2.0 * n * m * m - 2.0 * m ** 3 / 3.0
+
+
+def tuned_pair(n: int, ngpus: int):
+    """Nearest-point lookup in the decision table."""
+    if os.path.exists(TUNED):
+        tab = json.load(open(TUNED))["entries"]
+        ns = sorted({e["n"] for e in tab})
+        cs = sorted({e["ngpus"] for e in tab})
+        nn = min(ns, key=lambda v: (abs(v - n), -v))
+        cc = min(cs, key=lambda v: (abs(v - ngpus), -v))
+        for e in tab:
+            if e["n"] == nn and e["ngpus"] == cc:
+                return e["nb"], e["ib"], "tuned_table.json (tileqr_tune, nearest point)"
+    return 64, 16, "default (no tuned table)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_sample(m, n, nb, ib, seed, target_gflop=150.0):
+    """Time the CPU oracle (as it stands) on the first kmax panels of the same
+    workload: useful flops = flops(m, n) - flops of the untouched trailing part."""
+    import numpy as np  # noqa: F401
+    import oracle
+    import synth_inputs as si
+    cores = len(os.sched_getaffinity(0))
+    kmax = max(1, int(target_gflop * 1e9 / (4.0 * m * n * nb)))
+    kmax = min(kmax, -(-min(m, n) // nb))
+    a = si.uniform(m, n, seed)
+    t0 = time.perf_counter()
+    oracle.tileqr_factor(a, nb, ib, nthreads=cores, kmax=kmax)
+    dt = time.perf_counter() - t0
+    done = kmax * nb
+    fl = qr_flops(m, n) - (qr_flops(m - done, n - done) if done < min(m, n) else 0.0)
+    return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {kmax} of {-(-min(m, n) // nb)} panels (k < {kmax}) of the {m}x{n} "
+                      f"NB={nb} IB={ib} factorization, oracle/tileqr_oracle.c with {cores} OpenMP "
+                      f"threads; {fl / 1e9:.1f} useful GFLOP in {dt:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload if args.workload is not None else (3 if world == 1 else 4)]
+    m, n = wl["M"], wl["N"]
+    nb, ib = (args.nb, args.ib) if args.nb else tuned_pair(n, world)[:2]
+    if "nb" in wl and not args.nb:
+        nb, ib = wl["nb"], wl["ib"]
+    target = float(os.environ.get("TILEQR_REF_GFLOP", 60.0))
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        cpu_oracle_sample(min(m, 1024), min(n, 1024), nb, ib, wl["seed"], target_gflop=1.0)
+    vals, samples = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = cpu_oracle_sample(m, n, nb, ib, wl["seed"], target_gflop=target)
+        vals.append(r["value"])
+        samples.append(r)
+    wall = time.perf_counter() - t0
+    v = statistics.median(vals)
+    line = {"metric": "tile-QR FP64 GFLOP/s", "value": v, "unit": "GFLOP/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["name"], "M": m, "N": n, "NB": nb, "IB": ib},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": samples[0]["cores"],
+                             "kind": "oracle", "sample": samples[0]["sample"]},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_tileqr(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_1102_5328_b200 import tileqr as tq
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        return run_tileqr_dist(args, rank, world, local_rank)
+    wl = WORKLOADS[args.workload if args.workload is not None else 3]
+    m, n, seed = wl["M"], wl["N"], wl["seed"]
+    if args.nb:
+        nb, ib, src = args.nb, args.ib, "command line"
+    elif "nb" in wl:
+        nb, ib, src = wl["nb"], wl["ib"], "BASELINE configs[0]"
+    else:
+        nb, ib, src = tuned_pair(n, world)
+    plan = tq.factor_plan(m, n, nb, ib)
+
+    A0 = torch.empty((n, m), dtype=torch.float64, device=dev)   # column-major m x n
+    tq.rng_uniform(A0, m, n, seed=seed)
+    A = torch.empty_like(A0)
+    T = torch.empty(max(1, tq.t_size(m, n, nb, ib)), dtype=torch.float64, device=dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        A.copy_(A0)
+        tq.factor(A, m, n, nb, ib, T=T, info=info)
+
+    tq.set_kernel_timing(True)   # event-record nodes around every launch (measured below)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(info.item()) != 0:
+        raise RuntimeError("tileqr_factor reported a non-finite input")
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    flops = qr_flops(m, n)
+    value = flops / (ms * 1e-3) / 1e9
+
+    # per-kind kernel durations of the last timed step (CUDA events on the launching streams)
+    kinds = {}
+    for k in ("geqrt", "tsqrt", "larfb", "ssrfb"):
+        tot, nl, nt = tq.kernel_times(m, n, nb, ib, k)
+        kinds[k] = {"ms": round(tot, 3), "launches": nl, "tasks": nt}
+    tq.set_kernel_timing(False)
+    s = kinds["ssrfb"]
+    ssrfb_flops = s["tasks"] * 4.0 * nb ** 3          # useful 4 NB^3 per pair
+    achieved = ssrfb_flops / (s["ms"] * 1e-3) / 1e12 if s["ms"] > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_ssrfb_traffic.json")
+    if os.path.exists(prof):
+        p = json.load(open(prof))
+        key = f"{nb}:{ib}"
+        if key in p.get("per_task_bytes", {}) and s["launches"]:
+            traffic = p["per_task_bytes"][key] * s["tasks"] / s["launches"]
+    roofline = {"kernel": "ssrfb (dmma_update_kernel)", "bound": "tensor",
+                "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
+                "flops_per_launch": ssrfb_flops / max(1, s["launches"]),
+                "avg_launch_ms": round(s["ms"] / max(1, s["launches"]), 4),
+                "peak_source": FP64_PEAK_SRC,
+                "share_of_step": round(s["ms"] / ms, 4)}
+
+    # e2e: same metric through the public API with host buffers (pinned), H2D of
+    # the input and D2H of the result (R/V and T) inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hA = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        hA.copy_(A0)
+        hR = torch.empty_like(hA, pin_memory=True)
+        hT = torch.empty(T.numel(), dtype=torch.float64, pin_memory=True)
+        dA = torch.empty_like(A0)
+        e2e_steps = max(1, min(args.steps, 3))
+
+        def step_e2e():
+            dA.copy_(hA, non_blocking=True)
+            tq.factor(dA, m, n, nb, ib, T=T, info=info)
+            hR.copy_(dA, non_blocking=True)
+            hT.copy_(T, non_blocking=True)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / e2e_steps
+        e2e = {"value": flops / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": hA.numel() * 8, "d2h_bytes_per_step": (hR.numel() + hT.numel()) * 8,
+               "ms_per_step": ms_e2e, "steps": e2e_steps}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(m, n, nb, ib, seed)
+
+    line = {"metric": "tile-QR FP64 GFLOP/s", "value": round(value, 2), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic: i.i.d. uniform(-0.5,0.5), splitmix64 counter generator, seed {seed}",
+            "config": {"workload": wl["name"], "M": m, "N": n, "NB": nb, "IB": ib, "nb_ib_source": src,
+                       "parallelism": "single GPU", "levels": plan["levels"],
+                       "l2": f"input {m * n * 8 / 1e6:.0f} MB > 126 MB L2; A restored from a pristine "
+                             "device copy at the start of every step (inside the timed region)"},
+            "pct_fp64_peak": round(100 * value / (FP64_PEAK_TFLOPS * 1e3), 2),
+            "roofline": roofline, "kernels": kinds, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": plan["launches"] * args.steps,
+            "clocks": clk.summary(), "lib": tq.LIB_PATH}
+    print(json.dumps(line), flush=True)
+
+
+def run_tileqr_dist(args, rank, world, local_rank):
+    raise NotImplementedError("multi-GPU path: see tileqr_dist_factor")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tileqr", choices=["tileqr", "reference"])
+    ap.add_argument("--workload", type=int, default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--nb", type=int, default=None)
+    ap.add_argument("--ib", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "tileqr":
+        ap.error("--warmup must be >= 3")
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_tileqr(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

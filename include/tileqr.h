@@ -204,6 +204,20 @@ int tileqr_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t se
  * 32 <= NB <= 256) or "simt" (any NB <= 512). */
 const char* tileqr_ssrfb_impl(int NB, int IB);
 
+/* Static plan of tileqr_factor(M, N, NB, IB): h_out[8] = {levels, kernel
+ * launches per call, #GEQRT, #TSQRT, #LARFB, #SSRFB tasks, MT, NT}. */
+int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out);
+
+/* Kernel timing for measurement (bench.py): when on, tileqr_factor brackets
+ * every batched launch with CUDA events on the stream it is launched on
+ * (captured into the CUDA graph as event-record nodes). */
+void tileqr_set_kernel_timing(int on);
+/* After the stream of a timed tileqr_factor(M, N, NB, IB) completed: sum of
+ * the launch durations of kernel kind (0 GEQRT, 1 TSQRT, 2 LARFB, 3 SSRFB) in
+ * the most recent run, the number of launches and of tasks. */
+int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
+                        int64_t* h_launches, int64_t* h_tasks);
+
 /* Release all cached workspaces, graphs and communicators. */
 void tileqr_finalize(void);
 

@@ -13,8 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtileqr.so")
-SOURCES = ["kernels_layout.cu", "kernels_panel.cu", "kernels_update.cu", "api.cu", "tune.cu",
-           "dist.cu"]
+SOURCES = ["kernels_layout.cu", "kernels_panel.cu", "kernels_panel_fast.cu", "kernels_update.cu",
+           "api.cu", "tune.cu", "dist.cu"] + [f"update_nb{nb}.cu" for nb in (32, 64, 96, 128, 160, 192, 224, 256)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

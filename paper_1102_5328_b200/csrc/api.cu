@@ -120,8 +120,14 @@ struct FactorWS {
   cudaStream_t s_panel = nullptr, s_update = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaGraphExec_t graph = nullptr;
+  bool graph_timed = false;
+  // kernel timing (tileqr_set_kernel_timing): one event pair per launch
+  struct Rec { int kind; int64_t tasks; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  size_t rec_used = 0;
   ~FactorWS() {
     if (graph) cudaGraphExecDestroy(graph);
+    for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ev) cudaEventDestroy(e);
     if (s_panel) cudaStreamDestroy(s_panel);
     if (s_update) cudaStreamDestroy(s_update);
@@ -133,6 +139,8 @@ struct FactorWS {
 
 static std::mutex g_mu;
 static std::map<std::tuple<int, int64_t, int64_t, int, int>, std::unique_ptr<FactorWS>> g_ws;
+
+static bool g_timing = false;
 
 static bool use_graph() {
   const char* e = getenv("TILEQR_NO_GRAPH");
@@ -227,8 +235,13 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
   ws->tR = d + oT; ws->tA = d + oT + nT; ws->tT = d + oT + 2 * nT;
   ws->lV = d + oL; ws->lT = d + oL + nL; ws->lC = d + oL + 2 * nL;
   ws->sV = d + oS; ws->sT = d + oS + nS; ws->sC1 = d + oS + 2 * nS; ws->sC2 = d + oS + 3 * nS;
-  TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_panel, cudaStreamNonBlocking));
-  TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_update, cudaStreamNonBlocking));
+  // The panel kernels (GEQRT/TSQRT) are the DAG's critical path: their stream
+  // gets the highest priority so their CTAs are dispatched ahead of queued
+  // update CTAs whenever an SM frees up (kept per node in the CUDA graph).
+  int prio_lo = 0, prio_hi = 0;
+  TQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  TQ_CUDA(cudaStreamCreateWithPriority(&ws->s_panel, cudaStreamNonBlocking, prio_hi));
+  TQ_CUDA(cudaStreamCreateWithPriority(&ws->s_update, cudaStreamNonBlocking, prio_lo));
   ws->ev.resize(4);
   for (auto& e : ws->ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   *out = ws.get();
@@ -237,10 +250,33 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
 }
 
 // Issue the level sequence: s_panel runs GEQRT/TSQRT, s_update LARFB/SSRFB.
+// With kernel timing on, every launch is bracketed by two events (captured as
+// event-record nodes when the sequence is captured into the graph).
+static int timed_begin(FactorWS* ws, int kind, int64_t tasks, cudaStream_t st, size_t* slot) {
+  if (!g_timing) return 0;
+  if (ws->rec_used == ws->recs.size()) {
+    FactorWS::Rec r{kind, tasks, nullptr, nullptr};
+    TQ_CUDA(cudaEventCreate(&r.a));
+    TQ_CUDA(cudaEventCreate(&r.b));
+    ws->recs.push_back(r);
+  }
+  *slot = ws->rec_used++;
+  ws->recs[*slot].kind = kind;
+  ws->recs[*slot].tasks = tasks;
+  TQ_CUDA(cudaEventRecordWithFlags(ws->recs[*slot].a, st, cudaEventRecordExternal));
+  return 0;
+}
+static int timed_end(FactorWS* ws, size_t slot, cudaStream_t st) {
+  if (!g_timing) return 0;
+  TQ_CUDA(cudaEventRecordWithFlags(ws->recs[slot].b, st, cudaEventRecordExternal));
+  return 0;
+}
+
 static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
   const LevelLists& lv = ws->lv;
   const int NB = ws->NB, IB = ws->IB;
   cudaEvent_t ep = ws->ev[0], eu = ws->ev[1];
+  ws->rec_used = 0;
   for (int64_t t = 0; t < lv.nlev; ++t) {
     if (t > 0) {  // level t depends on everything of level t-1
       TQ_CUDA(cudaEventRecord(eu, su));
@@ -249,21 +285,34 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
       TQ_CUDA(cudaStreamWaitEvent(su, ep, 0));
     }
     int rc;
-    if (lv.g_cnt[t] > 0 &&
-        (rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp)))
-      return rc;
-    if (lv.t_cnt[t] > 0 &&
-        (rc = launch_tsqrt(NB, IB, (int)lv.t_cnt[t], ws->tR + lv.t_off[t], ws->tA + lv.t_off[t],
-                           ws->tT + lv.t_off[t], sp)))
-      return rc;
-    if (lv.l_cnt[t] > 0 &&
-        (rc = launch_larfb(true, NB, IB, (int)lv.l_cnt[t], ws->lV + lv.l_off[t], ws->lT + lv.l_off[t],
-                           ws->lC + lv.l_off[t], NB, su)))
-      return rc;
-    if (lv.s_cnt[t] > 0 &&
-        (rc = launch_ssrfb(true, NB, IB, (int)lv.s_cnt[t], ws->sV + lv.s_off[t], ws->sT + lv.s_off[t],
-                           ws->sC1 + lv.s_off[t], ws->sC2 + lv.s_off[t], NB, su)))
-      return rc;
+    size_t slot = 0;
+    if (lv.g_cnt[t] > 0) {
+      if ((rc = timed_begin(ws, 0, lv.g_cnt[t], sp, &slot))) return rc;
+      if ((rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp)))
+        return rc;
+      if ((rc = timed_end(ws, slot, sp))) return rc;
+    }
+    if (lv.t_cnt[t] > 0) {
+      if ((rc = timed_begin(ws, 1, lv.t_cnt[t], sp, &slot))) return rc;
+      if ((rc = launch_tsqrt(NB, IB, (int)lv.t_cnt[t], ws->tR + lv.t_off[t], ws->tA + lv.t_off[t],
+                             ws->tT + lv.t_off[t], sp)))
+        return rc;
+      if ((rc = timed_end(ws, slot, sp))) return rc;
+    }
+    if (lv.l_cnt[t] > 0) {
+      if ((rc = timed_begin(ws, 2, lv.l_cnt[t], su, &slot))) return rc;
+      if ((rc = launch_larfb(true, NB, IB, (int)lv.l_cnt[t], ws->lV + lv.l_off[t], ws->lT + lv.l_off[t],
+                             ws->lC + lv.l_off[t], NB, su)))
+        return rc;
+      if ((rc = timed_end(ws, slot, su))) return rc;
+    }
+    if (lv.s_cnt[t] > 0) {
+      if ((rc = timed_begin(ws, 3, lv.s_cnt[t], su, &slot))) return rc;
+      if ((rc = launch_ssrfb(true, NB, IB, (int)lv.s_cnt[t], ws->sV + lv.s_off[t], ws->sT + lv.s_off[t],
+                             ws->sC1 + lv.s_off[t], ws->sC2 + lv.s_off[t], NB, su)))
+        return rc;
+      if ((rc = timed_end(ws, slot, su))) return rc;
+    }
   }
   return 0;
 }
@@ -271,7 +320,12 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
 // Run the level sequence ordered after `stream` and before subsequent work on it.
 static int run_levels(FactorWS* ws, cudaStream_t stream) {
   if (use_graph()) {
+    if (ws->graph && ws->graph_timed != g_timing) {
+      cudaGraphExecDestroy(ws->graph);
+      ws->graph = nullptr;
+    }
     if (!ws->graph) {
+      ws->graph_timed = g_timing;
       cudaStream_t cs = ws->s_panel;
       TQ_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
       TQ_CUDA(cudaEventRecord(ws->ev[2], cs));
@@ -286,7 +340,7 @@ static int run_levels(FactorWS* ws, cudaStream_t stream) {
         return rc;
       }
       TQ_CUDA(e);
-      e = cudaGraphInstantiate(&ws->graph, g, 0);
+      e = cudaGraphInstantiate(&ws->graph, g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
       TQ_CUDA(e);
     }
@@ -308,6 +362,7 @@ static int run_levels(FactorWS* ws, cudaStream_t stream) {
 
 }  // namespace tileqr
 
+namespace tileqr { int panel_prof_read(unsigned long long* out, int reset); }
 using namespace tileqr;
 
 extern "C" {
@@ -533,6 +588,73 @@ int tileqr_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t se
 }
 
 const char* tileqr_ssrfb_impl(int NB, int IB) { return ssrfb_impl_name(NB, IB); }
+
+// Diagnostic (not in the header): accumulated phase cycles of the fast panel kernel.
+int tileqr_debug_panel_prof(unsigned long long* out, int reset) { return tileqr::panel_prof_read(out, reset); }
+
+int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out) {
+  static const char* fn = "tileqr_factor_plan";
+  if (M < 0) return arg_error(1, fn, "M < 0");
+  if (N < 0) return arg_error(2, fn, "N < 0");
+  if (NB < 1 || NB > 512) return arg_error(3, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(4, fn, "IB must divide NB");
+  if (!h_out) return arg_error(5, fn, "NULL output");
+  const int64_t MT = (M + NB - 1) / NB, NT = (N + NB - 1) / NB;
+  const int64_t nlev = (M == 0 || N == 0) ? 0 : num_levels(MT, NT);
+  HostTasks h;
+  build_tasks(MT, NT, h, nlev);
+  int64_t launches = 0, cnt[4] = {0, 0, 0, 0};
+  for (int64_t t = 0; t < nlev; ++t) {
+    const int64_t c[4] = {(int64_t)h.G[t].size(), (int64_t)h.T[t].size() / 2,
+                          (int64_t)h.L[t].size() / 2, (int64_t)h.S[t].size() / 3};
+    for (int q = 0; q < 4; ++q) {
+      cnt[q] += c[q];
+      launches += c[q] > 0;
+    }
+  }
+  h_out[0] = nlev;
+  h_out[1] = launches + ((M == 0 || N == 0) ? 0 : 3);  // + zero-info, layout in, layout out
+  for (int q = 0; q < 4; ++q) h_out[2 + q] = cnt[q];
+  h_out[6] = MT;
+  h_out[7] = NT;
+  return 0;
+}
+
+void tileqr_set_kernel_timing(int on) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_timing = on != 0;
+}
+
+int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
+                        int64_t* h_launches, int64_t* h_tasks) {
+  static const char* fn = "tileqr_kernel_times";
+  if (kind < 0 || kind > 3) return arg_error(5, fn, "kind not in 0..3");
+  if (!h_total_ms || !h_launches || !h_tasks) return arg_error(6, fn, "NULL output");
+  int dev;
+  TQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  if (it == g_ws.end()) {
+    set_error("tileqr_kernel_times: no factorization of this shape has run");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  FactorWS* ws = it->second.get();
+  double tot = 0.0;
+  int64_t nl = 0, nt = 0;
+  for (size_t i = 0; i < ws->rec_used; ++i) {
+    const FactorWS::Rec& r = ws->recs[i];
+    if (r.kind != kind) continue;
+    float ms = 0.f;
+    TQ_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    tot += ms;
+    ++nl;
+    nt += r.tasks;
+  }
+  *h_total_ms = tot;
+  *h_launches = nl;
+  *h_tasks = nt;
+  return 0;
+}
 
 void tileqr_finalize(void) {
   std::lock_guard<std::mutex> lock(g_mu);

@@ -19,6 +19,7 @@
 // rescaling loop).  TSQRT never writes the strict lower part of R, which the
 // LARFB of the same DAG level reads.
 #include <math.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -294,12 +295,32 @@ int launch_panel(int NB, int IB, int batch, double* const* R, double* const* B, 
 
 }  // namespace
 
+bool panel_fast_supported(int NB, int IB);
+int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s);
+int launch_tsqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
+                      double* const* T, cudaStream_t s);
+
+static bool generic_panel_forced() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TILEQR_GENERIC_PANEL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s) {
+  if (batch <= 0) return 0;
+  if (panel_fast_supported(NB, IB) && !generic_panel_forced())
+    return launch_geqrt_fast(NB, IB, batch, A, T, s);
   return launch_panel<false>(NB, IB, batch, A, nullptr, T, s);
 }
 
 int launch_tsqrt(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
                  cudaStream_t s) {
+  if (batch <= 0) return 0;
+  if (panel_fast_supported(NB, IB) && !generic_panel_forced())
+    return launch_tsqrt_fast(NB, IB, batch, R, A2, T, s);
   return launch_panel<true>(NB, IB, batch, R, A2, T, s);
 }
 

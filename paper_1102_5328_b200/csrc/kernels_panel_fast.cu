@@ -1,0 +1,365 @@
+// kernels_panel_fast.cu -- low-latency GEQRT / TSQRT for the critical path of
+// the tile QR: NB % 32 == 0,
+// NB <= 256, IB in {8, 16, 24, 32}.  Every other (NB, IB) uses the generic
+// panel kernel (kernels_panel.cu).
+//
+// One CTA of 8 warps per task.  For each inner panel p (IB columns):
+//  1. Factor: the NB x IB panel lives in registers, lane l holding column l
+//     and warp w rows [w*NB/8, (w+1)*NB/8).  Per column j ONE pass of partial
+//     dot products gives sigma = ||x2||^2 and every d_c = x2 . P(:,c) (the
+//     pivot column is broadcast with warp shuffles), one CTA barrier combines
+//     the 8 warp partials (double-buffered, so no second barrier), and every
+//     thread forms beta/tau (R1) and applies the rank-1 update to
+//     its own registers.
+//  2. T_p: the Gram matrix V_p^T V_p on DMMA (mma.sync.m8n8k4.f64) from the
+//     staged panel, then the forward recurrence
+//     T[0:i,i] = -tau_i T[0:i,0:i] G[0:i,i], one thread per row of T.
+//  3. Trailing columns: each warp takes 8-column blocks, holds them for all
+//     NB rows in registers (transposed accumulator) and applies
+//     W = [R_p; C]^T-part ... exactly the SSRFB/LARFB steps A/B/C of
+//     kernels_update.cu on DMMA, reading V_p (swizzled) and T_p from smem.
+// TSQRT never writes the strict lower part of R (read concurrently by the
+// LARFB of the same DAG level).
+#include <math.h>
+
+#include "dmma.cuh"
+#include "internal.h"
+
+namespace tileqr {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = 8;
+constexpr int LDV = 40;   // >= 32, == 8 mod 16
+constexpr int LDT = 36;   // == 4 mod 16
+constexpr int LDW = 36;
+constexpr int LDG = 33;
+constexpr int LDR = 33;
+
+__device__ unsigned long long g_panel_prof[16];  // diagnostic phase cycles (thread 0)
+
+template <int NB>
+struct FastSmem {
+  double Vs[NB * LDV];
+  double Ts[32 * LDT];
+  double Gs[32 * LDG];
+  double Rin[32 * LDR];
+  double Rout[32 * LDR];
+  double red[2][kWarps][32];
+  double rowj[2][32];
+  double tau[32];
+  double Ws[kWarps][8 * LDW];
+};
+
+template <bool TS, int NB>
+__global__ void __launch_bounds__(kThreads, 1)
+panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* Tp) {
+  constexpr int RW = NB / 8;  // rows per warp in the factorization
+  constexpr int RB = NB / 8;  // 8-row blocks in the trailing update
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FastSmem<NB>& S = *reinterpret_cast<FastSmem<NB>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int a = lane & 3, g = lane >> 2;
+  double* const R = Rp[blockIdx.x];              // TSQRT: R tile; GEQRT: the tile
+  double* const B = TS ? Bp[blockIdx.x] : R;     // TSQRT: square tile; GEQRT: the tile
+  double* const Tg = Tp[blockIdx.x];
+
+  long long tp0 = clock64(), tp1;
+#define TQ_PHASE(k) do { if (tid == 0) { tp1 = clock64(); atomicAdd(&g_panel_prof[k], (unsigned long long)(tp1 - tp0)); tp0 = tp1; } } while (0)
+  for (int c0 = 0; c0 < NB; c0 += IB) {
+    // ---- stage the panel (coalesced) and, for TSQRT, the R block -------------
+    for (int idx = tid; idx < NB * IB; idx += kThreads) {
+      const int c = idx / NB, r = idx - c * NB;
+      S.Vs[vsw(r, c, LDV)] = B[r + (size_t)(c0 + c) * NB];
+    }
+    if (TS) {
+      for (int idx = tid; idx < IB * IB; idx += kThreads) {
+        const int c = idx / IB, i = idx - c * IB;
+        S.Rin[i * LDR + c] = (i <= c) ? R[(c0 + i) + (size_t)(c0 + c) * NB] : 0.0;
+      }
+    }
+    __syncthreads();
+    double x[RW];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) x[q] = lane < IB ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
+
+    TQ_PHASE(0);
+    // ---- 1. factor the panel column by column --------------------------------
+    int buf = 0;
+    for (int jj = 0; jj < IB; ++jj) {
+      const int j = c0 + jj;
+      double vj[RW];
+      double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
+#pragma unroll
+      for (int q = 0; q < RW; ++q) {
+        vj[q] = __shfl_sync(0xffffffffu, x[q], jj);
+        const int r = warp * RW + q;
+        if (TS || r > j) pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
+      }
+      S.red[buf][warp][lane] = (pp[0] + pp[1]) + (pp[2] + pp[3]);
+      if (!TS && warp == j / RW) {
+        double rv = 0.0;
+#pragma unroll
+        for (int q = 0; q < RW; ++q)
+          if (warp * RW + q == j) rv = x[q];
+        S.rowj[buf][lane] = rv;
+      }
+      __syncthreads();
+      double ps[kWarps], pd[kWarps];
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        ps[w] = S.red[buf][w][jj];
+        pd[w] = S.red[buf][w][lane];
+      }
+      const double sigma = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+      const double d = ((pd[0] + pd[1]) + (pd[2] + pd[3])) + ((pd[4] + pd[5]) + (pd[6] + pd[7]));
+      const double alpha = TS ? S.Rin[jj * LDR + jj] : S.rowj[buf][jj];
+      const double rjl = TS ? S.Rin[jj * LDR + lane] : S.rowj[buf][lane];
+      double tau = 0.0, scal = 0.0, beta = alpha;
+      if (sigma != 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, sigma));
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        // two independent correctly rounded reciprocals instead of two divisions
+        const double ib = __drcp_rn(beta);
+        scal = __drcp_rn(alpha - beta);
+        tau = (beta - alpha) * ib;
+      }
+      const double w = fma(scal, d, rjl);
+      const double tw = lane < IB ? tau * w : 0.0;
+#pragma unroll
+      for (int q = 0; q < RW; ++q) {
+        const int r = warp * RW + q;
+        if (TS || r > j) {
+          const double v = vj[q] * scal;
+          if (lane > jj) x[q] = fma(-tw, v, x[q]);
+          else if (lane == jj) x[q] = v;
+        } else if (r == j) {
+          if (lane > jj) x[q] -= tw;
+          else if (lane == jj) x[q] = beta;
+        }
+      }
+      if (TS && warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
+      if (tid == 0) S.tau[jj] = tau;
+      buf ^= 1;
+    }
+    __syncthreads();  // everyone done reading Vs (panel values) and red
+    TQ_PHASE(1);
+
+    // ---- write the factored panel: registers -> smem -> global (coalesced) ----
+#pragma unroll
+    for (int q = 0; q < RW; ++q) S.Vs[vsw(warp * RW + q, lane, LDV)] = lane < IB ? x[q] : 0.0;
+    __syncthreads();
+    for (int idx = tid; idx < NB * IB; idx += kThreads) {
+      const int c = idx / NB, r = idx - c * NB;
+      double* p = &S.Vs[vsw(r, c, LDV)];
+      const double v = *p;
+      B[r + (size_t)(c0 + c) * NB] = v;  // TSQRT: V2; GEQRT: R above/on, V below the diagonal
+      // GEQRT: the DMMA operand is the unit lower trapezoid V_p (same thread, no hazard)
+      if (!TS) *p = (r == c0 + c) ? 1.0 : (r > c0 + c ? v : 0.0);
+    }
+    if (TS) {
+      for (int idx = tid; idx < IB * IB; idx += kThreads) {
+        const int c = idx / IB, i = idx - c * IB;
+        if (i <= c) R[(c0 + i) + (size_t)(c0 + c) * NB] = S.Rout[i * LDR + c];
+      }
+    }
+
+    __syncthreads();  // GEQRT rewrote Vs in place: complete before the Gram product
+    TQ_PHASE(2);
+    // ---- 2. T_p: G = V_p^T V_p (DMMA), recurrence ---------------------------
+    {
+      const int nbk = IB / 8;
+      int blk = 0;
+      for (int mb = 0; mb < nbk; ++mb)
+        for (int nb = mb; nb < nbk; ++nb, ++blk) {
+          if (blk % kWarps != warp) continue;
+          double g0 = 0.0, g1 = 0.0;
+          const int k0 = TS ? 0 : (c0 & ~3);
+          for (int k4 = k0; k4 < NB; k4 += 4) {
+            const int r = k4 + a;
+            dmma(g0, g1, S.Vs[vsw(r, 8 * mb + g, LDV)], S.Vs[vsw(r, 8 * nb + g, LDV)]);
+          }
+          S.Gs[(8 * mb + g) * LDG + 8 * nb + 2 * a] = g0;
+          S.Gs[(8 * mb + g) * LDG + 8 * nb + 2 * a + 1] = g1;
+        }
+    }
+    __syncthreads();
+    TQ_PHASE(5);
+    // T_p in parallel: 8x8 diagonal blocks by the column recurrence, then
+    // pairwise merges T12 = -T11 G12 T22 (Q1 Q2 = I - [V1 V2] [T11 T12; 0 T22]
+    // [V1 V2]^T), log2(IB/8) levels.
+    if (tid < IB) {
+      const int b0 = tid & ~7, r = tid;
+      for (int i = b0; i < b0 + 8; ++i) {
+        double v;
+        if (i < r) {
+          v = 0.0;
+        } else if (i == r) {
+          v = S.tau[i];
+        } else {
+          double acc = 0.0;
+          for (int l = r; l < i; ++l) acc = fma(S.Ts[r + l * LDT], S.Gs[l * LDG + i], acc);
+          v = -S.tau[i] * acc;
+        }
+        S.Ts[r + i * LDT] = v;
+      }
+    }
+    __syncthreads();
+    TQ_PHASE(6);
+    for (int s = 8; s < IB; s *= 2) {
+      // X = G12 T22 for every pair (left = [st, st+s), right = [st+s, min(st+2s, IB)))
+      for (int e = tid; e < IB * IB; e += kThreads) {
+        const int i = e / IB, k = e - i * IB;  // row i (left block), column k (right block)
+        const int st = i & ~(2 * s - 1);
+        if (i < st + s && k >= st + s && k < min(st + 2 * s, IB)) {
+          double acc = 0.0;
+          for (int l = st + s; l <= k; ++l) acc = fma(S.Gs[i * LDG + l], S.Ts[l + k * LDT], acc);
+          S.Rin[i * LDR + k] = acc;  // Rin is free after the factorization: X buffer
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < IB * IB; e += kThreads) {
+        const int i = e / IB, k = e - i * IB;
+        const int st = i & ~(2 * s - 1);
+        if (i < st + s && k >= st + s && k < min(st + 2 * s, IB)) {
+          double acc = 0.0;
+          for (int l = i; l < st + s; ++l) acc = fma(S.Ts[i + l * LDT], S.Rin[l * LDR + k], acc);
+          S.Ts[i + k * LDT] = -acc;
+        } else if (i >= st + s && k < st + s && i < IB) {
+          S.Ts[i + k * LDT] = 0.0;  // strictly lower part
+        }
+      }
+      __syncthreads();
+    }
+    TQ_PHASE(7);
+    for (int e = tid; e < IB * IB; e += kThreads) {
+      const int i = e / IB, r = e - i * IB;
+      Tg[(size_t)(c0 + i) * IB + r] = (r <= i) ? S.Ts[r + i * LDT] : 0.0;
+    }
+
+    __syncthreads();
+    TQ_PHASE(3);
+    // ---- 3. trailing columns [c0+IB, NB): 8-column blocks per warp ------------
+    double* Wsw = S.Ws[warp];
+    const int nbi = IB / 8;
+    for (int cb = c0 + IB + 8 * warp; cb < NB; cb += 8 * kWarps) {
+      const int col = cb + g;
+      double acc[RB][2];
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        const double2 v = *reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)col * NB);
+        acc[rb][0] = v.x;
+        acc[rb][1] = v.y;
+      }
+      // step A: W^T(col, i) = [TS: R(c0+i, col)] + sum_r C^T(col, r) V_p(r, i)
+      double wacc[4][2];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          wacc[nb][j] = (TS && nb < nbi) ? R[(c0 + 8 * nb + 2 * a + j) + (size_t)col * NB] : 0.0;
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        if (!TS && 8 * rb + 7 < c0) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int r = 8 * rb + 2 * a + j;
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb)
+            if (nb < nbi) dmma(wacc[nb][0], wacc[nb][1], acc[rb][j], S.Vs[vsw(r, 8 * nb + g, LDV)]);
+        }
+      }
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+        if (nb < nbi) {
+          Wsw[g * LDW + 8 * nb + 2 * a] = wacc[nb][0];
+          Wsw[g * LDW + 8 * nb + 2 * a + 1] = wacc[nb][1];
+        }
+      __syncwarp();
+      // step B: W'^T = W^T T_p (descending blocks, in place); TS: R(c0+i, col) -= W'
+      for (int nb = nbi - 1; nb >= 0; --nb) {
+        double o0 = 0.0, o1 = 0.0;
+        for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
+          dmma(o0, o1, Wsw[g * LDW + k4 + a], S.Ts[(k4 + a) + (8 * nb + g) * LDT]);
+        __syncwarp();
+        Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
+        Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
+        if (TS) {
+          R[(c0 + 8 * nb + 2 * a) + (size_t)col * NB] -= o0;
+          R[(c0 + 8 * nb + 2 * a + 1) + (size_t)col * NB] -= o1;
+        }
+        __syncwarp();
+      }
+      // step C: C^T(col, r) += (-W'^T)(col, i) V_p(r, i)
+      for (int k4 = 0; k4 < IB; k4 += 4) {
+        const double af = Wsw[g * LDW + k4 + a];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          if (!TS && 8 * rb + 7 < c0) continue;
+          dmma(acc[rb][0], acc[rb][1], af, S.Vs[vsw(8 * rb + g, k4 + a, LDV)]);
+        }
+      }
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb)
+        *reinterpret_cast<double2*>(B + 8 * rb + 2 * a + (size_t)col * NB) =
+            make_double2(acc[rb][0], acc[rb][1]);
+      __syncwarp();
+    }
+    __syncthreads();  // trailing writes visible before the next panel is staged
+    TQ_PHASE(4);
+  }
+#undef TQ_PHASE
+}
+
+template <bool TS, int NB>
+int launch_fast_t(int IB, int batch, double* const* R, double* const* B, double* const* T,
+                  cudaStream_t s) {
+  auto kern = panel_fast_kernel<TS, NB>;
+  const size_t bytes = sizeof(FastSmem<NB>);
+  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  kern<<<batch, kThreads, bytes, s>>>(IB, R, B, T);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+template <bool TS>
+int launch_fast(int NB, int IB, int batch, double* const* R, double* const* B, double* const* T,
+                cudaStream_t s) {
+  switch (NB) {
+    case 32: return launch_fast_t<TS, 32>(IB, batch, R, B, T, s);
+    case 64: return launch_fast_t<TS, 64>(IB, batch, R, B, T, s);
+    case 96: return launch_fast_t<TS, 96>(IB, batch, R, B, T, s);
+    case 128: return launch_fast_t<TS, 128>(IB, batch, R, B, T, s);
+    case 160: return launch_fast_t<TS, 160>(IB, batch, R, B, T, s);
+    case 192: return launch_fast_t<TS, 192>(IB, batch, R, B, T, s);
+    case 224: return launch_fast_t<TS, 224>(IB, batch, R, B, T, s);
+    case 256: return launch_fast_t<TS, 256>(IB, batch, R, B, T, s);
+    default: return -1;
+  }
+}
+
+}  // namespace
+
+int panel_prof_read(unsigned long long* out, int reset) {
+  TQ_CUDA(cudaMemcpyFromSymbol(out, g_panel_prof, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {};
+    TQ_CUDA(cudaMemcpyToSymbol(g_panel_prof, z, sizeof z));
+  }
+  return 0;
+}
+
+bool panel_fast_supported(int NB, int IB) {
+  return NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB <= 32;
+}
+
+int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s) {
+  return launch_fast<false>(NB, IB, batch, A, nullptr, T, s);
+}
+
+int launch_tsqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
+                      double* const* T, cudaStream_t s) {
+  return launch_fast<true>(NB, IB, batch, R, A2, T, s);
+}
+
+}  // namespace tileqr

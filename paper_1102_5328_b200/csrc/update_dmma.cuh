@@ -1,0 +1,330 @@
+// update_dmma.cuh -- DMMA (FP64 tensor core) trailing-update kernel of the
+// tile QR: SSRFB (TSMQR) and LARFB (ORMQR).
+//
+// For every inner panel p of IB reflectors (ascending for Q^T, descending
+// for Q):
+//   step A  W^T  = C1[p rows]^T + C2^T V_p          (SSRFB; LARFB: C^T V_p)
+//   step B  W'^T = W^T op(T_p)^T,  C1[p rows] -= W'
+//   step C  C2^T -= W'^T V_p^T                       (LARFB: C^T -= W'^T V_p^T)
+// A CTA of 4 warps owns a column slab of one task; each warp keeps 8*MB
+// columns of C2 for ALL NB rows in registers as the transposed accumulator
+// C2^T for the whole kernel (C2 read and written exactly once).  Step A
+// feeds those accumulator registers straight back as DMMA A-fragments: the k
+// index of each m8n8k4 step is permuted to rows {2t+j} of an 8-row block so
+// that fragment == accumulator register j (no shuffles).  V_p is staged by
+// cp.async in chunks of KW <= 32 columns into a double-buffered, XOR-swizzled
+// row-major layout (conflict-free for both fragment patterns); T_p is staged
+// next to it.  Geometry (NB, MB, KW) is compile-time so that every shared
+// address is an LDS with a constant offset.
+#pragma once
+
+#include "dmma.cuh"
+#include "internal.h"
+
+namespace tileqr {
+namespace upd {
+
+constexpr int kWarps = 4;
+constexpr int kThreads = kWarps * 32;
+
+template <int KW>
+struct Geo {
+  static constexpr int LDV = (KW <= 16 ? 16 : 32) + 8;  // == 8 mod 16, >= swizzled column
+  static constexpr int LDT = (KW <= 16 ? 16 : 32) + 4;  // == 4 mod 16
+};
+
+// MULTI: IBp > 32, processed as nch chunks of KW = 32 columns (last chunk
+// zero-padded); V_p is staged twice per panel (for step A and for step C) and
+// T_p is read from global memory.
+template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI>
+__global__ void __launch_bounds__(kThreads)
+update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double* const* Tp,
+              double* const* C1p, double* const* C2p, int twobuf) {
+  constexpr int RB = NB / 8;
+  constexpr int LDV = Geo<KW>::LDV;
+  constexpr int LDT = Geo<KW>::LDT;
+  constexpr int NBK = KW / 8;            // 8-column blocks per chunk
+  constexpr int CHUNK = NB * LDV;        // doubles per V buffer
+  constexpr int TBUF = MULTI ? 0 : KW * LDT;
+  const int LDW = MULTI ? IBp + 4 : KW + 4;  // per-warp W^T row length (== 4 mod 16 when IBp % 16 == 0)
+  extern __shared__ __align__(16) double smem[];
+  // [V buf 0][V buf 1][T buf 0][T buf 1][W^T per warp] (one V/T buffer if !twobuf)
+  const int nbuf = twobuf ? 2 : 1;
+  double* const Tbase = smem + nbuf * CHUNK;
+  double* const Wsw = Tbase + nbuf * TBUF + (threadIdx.x >> 5) * 8 * MB * LDW;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int a = lane & 3, g = lane >> 2;
+  const int b = blockIdx.y;
+  const int wcol0 = (blockIdx.x * kWarps + warp) * 8 * MB;
+  const double* __restrict__ V = Vp[b];
+  const double* __restrict__ T = Tp[b];
+  double* __restrict__ C1 = LARFB ? nullptr : C1p[b];
+  double* __restrict__ C2 = C2p[b];
+
+  // ---- C2 slab -> registers: acc[mb][rb][j] = C2(8rb+2a+j, wcol0+8mb+g) ----
+  double acc[MB][RB][2];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    const int col = wcol0 + 8 * mb + g;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {
+      double2 v = make_double2(0.0, 0.0);
+      if (col < ncols) v = *reinterpret_cast<const double2*>(C2 + 8 * rb + 2 * a + (size_t)col * NB);
+      acc[mb][rb][0] = v.x;
+      acc[mb][rb][1] = v.y;
+    }
+  }
+
+  const int np = NB / IB;
+  const int nch = MULTI ? (IBp + KW - 1) / KW : 1;
+  const int nitems = MULTI ? np * 2 * nch : np;
+
+  // item -> (panel p, chunk q, phase: 0 = A only, 1 = C only, 2 = both)
+  auto item_p = [&](int idx) { int p = MULTI ? idx / (2 * nch) : idx; return TRANS ? p : np - 1 - p; };
+  auto item_q = [&](int idx) { if (!MULTI) return 0; int r = idx % (2 * nch); return r < nch ? r : r - nch; };
+  auto item_phase = [&](int idx) { if (!MULTI) return 2; return (idx % (2 * nch)) < nch ? 0 : 1; };
+
+  auto stage = [&](int idx, int slot) {
+    const int p = item_p(idx), q = item_q(idx);
+    const int c0 = p * IB;
+    double* buf = smem + slot * CHUNK;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < NB * KW; e += kThreads) {
+      const int ii = e / NB, r = e - ii * NB;
+      const int i = q * KW + ii;  // column within the panel
+      double* dst = buf + vsw(r, ii, LDV);
+      if (i >= IB) {
+        *dst = 0.0;
+      } else if (LARFB) {
+        const int col = c0 + i;
+        if (r > col) cp_async8(dst, V + r + (size_t)col * NB);
+        else *dst = (r == col) ? 1.0 : 0.0;
+      } else {
+        cp_async8(dst, V + r + (size_t)(c0 + i) * NB);
+      }
+    }
+    if (!MULTI) {
+      double* tb = Tbase + slot * TBUF;
+      for (int e = threadIdx.x; e < KW * KW; e += kThreads) {
+        const int i = e / KW, l = e - i * KW;
+        double* dst = tb + l + i * LDT;
+        if (l < IB && i < IB) cp_async8(dst, T + (size_t)c0 * IB + l + (size_t)i * IB);
+        else *dst = 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+
+  stage(0, 0);
+  for (int idx = 0; idx < nitems; ++idx) {
+    const int slot = twobuf ? (idx & 1) : 0;
+    const int p = item_p(idx), q = item_q(idx), phase = item_phase(idx);
+    const int c0 = p * IB;
+    const double* Vs = smem + slot * CHUNK;
+    if (twobuf && idx + 1 < nitems) {
+      stage(idx + 1, slot ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+
+    // ---- step A --------------------------------------------------------------
+    if (phase != 1) {
+      double wacc[MB][NBK][2];
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) {
+        const int col = wcol0 + 8 * mb + g;
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i = q * KW + 8 * nb + 2 * a + j;
+            wacc[mb][nb][j] = (!LARFB && col < ncols && i < IB) ? C1[c0 + i + (size_t)col * NB] : 0.0;
+          }
+      }
+      const int rb0 = LARFB ? (c0 >> 3) : 0;  // V_p is zero above row c0
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        if (rb < rb0) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int r = 8 * rb + 2 * a + j;
+#pragma unroll
+          for (int nb = 0; nb < NBK; ++nb) {
+            const double bf = Vs[vsw(r, 8 * nb + g, LDV)];
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) dmma(wacc[mb][nb][0], wacc[mb][nb][1], acc[mb][rb][j], bf);
+          }
+        }
+      }
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          double* w = Wsw + (8 * mb + g) * LDW + q * KW + 8 * nb + 2 * a;
+          w[0] = wacc[mb][nb][0];
+          w[1] = wacc[mb][nb][1];
+        }
+    }
+
+    // ---- step B (after the last A chunk of the panel) ------------------------
+    const bool lastA = !MULTI || (phase == 0 && q == nch - 1);
+    if (lastA) {
+      __syncwarp();
+      const int nbt = MULTI ? IBp / 8 : NBK;
+      const double* Ts = Tbase + slot * TBUF;
+      const double* Tgl = T + (size_t)c0 * IB;
+#pragma unroll
+      for (int s = 0; s < (MULTI ? 1 : NBK); ++s) {
+        // MULTI uses the runtime loop below instead
+        if (MULTI) break;
+        const int nb = TRANS ? NBK - 1 - s : s;
+        double o[MB][2];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) o[mb][0] = o[mb][1] = 0.0;
+        // TRANS: W'(:,i) = sum_{l<=i} W(:,l) T(l,i);  !TRANS: sum_{l>=i} W(:,l) T(i,l)
+#pragma unroll
+        for (int k4 = 0; k4 < KW; k4 += 4) {
+          if (TRANS ? (k4 >= 8 * nb + 8) : (k4 < 8 * nb)) continue;
+          const double bf = TRANS ? Ts[(k4 + a) + (8 * nb + g) * LDT] : Ts[(8 * nb + g) + (k4 + a) * LDT];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) dmma(o[mb][0], o[mb][1], Wsw[(8 * mb + g) * LDW + k4 + a], bf);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          const int col = wcol0 + 8 * mb + g;
+          double* w = Wsw + (8 * mb + g) * LDW + 8 * nb + 2 * a;
+          w[0] = -o[mb][0];
+          w[1] = -o[mb][1];
+          if (!LARFB && col < ncols) {
+            const int i = 8 * nb + 2 * a;
+            if (i < IB) C1[c0 + i + (size_t)col * NB] -= o[mb][0];
+            if (i + 1 < IB) C1[c0 + i + 1 + (size_t)col * NB] -= o[mb][1];
+          }
+        }
+        __syncwarp();
+      }
+      if (MULTI) {
+        for (int s = 0; s < nbt; ++s) {
+          const int nb = TRANS ? nbt - 1 - s : s;
+          double o[MB][2];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) o[mb][0] = o[mb][1] = 0.0;
+          const int kb = TRANS ? 0 : 8 * nb, ke = TRANS ? 8 * nb + 8 : IBp;
+          for (int k4 = kb; k4 < ke; k4 += 4) {
+            const int l = k4 + a, i = 8 * nb + g;
+            double bf = 0.0;
+            if (l < IB && i < IB) bf = TRANS ? __ldg(Tgl + l + (size_t)i * IB) : __ldg(Tgl + i + (size_t)l * IB);
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) dmma(o[mb][0], o[mb][1], Wsw[(8 * mb + g) * LDW + k4 + a], bf);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) {
+            const int col = wcol0 + 8 * mb + g;
+            double* w = Wsw + (8 * mb + g) * LDW + 8 * nb + 2 * a;
+            w[0] = -o[mb][0];
+            w[1] = -o[mb][1];
+            if (!LARFB && col < ncols) {
+              const int i = 8 * nb + 2 * a;
+              if (i < IB) C1[c0 + i + (size_t)col * NB] -= o[mb][0];
+              if (i + 1 < IB) C1[c0 + i + 1 + (size_t)col * NB] -= o[mb][1];
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+
+    // ---- step C --------------------------------------------------------------
+    if (phase != 0) {
+      const int rb0 = LARFB ? (c0 >> 3) : 0;
+#pragma unroll
+      for (int k4 = 0; k4 < KW; k4 += 4) {
+        double af[MB];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) af[mb] = Wsw[(8 * mb + g) * LDW + q * KW + k4 + a];
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          if (rb < rb0) continue;
+          const double bf = Vs[vsw(8 * rb + g, k4 + a, LDV)];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], af[mb], bf);
+        }
+      }
+    }
+    __syncthreads();  // buffer `slot` is restaged by the next iteration
+    if (!twobuf && idx + 1 < nitems) stage(idx + 1, 0);
+  }
+
+  // ---- registers -> C2 -------------------------------------------------------
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    const int col = wcol0 + 8 * mb + g;
+    if (col < ncols) {
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb)
+        *reinterpret_cast<double2*>(C2 + 8 * rb + 2 * a + (size_t)col * NB) =
+            make_double2(acc[mb][rb][0], acc[mb][rb][1]);
+    }
+  }
+}
+
+inline int round_up8(int x) { return (x + 7) / 8 * 8; }
+
+template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI>
+int launch_update_t(int IB, int batch, const double* const* V, const double* const* T,
+                    double* const* C1, double* const* C2, int ncols, cudaStream_t s) {
+  constexpr int LDV = Geo<KW>::LDV;
+  constexpr int LDT = Geo<KW>::LDT;
+  const int IBp = MULTI ? (round_up8(IB) + 31) / 32 * 32 : KW;
+  const int LDW = MULTI ? IBp + 4 : KW + 4;
+  // double-buffer V/T chunks when they fit in 227 KB, else single-buffer
+  const size_t vt = (size_t)NB * LDV + (MULTI ? 0 : (size_t)KW * LDT);
+  const size_t wd = (size_t)kWarps * 8 * MB * LDW;
+  int twobuf = 1;
+  size_t bytes = (2 * vt + wd) * sizeof(double);
+  if (bytes > 227 * 1024) {
+    twobuf = 0;
+    bytes = (vt + wd) * sizeof(double);
+  }
+  auto kern = update_kernel<NB, MB, KW, TRANS, LARFB, MULTI>;
+  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const int cols_per_cta = kWarps * 8 * MB;
+  dim3 grid((ncols + cols_per_cta - 1) / cols_per_cta, batch);
+  kern<<<grid, kThreads, bytes, s>>>(IB, IBp, ncols, V, T, C1, C2, twobuf);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int NB, bool TRANS, bool LARFB>
+int launch_update_nb(int IB, int batch, const double* const* V, const double* const* T,
+                     double* const* C1, double* const* C2, int ncols, cudaStream_t s) {
+  constexpr int MB = NB <= 128 ? 2 : 1;
+  const int ibp = round_up8(IB);
+  switch (ibp) {
+    case 8: return launch_update_t<NB, MB, 8, TRANS, LARFB, false>(IB, batch, V, T, C1, C2, ncols, s);
+    case 16: return launch_update_t<NB, MB, 16, TRANS, LARFB, false>(IB, batch, V, T, C1, C2, ncols, s);
+    case 24: return launch_update_t<NB, MB, 24, TRANS, LARFB, false>(IB, batch, V, T, C1, C2, ncols, s);
+    case 32: return launch_update_t<NB, MB, 32, TRANS, LARFB, false>(IB, batch, V, T, C1, C2, ncols, s);
+    default: return launch_update_t<NB, MB, 32, TRANS, LARFB, true>(IB, batch, V, T, C1, C2, ncols, s);
+  }
+}
+
+// Entry of one NB (defined in update_nb<NB>.cu): LARFB selects the GEQRT form.
+template <int NB>
+int launch_update_dmma(bool trans, bool larfb, int IB, int batch, const double* const* V,
+                       const double* const* T, double* const* C1, double* const* C2, int ncols,
+                       cudaStream_t s) {
+  if (larfb)
+    return trans ? launch_update_nb<NB, true, true>(IB, batch, V, T, C1, C2, ncols, s)
+                 : launch_update_nb<NB, false, true>(IB, batch, V, T, C1, C2, ncols, s);
+  return trans ? launch_update_nb<NB, true, false>(IB, batch, V, T, C1, C2, ncols, s)
+               : launch_update_nb<NB, false, false>(IB, batch, V, T, C1, C2, ncols, s);
+}
+
+}  // namespace upd
+}  // namespace tileqr

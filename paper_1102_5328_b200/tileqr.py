@@ -53,6 +53,9 @@ _SIGS = {
     "tileqr_dist_finalize": ([], None),
     "tileqr_rng_uniform": ([_i64, _i64, _p, _i64, _u64, _u64, _p], _i),
     "tileqr_ssrfb_impl": ([_i, _i], ctypes.c_char_p),
+    "tileqr_factor_plan": ([_i64, _i64, _i, _i, ctypes.POINTER(_i64)], _i),
+    "tileqr_set_kernel_timing": ([_i], None),
+    "tileqr_kernel_times": ([_i64, _i64, _i, _i, _i, _PD, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
     "tileqr_finalize": ([], None),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -220,6 +223,28 @@ def payg_prune(results):
     keep = (ctypes.c_int * n)()
     _check(_lib.tileqr_payg_prune(n, nb, g, keep), "tileqr_payg_prune")
     return [r for r, k in zip(results, keep) if k]
+
+
+def factor_plan(m: int, n: int, nb: int, ib: int) -> dict:
+    out = (_i64 * 8)()
+    _check(_lib.tileqr_factor_plan(m, n, nb, ib, out), "tileqr_factor_plan")
+    keys = ["levels", "launches", "geqrt", "tsqrt", "larfb", "ssrfb", "MT", "NT"]
+    return dict(zip(keys, list(out)))
+
+
+def set_kernel_timing(on: bool):
+    _lib.tileqr_set_kernel_timing(int(bool(on)))
+
+
+KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3}
+
+
+def kernel_times(m: int, n: int, nb: int, ib: int, kind: str):
+    """(total_ms, launches, tasks) of one kernel kind in the last timed factor."""
+    tot, nl, nt = _d(), _i64(), _i64()
+    _check(_lib.tileqr_kernel_times(m, n, nb, ib, KINDS[kind], ctypes.byref(tot), ctypes.byref(nl),
+                                    ctypes.byref(nt)), "tileqr_kernel_times")
+    return tot.value, nl.value, nt.value
 
 
 def finalize():
