@@ -54,21 +54,20 @@ def upper_hull(points):
 
 
 def incoming_slopes(hull):
-    """Incoming steepness of each hull point i >= 1."""
-    return [None] + [Fraction(hull[i][2] - hull[i - 1][2]) / Fraction(hull[i][0] - hull[i - 1][0])
-                     for i in range(1, len(hull))]
+    """Incoming steepness of every hull point: the slope of the hull
+    segment ending at it; the first point's segment starts at the origin (0, 0)
+    (R13: a tile of order 0 runs at 0 Gflop/s)."""
+    out = [Fraction(hull[0][2]) / Fraction(hull[0][0])]
+    return out + [Fraction(hull[i][2] - hull[i - 1][2]) / Fraction(hull[i][0] - hull[i - 1][0])
+                  for i in range(1, len(hull))]
 
 
 def heuristic1(hull, cap: int = 8):
-    """Heuristic 1: the points after the `cap` steepest hull segments.
-
-    The first hull point has no incoming segment and is not selectable unless
-    it is the only point (R13).  Ties on slope -> smaller nb.
-    """
-    if len(hull) == 1:
-        return list(hull)
+    """Heuristic 1: the points after the `cap` steepest hull segments
+    (the first point's segment starts at the origin, R13).
+    Ties on slope -> smaller nb."""
     s = incoming_slopes(hull)
-    order = sorted(range(1, len(hull)), key=lambda i: (-s[i], hull[i][0]))
+    order = sorted(range(len(hull)), key=lambda i: (-s[i], hull[i][0]))
     pick = sorted(order[:cap])
     return [hull[i] for i in pick]
 
@@ -76,14 +75,15 @@ def heuristic1(hull, cap: int = 8):
 def heuristic2(hull, cap: int = 8):
     """Heuristic 2: split [min nb, max nb] into `cap` equal
     half-open intervals (last closed) and keep, in each, the hull point with
-    the largest incoming slope (first hull point excluded, R13)."""
+    the largest incoming slope (the first point's slope from the origin,
+    DESIGN.md R13)."""
     if len(hull) == 1:
         return list(hull)
     s = incoming_slopes(hull)
     x0, x1 = Fraction(hull[0][0]), Fraction(hull[-1][0])
     width = (x1 - x0) / cap
     best = {}
-    for i in range(1, len(hull)):
+    for i in range(len(hull)):
         x = Fraction(hull[i][0])
         seg = cap - 1 if x == x1 else int((x - x0) // width)
         cur = best.get(seg)

@@ -62,14 +62,15 @@ std::vector<Pt> upper_hull(const std::vector<Pt>& pts) {
   return h;
 }
 
+// incoming steepness; the first hull point's segment starts at the origin (R13)
 long double slope_in(const std::vector<Pt>& h, size_t i) {
+  if (i == 0) return (long double)h[0].g / (long double)h[0].nb;
   return ((long double)h[i].g - h[i - 1].g) / (long double)(h[i].nb - h[i - 1].nb);
 }
 
 std::vector<Pt> heuristic1(const std::vector<Pt>& h, int cap) {
-  if (h.size() <= 1) return h;
   std::vector<size_t> idx;
-  for (size_t i = 1; i < h.size(); ++i) idx.push_back(i);
+  for (size_t i = 0; i < h.size(); ++i) idx.push_back(i);
   std::stable_sort(idx.begin(), idx.end(), [&](size_t x, size_t y) {
     const long double sx = slope_in(h, x), sy = slope_in(h, y);
     if (sx != sy) return sx > sy;
@@ -87,7 +88,7 @@ std::vector<Pt> heuristic2(const std::vector<Pt>& h, int cap) {
   const long double x0 = h.front().nb, x1 = h.back().nb;
   const long double width = (x1 - x0) / cap;
   std::map<int, size_t> best;  // segment -> hull index
-  for (size_t i = 1; i < h.size(); ++i) {
+  for (size_t i = 0; i < h.size(); ++i) {
     int seg = (h[i].nb == h.back().nb) ? cap - 1 : (int)((h[i].nb - x0) / width);
     if (seg >= cap) seg = cap - 1;
     auto it = best.find(seg);

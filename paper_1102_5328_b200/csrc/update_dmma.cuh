@@ -11,11 +11,13 @@
 // C2^T for the whole kernel (C2 read and written exactly once).  Step A
 // feeds those accumulator registers straight back as DMMA A-fragments: the k
 // index of each m8n8k4 step is permuted to rows {2t+j} of an 8-row block so
-// that fragment == accumulator register j (no shuffles).  V_p is staged by
-// cp.async in chunks of KW <= 32 columns into a double-buffered, XOR-swizzled
-// row-major layout (conflict-free for both fragment patterns); T_p is staged
-// next to it.  Geometry (NB, MB, KW) is compile-time so that every shared
-// address is an LDS with a constant offset.
+// that fragment == accumulator register j (no shuffles).
+// Per panel, V_p (in chunks of KW <= 32 columns), T_p and the IB rows of C1
+// are staged by cp.async into double buffers while the previous panel
+// computes; V_p uses an XOR-swizzled row-major layout that is bank-conflict
+// free both for the staging writes (4 rows x 8 columns per warp) and for the
+// two fragment patterns.  Geometry (NB, MB, KW) is compile-time, so every
+// shared address is an LDS/STS with a constant offset.
 #pragma once
 
 #include "dmma.cuh"
@@ -31,6 +33,16 @@ template <int KW>
 struct Geo {
   static constexpr int LDV = (KW <= 16 ? 16 : 32) + 8;  // == 8 mod 16, >= swizzled column
   static constexpr int LDT = (KW <= 16 ? 16 : 32) + 4;  // == 4 mod 16
+  static constexpr int LDC = (KW <= 16 ? 16 : 32) + 4;  // C1 rows per column, == 4 mod 16
+};
+
+// smem doubles of one stage buffer set and of the per-warp W^T
+template <int NB, int MB, int KW, bool LARFB, bool MULTI>
+struct Layout {
+  static constexpr int CHUNK = NB * Geo<KW>::LDV;
+  static constexpr int TBUF = MULTI ? 0 : KW * Geo<KW>::LDT;
+  static constexpr int CBUF = LARFB ? 0 : kWarps * 8 * MB * Geo<KW>::LDC;
+  static constexpr int STAGE = CHUNK + TBUF + CBUF;
 };
 
 // MULTI: IBp > 32, processed as nch chunks of KW = 32 columns (last chunk
@@ -40,41 +52,28 @@ template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI>
 __global__ void __launch_bounds__(kThreads)
 update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double* const* Tp,
               double* const* C1p, double* const* C2p, int twobuf) {
+  using L = Layout<NB, MB, KW, LARFB, MULTI>;
   constexpr int RB = NB / 8;
   constexpr int LDV = Geo<KW>::LDV;
   constexpr int LDT = Geo<KW>::LDT;
-  constexpr int NBK = KW / 8;            // 8-column blocks per chunk
-  constexpr int CHUNK = NB * LDV;        // doubles per V buffer
-  constexpr int TBUF = MULTI ? 0 : KW * LDT;
-  const int LDW = MULTI ? IBp + 4 : KW + 4;  // per-warp W^T row length (== 4 mod 16 when IBp % 16 == 0)
+  constexpr int LDC = Geo<KW>::LDC;
+  constexpr int NBK = KW / 8;  // 8-column blocks per chunk
+  constexpr int CPC = kWarps * 8 * MB;  // columns per CTA
+  const int LDW = MULTI ? IBp + 4 : KW + 4;  // == 4 mod 16 (IBp % 32 == 0 when MULTI)
   extern __shared__ __align__(16) double smem[];
-  // [V buf 0][V buf 1][T buf 0][T buf 1][W^T per warp] (one V/T buffer if !twobuf)
+  // [stage 0: V | T | C1][stage 1: V | T | C1][W^T per warp] (one stage if !twobuf)
   const int nbuf = twobuf ? 2 : 1;
-  double* const Tbase = smem + nbuf * CHUNK;
-  double* const Wsw = Tbase + nbuf * TBUF + (threadIdx.x >> 5) * 8 * MB * LDW;
+  double* const Wsw = smem + nbuf * L::STAGE + (threadIdx.x >> 5) * 8 * MB * LDW;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int a = lane & 3, g = lane >> 2;
   const int b = blockIdx.y;
-  const int wcol0 = (blockIdx.x * kWarps + warp) * 8 * MB;
+  const int col0 = blockIdx.x * CPC;                    // first column of this CTA
+  const int wcl0 = warp * 8 * MB;                       // first column of this warp (CTA-local)
   const double* __restrict__ V = Vp[b];
   const double* __restrict__ T = Tp[b];
   double* __restrict__ C1 = LARFB ? nullptr : C1p[b];
   double* __restrict__ C2 = C2p[b];
-
-  // ---- C2 slab -> registers: acc[mb][rb][j] = C2(8rb+2a+j, wcol0+8mb+g) ----
-  double acc[MB][RB][2];
-#pragma unroll
-  for (int mb = 0; mb < MB; ++mb) {
-    const int col = wcol0 + 8 * mb + g;
-#pragma unroll
-    for (int rb = 0; rb < RB; ++rb) {
-      double2 v = make_double2(0.0, 0.0);
-      if (col < ncols) v = *reinterpret_cast<const double2*>(C2 + 8 * rb + 2 * a + (size_t)col * NB);
-      acc[mb][rb][0] = v.x;
-      acc[mb][rb][1] = v.y;
-    }
-  }
 
   const int np = NB / IB;
   const int nch = MULTI ? (IBp + KW - 1) / KW : 1;
@@ -86,14 +85,17 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
   auto item_phase = [&](int idx) { if (!MULTI) return 2; return (idx % (2 * nch)) < nch ? 0 : 1; };
 
   auto stage = [&](int idx, int slot) {
-    const int p = item_p(idx), q = item_q(idx);
+    const int p = item_p(idx), q = item_q(idx), phase = item_phase(idx);
     const int c0 = p * IB;
-    double* buf = smem + slot * CHUNK;
+    double* vb = smem + slot * L::STAGE;
+    // V chunk: each warp instruction moves a 4-row x 8-column block
+    constexpr int RG = NB / 4;
 #pragma unroll 4
     for (int e = threadIdx.x; e < NB * KW; e += kThreads) {
-      const int ii = e / NB, r = e - ii * NB;
+      const int blk = e >> 5, l = e & 31;
+      const int r = 4 * (blk % RG) + (l & 3), ii = 8 * (blk / RG) + (l >> 2);
       const int i = q * KW + ii;  // column within the panel
-      double* dst = buf + vsw(r, ii, LDV);
+      double* dst = vb + vsw(r, ii, LDV);
       if (i >= IB) {
         *dst = 0.0;
       } else if (LARFB) {
@@ -105,7 +107,7 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
       }
     }
     if (!MULTI) {
-      double* tb = Tbase + slot * TBUF;
+      double* tb = vb + L::CHUNK;
       for (int e = threadIdx.x; e < KW * KW; e += kThreads) {
         const int i = e / KW, l = e - i * KW;
         double* dst = tb + l + i * LDT;
@@ -113,15 +115,42 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
         else *dst = 0.0;
       }
     }
+    if (!LARFB && phase != 1) {  // C1 rows c0 + q*KW + [0, KW) of the CTA's columns
+      double* cb = vb + L::CHUNK + L::TBUF;
+      for (int e = threadIdx.x; e < CPC * KW; e += kThreads) {
+        const int cl = e / KW, ii = e - cl * KW;
+        const int i = q * KW + ii, col = col0 + cl;
+        double* dst = cb + cl * LDC + ii;
+        if (i < IB && col < ncols) cp_async8(dst, C1 + c0 + i + (size_t)col * NB);
+        else *dst = 0.0;
+      }
+    }
     cp_async_commit();
   };
 
-  stage(0, 0);
+  stage(0, 0);  // first panel's operands in flight while C2 is loaded
+
+  // ---- C2 slab -> registers: acc[mb][rb][j] = C2(8rb+2a+j, col0+wcl0+8mb+g) ----
+  double acc[MB][RB][2];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    const int col = col0 + wcl0 + 8 * mb + g;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {
+      double2 v = make_double2(0.0, 0.0);
+      if (col < ncols) v = *reinterpret_cast<const double2*>(C2 + 8 * rb + 2 * a + (size_t)col * NB);
+      acc[mb][rb][0] = v.x;
+      acc[mb][rb][1] = v.y;
+    }
+  }
+
   for (int idx = 0; idx < nitems; ++idx) {
     const int slot = twobuf ? (idx & 1) : 0;
     const int p = item_p(idx), q = item_q(idx), phase = item_phase(idx);
     const int c0 = p * IB;
-    const double* Vs = smem + slot * CHUNK;
+    const double* Vs = smem + slot * L::STAGE;
+    const double* Ts = Vs + L::CHUNK;
+    const double* C1s = Vs + L::CHUNK + L::TBUF;
     if (twobuf && idx + 1 < nitems) {
       stage(idx + 1, slot ^ 1);
       cp_async_wait<1>();
@@ -134,16 +163,12 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
     if (phase != 1) {
       double wacc[MB][NBK][2];
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) {
-        const int col = wcol0 + 8 * mb + g;
+      for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
         for (int nb = 0; nb < NBK; ++nb)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int i = q * KW + 8 * nb + 2 * a + j;
-            wacc[mb][nb][j] = (!LARFB && col < ncols && i < IB) ? C1[c0 + i + (size_t)col * NB] : 0.0;
-          }
-      }
+          for (int j = 0; j < 2; ++j)
+            wacc[mb][nb][j] = LARFB ? 0.0 : C1s[(wcl0 + 8 * mb + g) * LDC + 8 * nb + 2 * a + j];
       const int rb0 = LARFB ? (c0 >> 3) : 0;  // V_p is zero above row c0
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
@@ -171,31 +196,66 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
 
     // ---- step B (after the last A chunk of the panel) ------------------------
     const bool lastA = !MULTI || (phase == 0 && q == nch - 1);
-    if (lastA) {
+    if (lastA && !MULTI) {
       __syncwarp();
-      const int nbt = MULTI ? IBp / 8 : NBK;
-      const double* Ts = Tbase + slot * TBUF;
-      const double* Tgl = T + (size_t)c0 * IB;
+      // all output blocks at once (independent DMMA chains), then write back.
+      // TRANS: W'(:,i) = sum_{l<=i} W(:,l) T(l,i);  !TRANS: sum_{l>=i} W(:,l) T(i,l)
+      double o[NBK][MB][2];
 #pragma unroll
-      for (int s = 0; s < (MULTI ? 1 : NBK); ++s) {
-        // MULTI uses the runtime loop below instead
-        if (MULTI) break;
-        const int nb = TRANS ? NBK - 1 - s : s;
+      for (int nb = 0; nb < NBK; ++nb)
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) o[nb][mb][0] = o[nb][mb][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < KW; k4 += 4) {
+        double af[MB];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) af[mb] = Wsw[(8 * mb + g) * LDW + k4 + a];
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          if (TRANS ? (k4 >= 8 * nb + 8) : (k4 < 8 * nb)) continue;
+          const double bf = TRANS ? Ts[(k4 + a) + (8 * nb + g) * LDT] : Ts[(8 * nb + g) + (k4 + a) * LDT];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) dmma(o[nb][mb][0], o[nb][mb][1], af[mb], bf);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int nb = 0; nb < NBK; ++nb)
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          const int cl = wcl0 + 8 * mb + g, col = col0 + cl;
+          double* w = Wsw + (8 * mb + g) * LDW + 8 * nb + 2 * a;
+          w[0] = -o[nb][mb][0];
+          w[1] = -o[nb][mb][1];
+          if (!LARFB && col < ncols) {
+            const int i = 8 * nb + 2 * a;
+            if (i < IB) C1[c0 + i + (size_t)col * NB] = C1s[cl * LDC + i] - o[nb][mb][0];
+            if (i + 1 < IB) C1[c0 + i + 1 + (size_t)col * NB] = C1s[cl * LDC + i + 1] - o[nb][mb][1];
+          }
+        }
+      __syncwarp();
+    }
+    if (lastA && MULTI) {
+      __syncwarp();
+      const int nbt = IBp / 8;
+      const double* Tgl = T + (size_t)c0 * IB;
+      for (int s = 0; s < nbt; ++s) {
+        const int nb = TRANS ? nbt - 1 - s : s;  // in place: descending for TRANS
         double o[MB][2];
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) o[mb][0] = o[mb][1] = 0.0;
-        // TRANS: W'(:,i) = sum_{l<=i} W(:,l) T(l,i);  !TRANS: sum_{l>=i} W(:,l) T(i,l)
-#pragma unroll
-        for (int k4 = 0; k4 < KW; k4 += 4) {
-          if (TRANS ? (k4 >= 8 * nb + 8) : (k4 < 8 * nb)) continue;
-          const double bf = TRANS ? Ts[(k4 + a) + (8 * nb + g) * LDT] : Ts[(8 * nb + g) + (k4 + a) * LDT];
+        const int kb = TRANS ? 0 : 8 * nb, ke = TRANS ? 8 * nb + 8 : IBp;
+        for (int k4 = kb; k4 < ke; k4 += 4) {
+          const int l = k4 + a, i = 8 * nb + g;
+          double bf = 0.0;
+          if (l < IB && i < IB) bf = TRANS ? __ldg(Tgl + l + (size_t)i * IB) : __ldg(Tgl + i + (size_t)l * IB);
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb) dmma(o[mb][0], o[mb][1], Wsw[(8 * mb + g) * LDW + k4 + a], bf);
         }
         __syncwarp();
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
-          const int col = wcol0 + 8 * mb + g;
+          const int col = col0 + wcl0 + 8 * mb + g;
           double* w = Wsw + (8 * mb + g) * LDW + 8 * nb + 2 * a;
           w[0] = -o[mb][0];
           w[1] = -o[mb][1];
@@ -206,36 +266,6 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
           }
         }
         __syncwarp();
-      }
-      if (MULTI) {
-        for (int s = 0; s < nbt; ++s) {
-          const int nb = TRANS ? nbt - 1 - s : s;
-          double o[MB][2];
-#pragma unroll
-          for (int mb = 0; mb < MB; ++mb) o[mb][0] = o[mb][1] = 0.0;
-          const int kb = TRANS ? 0 : 8 * nb, ke = TRANS ? 8 * nb + 8 : IBp;
-          for (int k4 = kb; k4 < ke; k4 += 4) {
-            const int l = k4 + a, i = 8 * nb + g;
-            double bf = 0.0;
-            if (l < IB && i < IB) bf = TRANS ? __ldg(Tgl + l + (size_t)i * IB) : __ldg(Tgl + i + (size_t)l * IB);
-#pragma unroll
-            for (int mb = 0; mb < MB; ++mb) dmma(o[mb][0], o[mb][1], Wsw[(8 * mb + g) * LDW + k4 + a], bf);
-          }
-          __syncwarp();
-#pragma unroll
-          for (int mb = 0; mb < MB; ++mb) {
-            const int col = wcol0 + 8 * mb + g;
-            double* w = Wsw + (8 * mb + g) * LDW + 8 * nb + 2 * a;
-            w[0] = -o[mb][0];
-            w[1] = -o[mb][1];
-            if (!LARFB && col < ncols) {
-              const int i = 8 * nb + 2 * a;
-              if (i < IB) C1[c0 + i + (size_t)col * NB] -= o[mb][0];
-              if (i + 1 < IB) C1[c0 + i + 1 + (size_t)col * NB] -= o[mb][1];
-            }
-          }
-          __syncwarp();
-        }
       }
     }
 
@@ -256,14 +286,14 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
         }
       }
     }
-    __syncthreads();  // buffer `slot` is restaged by the next iteration
+    __syncthreads();  // stage buffer `slot` is restaged by the next iteration
     if (!twobuf && idx + 1 < nitems) stage(idx + 1, 0);
   }
 
   // ---- registers -> C2 -------------------------------------------------------
 #pragma unroll
   for (int mb = 0; mb < MB; ++mb) {
-    const int col = wcol0 + 8 * mb + g;
+    const int col = col0 + wcl0 + 8 * mb + g;
     if (col < ncols) {
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb)
@@ -278,18 +308,16 @@ inline int round_up8(int x) { return (x + 7) / 8 * 8; }
 template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI>
 int launch_update_t(int IB, int batch, const double* const* V, const double* const* T,
                     double* const* C1, double* const* C2, int ncols, cudaStream_t s) {
-  constexpr int LDV = Geo<KW>::LDV;
-  constexpr int LDT = Geo<KW>::LDT;
+  using L = Layout<NB, MB, KW, LARFB, MULTI>;
   const int IBp = MULTI ? (round_up8(IB) + 31) / 32 * 32 : KW;
   const int LDW = MULTI ? IBp + 4 : KW + 4;
-  // double-buffer V/T chunks when they fit in 227 KB, else single-buffer
-  const size_t vt = (size_t)NB * LDV + (MULTI ? 0 : (size_t)KW * LDT);
   const size_t wd = (size_t)kWarps * 8 * MB * LDW;
+  // double-buffer the staged operands when they fit in 227 KB, else single-buffer
   int twobuf = 1;
-  size_t bytes = (2 * vt + wd) * sizeof(double);
+  size_t bytes = (2 * (size_t)L::STAGE + wd) * sizeof(double);
   if (bytes > 227 * 1024) {
     twobuf = 0;
-    bytes = (vt + wd) * sizeof(double);
+    bytes = ((size_t)L::STAGE + wd) * sizeof(double);
   }
   auto kern = update_kernel<NB, MB, KW, TRANS, LARFB, MULTI>;
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));

@@ -85,9 +85,10 @@ def _hull(xs, ys):
     return [(x, 1, y) for x, y in zip(xs, ys)]
 
 
-def test_heuristic1_examples():
+def test_heuristic1_examples():  # S:275-277, with reading R13 (first slope from the origin)
     h = _hull([1, 2, 3], [0.0, 0.9, 1.0])
-    assert [p[0] for p in tuner.heuristic1(h)] == [2, 3]
+    assert [p[0] for p in tuner.heuristic1(h)] == [1, 2, 3]  # |hull| <= cap: all selected
+    assert [p[0] for p in tuner.heuristic1(h, 2)] == [2, 3]  # first point: slope 0 from origin
     xs = list(range(10, 130, 10))
     ys = [0.0]
     for i in range(1, 12):
@@ -102,9 +103,17 @@ def test_heuristic2_examples():
     ys = [0, 10, 18, 24, 28, 30]
     h = _hull(xs, ys)
     assert [p[0] for p in tuner.heuristic2(h, 2)] == [80, 160]
-    assert [p[0] for p in tuner.heuristic2(h, 8)] == xs[1:]
+    assert [p[0] for p in tuner.heuristic2(h, 8)] == xs  # first point (y=0) alone in its segment
     h = _hull([10, 11, 12, 100], [0, 5, 8, 9])
     assert [p[0] for p in tuner.heuristic2(h, 1)] == [11]
+
+
+def test_first_hull_point_selectable_from_origin():
+    """Reading R13: the smallest NB carries the slope of the segment from the
+    origin, so a steep start (the usual small-N optimum) is pre-selected."""
+    h = _hull([64, 128, 224, 256], [20.0, 24.0, 22.7, 21.8])[:2]
+    assert [p[0] for p in tuner.heuristic2(h, 8)] == [64, 128]
+    assert [p[0] for p in tuner.heuristic1(h, 1)] == [64]
 
 
 def test_heuristic_caps_and_subsets():
