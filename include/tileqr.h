@@ -184,6 +184,16 @@ int tileqr_dist_local_cols(int64_t N, int NB, int* n_local);
  * (global idx = i + j*N), zero/identity padding as tileqr_factor does. */
 int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed,
                              tileqr_stream_t stream);
+/* Host-only schedule of one DAG level for `rank` of `nranks` (square MT x MT
+ * tiles), exported so the multi-GPU plan can be tested without GPUs.  Writes
+ * 5-tuples (kind, k, m, n, root) to h_out (capacity `cap` int64s): first the
+ * rank's panel tasks (kind 0 GEQRT(k), 1 TSQRT(k,m)), then the level's
+ * broadcast items (kind 4: V/T of tile (m,k) from root = k mod nranks, same
+ * list and order on every rank), then the rank's update tasks (2 LARFB(k,n),
+ * 3 SSRFB(k,m,n), n = local columns); h_counts[3] = the three counts.
+ * Errors: -1..-4 bad MT/nranks/rank/level, -6 capacity too small, -7 NULL. */
+int tileqr_dist_plan_level(int64_t MT, int nranks, int rank, int64_t level, int64_t* h_out,
+                           int64_t cap, int64_t* h_counts);
 /* Factor the distributed matrix in place; d_info as tileqr_factor. */
 int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
                        tileqr_stream_t stream);
@@ -208,10 +218,11 @@ const char* tileqr_ssrfb_impl(int NB, int IB);
  * launches per call, #GEQRT, #TSQRT, #LARFB, #SSRFB tasks, MT, NT}. */
 int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out);
 
-/* Kernel timing for measurement (bench.py): when on, tileqr_factor brackets
- * every batched launch with CUDA events on the stream it is launched on
- * (captured into the CUDA graph as event-record nodes). */
-void tileqr_set_kernel_timing(int on);
+/* Kernel timing for measurement (bench.py): bit k of `mask` (k = 0 GEQRT,
+ * 1 TSQRT, 2 LARFB, 3 SSRFB) makes tileqr_factor bracket every batched launch
+ * of that kind with CUDA events on the stream it is launched on (captured
+ * into the CUDA graph as event-record nodes); 0 turns timing off. */
+void tileqr_set_kernel_timing(int mask);
 /* After the stream of a timed tileqr_factor(M, N, NB, IB) completed: sum of
  * the launch durations of kernel kind (0 GEQRT, 1 TSQRT, 2 LARFB, 3 SSRFB) in
  * the most recent run, the number of launches and of tasks. */

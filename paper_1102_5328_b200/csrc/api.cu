@@ -120,7 +120,7 @@ struct FactorWS {
   cudaStream_t s_panel = nullptr, s_update = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaGraphExec_t graph = nullptr;
-  bool graph_timed = false;
+  int graph_timed = 0;
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
   struct Rec { int kind; int64_t tasks; cudaEvent_t a, b; };
   std::vector<Rec> recs;
@@ -140,7 +140,7 @@ struct FactorWS {
 static std::mutex g_mu;
 static std::map<std::tuple<int, int64_t, int64_t, int, int>, std::unique_ptr<FactorWS>> g_ws;
 
-static bool g_timing = false;
+static int g_timing = 0;  // bit k: time launches of kernel kind k
 
 static bool use_graph() {
   const char* e = getenv("TILEQR_NO_GRAPH");
@@ -253,7 +253,8 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
 // With kernel timing on, every launch is bracketed by two events (captured as
 // event-record nodes when the sequence is captured into the graph).
 static int timed_begin(FactorWS* ws, int kind, int64_t tasks, cudaStream_t st, size_t* slot) {
-  if (!g_timing) return 0;
+  *slot = (size_t)-1;
+  if (!(g_timing & (1 << kind))) return 0;
   if (ws->rec_used == ws->recs.size()) {
     FactorWS::Rec r{kind, tasks, nullptr, nullptr};
     TQ_CUDA(cudaEventCreate(&r.a));
@@ -267,7 +268,7 @@ static int timed_begin(FactorWS* ws, int kind, int64_t tasks, cudaStream_t st, s
   return 0;
 }
 static int timed_end(FactorWS* ws, size_t slot, cudaStream_t st) {
-  if (!g_timing) return 0;
+  if (slot == (size_t)-1) return 0;
   TQ_CUDA(cudaEventRecordWithFlags(ws->recs[slot].b, st, cudaEventRecordExternal));
   return 0;
 }
@@ -620,9 +621,9 @@ int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out) {
   return 0;
 }
 
-void tileqr_set_kernel_timing(int on) {
+void tileqr_set_kernel_timing(int mask) {
   std::lock_guard<std::mutex> lock(g_mu);
-  g_timing = on != 0;
+  g_timing = mask & 15;
 }
 
 int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,

@@ -1,24 +1,383 @@
-// dist.cu -- multi-GPU tile QR (placeholder until the NCCL path lands).
+// dist.cu -- multi-GPU tile QR: tile columns 1D block-cyclic over the ranks
+// (one process per GPU), panel V/T tiles broadcast with NCCL over NVLink
+// (J:north_star).
+//
+// Tile column n lives on rank n mod P, stored locally as MT tiles per local
+// column (local column j <-> global n = rank + j*P).  The DAG levels are the
+// single-GPU closed form (api.cu).  Per level t:
+//   panel stream : GEQRT(k) [3k == t] and TSQRT(k,m) [2k+m == t] on owner(k)
+//                  (their inputs are local: column k is owned by owner(k));
+//                  the owner copies V_kk (whose upper part the next TSQRT
+//                  rewrites) into its panel buffer.
+//   comm stream  : after the level's panel kernels, ONE grouped set of
+//                  ncclBroadcast calls, one per new V tile and T tile, from
+//                  owner(k) into every rank's per-panel receive buffer
+//                  pbuf[k][m-k] / pT[k][m-k] (written exactly once).
+//   update stream: LARFB(k,n) [3k+1 == t] and SSRFB(k,m,n) [2k+m+1 == t] for
+//                  the LOCAL columns n, reading V/T from the panel buffers;
+//                  it waits for the broadcasts of level t-1, the panel stream
+//                  of level t waits for the updates of level t-1.
+// Every tile sees the same kernel sequence with the same inputs as in
+// tileqr_factor, so R, V and T are bitwise identical for any P.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <memory>
+#include <string>
+#include <vector>
+
 #include "internal.h"
+
+namespace tileqr {
+
+int launch_dist_fill(int64_t N, int NB, int64_t MT, int nranks, int rank, int64_t nloc, double* A,
+                     uint64_t seed, cudaStream_t s);
+int launch_nonfinite_check(const double* A, int64_t n, int* d_info, cudaStream_t s);
+
+namespace {
+
+#define TQ_NCCL(call)                                                                   \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess) {                                                            \
+      char b_[256];                                                                     \
+      snprintf(b_, sizeof b_, "NCCL error %s in %s", ncclGetErrorString(r_), #call);    \
+      set_error(b_);                                                                    \
+      return TILEQR_ERR_NCCL;                                                           \
+    }                                                                                   \
+  } while (0)
+
+// A planned task of one rank at one level.  kind: 0 GEQRT(k), 1 TSQRT(k,m),
+// 2 LARFB(k,n), 3 SSRFB(k,m,n), 4 broadcast of V/T (k,m) from root.
+struct Task {
+  int kind;
+  int64_t k, m, n;
+  int root;
+};
+
+int64_t dist_levels(int64_t MT) { return MT <= 0 ? 0 : 3 * MT - 2; }
+
+// Host plan of level t for `rank` (square MT x MT tile matrix).
+void plan_level(int64_t MT, int P, int rank, int64_t t, std::vector<Task>& panel,
+                std::vector<Task>& bcast, std::vector<Task>& update) {
+  panel.clear();
+  bcast.clear();
+  update.clear();
+  // panel tasks and the broadcasts they feed (same order on every rank)
+  if (t % 3 == 0 && t / 3 < MT) {
+    const int64_t k = t / 3;
+    if ((int)(k % P) == rank) panel.push_back({0, k, k, k, (int)(k % P)});
+    bcast.push_back({4, k, k, -1, (int)(k % P)});
+  }
+  for (int64_t k = 0; k < MT; ++k) {
+    const int64_t m = t - 2 * k;
+    if (m <= k) break;
+    if (m >= MT) continue;
+    if ((int)(k % P) == rank) panel.push_back({1, k, m, k, (int)(k % P)});
+    bcast.push_back({4, k, m, -1, (int)(k % P)});
+  }
+  // update tasks on local columns
+  if ((t - 1) % 3 == 0 && t >= 1) {
+    const int64_t k = (t - 1) / 3;
+    if (k < MT)
+      for (int64_t n = k + 1; n < MT; ++n)
+        if ((int)(n % P) == rank) update.push_back({2, k, k, n, -1});
+  }
+  for (int64_t k = 0; k < MT; ++k) {
+    const int64_t m = t - 1 - 2 * k;
+    if (m <= k) break;
+    if (m >= MT) continue;
+    for (int64_t n = k + 1; n < MT; ++n)
+      if ((int)(n % P) == rank) update.push_back({3, k, m, n, -1});
+  }
+}
+
+struct LevelPlan {
+  // offsets into the device pointer array and counts, per level
+  size_t oG, oT, oL, oS;
+  int nG, nT, nL, nS;
+  std::vector<Task> panel, bcast;  // host copies (owner snapshots + broadcasts)
+};
+
+struct DistState {
+  bool init = false;
+  int nranks = 0, rank = 0, device = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t sp = nullptr, su = nullptr, sc = nullptr;
+  cudaEvent_t ep = nullptr, eu = nullptr, ec = nullptr, e0 = nullptr;
+  // cached workspace of one shape
+  int64_t N = -1;
+  int NB = 0, IB = 0;
+  double* A_cached = nullptr;
+  double* T_cached = nullptr;
+  double* pbuf = nullptr;  // V tiles of every panel: slot(k, m) = off(k) + (m - k)
+  double* pT = nullptr;    // T tiles of every panel
+  void** dptr = nullptr;   // all levels' pointer arrays
+  std::vector<LevelPlan> plan;
+};
+
+DistState g_d;
+
+int64_t slot_off(int64_t MT, int64_t k) { return k * MT - k * (k - 1) / 2; }
+
+void free_shape() {
+  cudaFree(g_d.pbuf);
+  cudaFree(g_d.pT);
+  cudaFree(g_d.dptr);
+  g_d.pbuf = nullptr;
+  g_d.pT = nullptr;
+  g_d.dptr = nullptr;
+  g_d.plan.clear();
+  g_d.N = -1;
+}
+
+}  // namespace
+}  // namespace tileqr
 
 using namespace tileqr;
 
 extern "C" {
-int tileqr_dist_unique_id(void* h_id) { (void)h_id; set_error("dist: not built"); return TILEQR_ERR_NOT_INIT; }
-int tileqr_dist_init(int nranks, int rank, const void* id, int device) {
-  (void)nranks; (void)rank; (void)id; (void)device;
-  set_error("dist: not built");
-  return TILEQR_ERR_NOT_INIT;
+
+int tileqr_dist_unique_id(void* h_id) {
+  if (!h_id) return -1;
+  ncclUniqueId id;
+  TQ_NCCL(ncclGetUniqueId(&id));
+  memcpy(h_id, &id, sizeof id);
+  return 0;
 }
-int tileqr_dist_local_cols(int64_t N, int NB, int* n_local) { (void)N; (void)NB; (void)n_local; return TILEQR_ERR_NOT_INIT; }
-int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed, tileqr_stream_t s) {
-  (void)N; (void)NB; (void)A_local; (void)seed; (void)s;
-  return TILEQR_ERR_NOT_INIT;
+
+int tileqr_dist_init(int nranks, int rank, const void* h_nccl_unique_id, int device) {
+  if (nranks < 1) return -1;
+  if (rank < 0 || rank >= nranks) return -2;
+  if (!h_nccl_unique_id) return -3;
+  if (device < 0) return -4;
+  if (g_d.init) tileqr_dist_finalize();
+  TQ_CUDA(cudaSetDevice(device));
+  ncclUniqueId id;
+  memcpy(&id, h_nccl_unique_id, sizeof id);
+  TQ_NCCL(ncclCommInitRank(&g_d.comm, nranks, id, rank));
+  int lo = 0, hi = 0;
+  TQ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  TQ_CUDA(cudaStreamCreateWithPriority(&g_d.sp, cudaStreamNonBlocking, hi));
+  TQ_CUDA(cudaStreamCreateWithPriority(&g_d.su, cudaStreamNonBlocking, lo));
+  TQ_CUDA(cudaStreamCreateWithPriority(&g_d.sc, cudaStreamNonBlocking, hi));
+  for (cudaEvent_t* e : {&g_d.ep, &g_d.eu, &g_d.ec, &g_d.e0})
+    TQ_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  g_d.nranks = nranks;
+  g_d.rank = rank;
+  g_d.device = device;
+  g_d.init = true;
+  return 0;
 }
+
+int tileqr_dist_local_cols(int64_t N, int NB, int* n_local) {
+  if (N < 0) return -1;
+  if (NB < 1 || NB > 512) return -2;
+  if (!n_local) return -3;
+  if (!g_d.init) {
+    set_error("tileqr_dist_local_cols: tileqr_dist_init not called");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  const int64_t NT = (N + NB - 1) / NB;
+  *n_local = (int)((NT - g_d.rank + g_d.nranks - 1) / g_d.nranks);
+  if (NT <= g_d.rank) *n_local = 0;
+  return 0;
+}
+
+int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed,
+                             tileqr_stream_t stream) {
+  if (N < 0) return -1;
+  if (NB < 1 || NB > 512) return -2;
+  if (!g_d.init) {
+    set_error("tileqr_dist_fill_uniform: tileqr_dist_init not called");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  int nloc = 0;
+  int rc = tileqr_dist_local_cols(N, NB, &nloc);
+  if (rc) return rc;
+  if (nloc == 0 || N == 0) return 0;
+  if (!A_local) return -3;
+  const int64_t MT = (N + NB - 1) / NB;
+  return launch_dist_fill(N, NB, MT, g_d.nranks, g_d.rank, nloc, A_local, seed,
+                          reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Host-only plan of one level, exported for CPU tests of the schedule:
+// writes tuples (kind, k, m, n, root) for the panel tasks, then the broadcast
+// items, then the update tasks of `rank`; counts in h_counts[3].
+int tileqr_dist_plan_level(int64_t MT, int nranks, int rank, int64_t level, int64_t* h_out,
+                           int64_t cap, int64_t* h_counts) {
+  if (MT < 0) return -1;
+  if (nranks < 1) return -2;
+  if (rank < 0 || rank >= nranks) return -3;
+  if (level < 0) return -4;
+  if (!h_counts) return -7;
+  std::vector<Task> p, b, u;
+  plan_level(MT, nranks, rank, level, p, b, u);
+  h_counts[0] = (int64_t)p.size();
+  h_counts[1] = (int64_t)b.size();
+  h_counts[2] = (int64_t)u.size();
+  const int64_t need = 5 * (int64_t)(p.size() + b.size() + u.size());
+  if (need > cap || (!h_out && need > 0)) return -6;
+  int64_t o = 0;
+  for (auto* v : {&p, &b, &u})
+    for (const Task& t : *v) {
+      h_out[o++] = t.kind;
+      h_out[o++] = t.k;
+      h_out[o++] = t.m;
+      h_out[o++] = t.n;
+      h_out[o++] = t.root;
+    }
+  return 0;
+}
+
 int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
-                       tileqr_stream_t s) {
-  (void)N; (void)A_local; (void)NB; (void)IB; (void)T_local; (void)d_info; (void)s;
-  return TILEQR_ERR_NOT_INIT;
+                       tileqr_stream_t stream) {
+  if (N < 0) return -1;
+  if (NB < 1 || NB > 512) return -3;
+  if (IB < 1 || IB > NB || NB % IB) return -4;
+  if (!g_d.init) {
+    set_error("tileqr_dist_factor: tileqr_dist_init not called");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_info) {
+    int rc = launch_zero_int(d_info, s);
+    if (rc) return rc;
+  }
+  if (N == 0) return 0;
+  const int P = g_d.nranks, me = g_d.rank;
+  const int64_t MT = (N + NB - 1) / NB;
+  int nloc = 0;
+  tileqr_dist_local_cols(N, NB, &nloc);
+  if (nloc > 0 && !A_local) return -2;
+  if (nloc > 0 && !T_local) return -5;
+  const size_t tile = (size_t)NB * NB, ttile = (size_t)IB * NB;
+  auto loc = [&](int64_t m, int64_t n) { return A_local + (size_t)(m + (n / P) * MT) * tile; };
+  auto locT = [&](int64_t m, int64_t n) { return T_local + (size_t)(m + (n / P) * MT) * ttile; };
+  auto pv = [&](int64_t k, int64_t m) { return g_d.pbuf + (size_t)(slot_off(MT, k) + (m - k)) * tile; };
+  auto pt = [&](int64_t k, int64_t m) { return g_d.pT + (size_t)(slot_off(MT, k) + (m - k)) * ttile; };
+  const int64_t nlev = dist_levels(MT);
+
+  // ---- per-shape workspace: panel buffers and every level's pointer arrays ----
+  if (g_d.N != N || g_d.NB != NB || g_d.IB != IB || g_d.A_cached != A_local || g_d.T_cached != T_local) {
+    free_shape();
+    const int64_t nslots = slot_off(MT, MT);
+    if (cudaMalloc(&g_d.pbuf, nslots * tile * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&g_d.pT, nslots * ttile * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      free_shape();
+      set_error("tileqr_dist_factor: panel buffer allocation failed");
+      return TILEQR_ERR_ALLOC;
+    }
+    std::vector<void*> hp;
+    std::vector<Task> panel, bc, upd;
+    g_d.plan.resize(nlev);
+    for (int64_t t = 0; t < nlev; ++t) {
+      plan_level(MT, P, me, t, panel, bc, upd);
+      LevelPlan& L = g_d.plan[t];
+      L.panel = panel;
+      L.bcast = bc;
+      std::vector<void*> gA, gT, tR, tA, tT, lV, lT, lC, sV, sT, s1, s2;
+      for (const Task& q : panel) {
+        if (q.kind == 0) { gA.push_back(loc(q.k, q.k)); gT.push_back(locT(q.k, q.k)); }
+        else { tR.push_back(loc(q.k, q.k)); tA.push_back(loc(q.m, q.k)); tT.push_back(locT(q.m, q.k)); }
+      }
+      for (const Task& q : upd) {
+        if (q.kind == 2) { lV.push_back(pv(q.k, q.k)); lT.push_back(pt(q.k, q.k)); lC.push_back(loc(q.k, q.n)); }
+        else { sV.push_back(pv(q.k, q.m)); sT.push_back(pt(q.k, q.m)); s1.push_back(loc(q.k, q.n)); s2.push_back(loc(q.m, q.n)); }
+      }
+      auto put = [&](std::vector<void*>& v) { size_t o = hp.size(); hp.insert(hp.end(), v.begin(), v.end()); return o; };
+      L.nG = (int)gA.size(); L.oG = put(gA); put(gT);
+      L.nT = (int)tR.size(); L.oT = put(tR); put(tA); put(tT);
+      L.nL = (int)lV.size(); L.oL = put(lV); put(lT); put(lC);
+      L.nS = (int)sV.size(); L.oS = put(sV); put(sT); put(s1); put(s2);
+    }
+    if (cudaMalloc(&g_d.dptr, std::max<size_t>(hp.size(), 1) * sizeof(void*)) != cudaSuccess) {
+      cudaGetLastError();
+      free_shape();
+      set_error("tileqr_dist_factor: task list allocation failed");
+      return TILEQR_ERR_ALLOC;
+    }
+    TQ_CUDA(cudaMemcpy(g_d.dptr, hp.data(), hp.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    g_d.N = N;
+    g_d.NB = NB;
+    g_d.IB = IB;
+    g_d.A_cached = A_local;
+    g_d.T_cached = T_local;
+  }
+  if (nloc > 0 && d_info) {
+    int rc = launch_nonfinite_check(A_local, (int64_t)nloc * MT * tile, d_info, s);
+    if (rc) return rc;
+  }
+
+  // the three internal streams start after the caller's prior work
+  TQ_CUDA(cudaEventRecord(g_d.e0, s));
+  for (cudaStream_t st : {g_d.sp, g_d.su, g_d.sc}) TQ_CUDA(cudaStreamWaitEvent(st, g_d.e0, 0));
+  double** d = reinterpret_cast<double**>(g_d.dptr);
+  for (int64_t t = 0; t < nlev; ++t) {
+    const LevelPlan& L = g_d.plan[t];
+    // panel(t) after update(t-1); update(t) after the broadcasts of level t-1
+    if (t > 0) {
+      TQ_CUDA(cudaEventRecord(g_d.eu, g_d.su));
+      TQ_CUDA(cudaStreamWaitEvent(g_d.sp, g_d.eu, 0));
+      TQ_CUDA(cudaEventRecord(g_d.ec, g_d.sc));
+      TQ_CUDA(cudaStreamWaitEvent(g_d.su, g_d.ec, 0));
+    }
+    int rc;
+    // ---- panel kernels on the owner, snapshot of V_kk into its panel slot ----
+    if (L.nG && (rc = launch_geqrt(NB, IB, L.nG, d + L.oG, d + L.oG + L.nG, g_d.sp))) return rc;
+    if (L.nT && (rc = launch_tsqrt(NB, IB, L.nT, d + L.oT, d + L.oT + L.nT, d + L.oT + 2 * L.nT, g_d.sp))) return rc;
+    for (const Task& q : L.panel)
+      if (q.kind == 0)  // before TSQRT(k, k+1) rewrites the upper part of tile (k, k)
+        TQ_CUDA(cudaMemcpyAsync(pv(q.k, q.k), loc(q.k, q.k), tile * sizeof(double),
+                                cudaMemcpyDeviceToDevice, g_d.sp));
+    // ---- one grouped broadcast of this level's new V/T tiles -----------------
+    if (!L.bcast.empty()) {
+      TQ_CUDA(cudaEventRecord(g_d.ep, g_d.sp));
+      TQ_CUDA(cudaStreamWaitEvent(g_d.sc, g_d.ep, 0));
+      TQ_NCCL(ncclGroupStart());
+      for (const Task& q : L.bcast) {
+        const bool root = q.root == me;
+        const double* sv = root ? (q.m == q.k ? pv(q.k, q.k) : loc(q.m, q.k)) : pv(q.k, q.m);
+        const double* st = root ? locT(q.m, q.k) : pt(q.k, q.m);
+        TQ_NCCL(ncclBroadcast(sv, pv(q.k, q.m), tile, ncclDouble, q.root, g_d.comm, g_d.sc));
+        TQ_NCCL(ncclBroadcast(st, pt(q.k, q.m), ttile, ncclDouble, q.root, g_d.comm, g_d.sc));
+      }
+      TQ_NCCL(ncclGroupEnd());
+    }
+    // ---- update kernels on the local columns ---------------------------------
+    if (L.nL && (rc = launch_larfb(true, NB, IB, L.nL, d + L.oL, d + L.oL + L.nL, d + L.oL + 2 * L.nL, NB, g_d.su)))
+      return rc;
+    if (L.nS && (rc = launch_ssrfb(true, NB, IB, L.nS, d + L.oS, d + L.oS + L.nS, d + L.oS + 2 * L.nS,
+                                   d + L.oS + 3 * L.nS, NB, g_d.su)))
+      return rc;
+  }
+  // join into the caller's stream
+  for (cudaStream_t st : {g_d.sp, g_d.su, g_d.sc}) {
+    TQ_CUDA(cudaEventRecord(g_d.e0, st));
+    TQ_CUDA(cudaStreamWaitEvent(s, g_d.e0, 0));
+  }
+  return 0;
 }
-void tileqr_dist_finalize(void) {}
+
+void tileqr_dist_finalize(void) {
+  if (!g_d.init) return;
+  cudaDeviceSynchronize();
+  free_shape();
+  if (g_d.comm) ncclCommDestroy(g_d.comm);
+  for (cudaStream_t st : {g_d.sp, g_d.su, g_d.sc})
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t e : {g_d.ep, g_d.eu, g_d.ec, g_d.e0})
+    if (e) cudaEventDestroy(e);
+  g_d.comm = nullptr;
+  g_d.sp = g_d.su = g_d.sc = nullptr;
+  g_d.ep = g_d.eu = g_d.ec = g_d.e0 = nullptr;
+  g_d.A_cached = g_d.T_cached = nullptr;
+  g_d.init = false;
 }
+
+}  // extern "C"

@@ -120,6 +120,41 @@ rng_uniform_kernel(int64_t M, int64_t N, double* __restrict__ A, int64_t lda, ui
 
 __global__ void zero_int_kernel(int* p) { *p = 0; }
 
+// Local tile columns of a 1D block-cyclic N x N matrix (dist path): local
+// column j holds global tile column n = rank + j*P; element (il, jl) of tile
+// (m, n) is the generator's value at global (i, c) = (m*NB+il, n*NB+jl),
+// idx = i + c*N, with the same padding as layout_to_tiles.
+__global__ void __launch_bounds__(kThreads)
+dist_fill_kernel(int64_t N, int NB, int64_t MT, int P, int rank, int64_t nloc, double* __restrict__ A,
+                 uint64_t key) {
+  const int64_t tile = (int64_t)NB * NB;
+  const int64_t total = nloc * MT * tile;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = w / tile, e = w - t * tile;
+    const int64_t m = t % MT, j = t / MT;
+    const int64_t jl = e / NB, il = e - jl * NB;
+    const int64_t i = m * NB + il, c = (rank + j * P) * NB + jl;
+    double v;
+    if (i < N && c < N) {
+      const uint64_t bits = splitmix64(key + (uint64_t)(i + c * N)) >> 11;
+      v = (double)bits * 0x1.0p-53 - 0.5;
+    } else {
+      v = (c >= N && i == c) ? 1.0 : 0.0;
+    }
+    A[w] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+nonfinite_kernel(const double* __restrict__ A, int64_t n, int* d_info) {
+  int bad = 0;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n;
+       w += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(A[w])) bad = 1;
+  if (bad) *d_info = 1;
+}
+
 uint64_t host_splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -159,6 +194,20 @@ int launch_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t se
   if (M <= 0 || N <= 0) return 0;
   rng_uniform_kernel<<<grid_for(M * N), kThreads, 0, s>>>(M, N, A, lda, host_splitmix64(seed),
                                                           offset);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_dist_fill(int64_t N, int NB, int64_t MT, int nranks, int rank, int64_t nloc, double* A,
+                     uint64_t seed, cudaStream_t s) {
+  dist_fill_kernel<<<grid_for(nloc * MT * NB * NB), kThreads, 0, s>>>(N, NB, MT, nranks, rank, nloc, A,
+                                                                      host_splitmix64(seed));
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_nonfinite_check(const double* A, int64_t n, int* d_info, cudaStream_t s) {
+  nonfinite_kernel<<<grid_for(n), kThreads, 0, s>>>(A, n, d_info);
   TQ_LAUNCH_CHECK();
   return 0;
 }

@@ -84,12 +84,29 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
   auto item_q = [&](int idx) { if (!MULTI) return 0; int r = idx % (2 * nch); return r < nch ? r : r - nch; };
   auto item_phase = [&](int idx) { if (!MULTI) return 2; return (idx % (2 * nch)) < nch ? 0 : 1; };
 
+  // Per-thread constants of the fast V staging (SSRFB, one chunk per panel):
+  // warp instruction `it` moves rows 4*((4*it % RG) + warp) + [0,4) of columns
+  // 8*(4*it / RG) + [0,8); the swizzle of those rows is a per-thread constant.
+  constexpr int RG = NB / 4;  // 4-row groups (NB % 16 == 0, so RG % 4 == 0)
+  const int st_r = 4 * warp + (lane & 3), st_c = lane >> 2;
+  const int st_sw = (((st_r >> 1) & 3) << 2);
   auto stage = [&](int idx, int slot) {
     const int p = item_p(idx), q = item_q(idx), phase = item_phase(idx);
     const int c0 = p * IB;
     double* vb = smem + slot * L::STAGE;
+    if (!LARFB && !MULTI) {
+      const double* src = V + (size_t)c0 * NB + st_r + (size_t)st_c * NB;
+      double* dst = vb + st_r * LDV + (st_c ^ st_sw);
+#pragma unroll
+      for (int it = 0; it < NB * KW / kThreads; ++it) {
+        const int rg0 = (4 * it) % RG, cg = (4 * it) / RG;  // compile-time
+        const int ii = 8 * cg + st_c;
+        double* d = dst + 4 * rg0 * LDV + (((8 * cg) ^ (st_c ^ st_sw)) - (st_c ^ st_sw));
+        if (ii < IB) cp_async8(d, src + 4 * rg0 + (size_t)(8 * cg) * NB);
+        else *d = 0.0;
+      }
+    } else {
     // V chunk: each warp instruction moves a 4-row x 8-column block
-    constexpr int RG = NB / 4;
 #pragma unroll 4
     for (int e = threadIdx.x; e < NB * KW; e += kThreads) {
       const int blk = e >> 5, l = e & 31;
@@ -105,6 +122,7 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
       } else {
         cp_async8(dst, V + r + (size_t)(c0 + i) * NB);
       }
+    }
     }
     if (!MULTI) {
       double* tb = vb + L::CHUNK;
@@ -161,29 +179,49 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
 
     // ---- step A --------------------------------------------------------------
     if (phase != 1) {
-      double wacc[MB][NBK][2];
+      // two partial sums per output block (k rows 2t and 2t+1 of each 8-row
+      // block) so that every DMMA chain has 2*MB*NBK independent links
+      double wacc[MB][NBK][2], wacc2[MB][NBK][2];
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
         for (int nb = 0; nb < NBK; ++nb)
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
+          for (int j = 0; j < 2; ++j) {
             wacc[mb][nb][j] = LARFB ? 0.0 : C1s[(wcl0 + 8 * mb + g) * LDC + 8 * nb + 2 * a + j];
+            wacc2[mb][nb][j] = 0.0;
+          }
       const int rb0 = LARFB ? (c0 >> 3) : 0;  // V_p is zero above row c0
+      // B-fragment (row 8rb+2a+j, column 8nb+g): its swizzle is 4a for every rb,
+      // so one per-thread base per (j, nb) and a compile-time offset per rb.
+      const double* pa[2][NBK];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) pa[j][nb] = Vs + (2 * a + j) * LDV + ((8 * nb + g) ^ (4 * a));
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         if (rb < rb0) continue;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int r = 8 * rb + 2 * a + j;
 #pragma unroll
           for (int nb = 0; nb < NBK; ++nb) {
-            const double bf = Vs[vsw(r, 8 * nb + g, LDV)];
+            const double bf = pa[j][nb][8 * rb * LDV];
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb) dmma(wacc[mb][nb][0], wacc[mb][nb][1], acc[mb][rb][j], bf);
+            for (int mb = 0; mb < MB; ++mb) {
+              if (j == 0) dmma(wacc[mb][nb][0], wacc[mb][nb][1], acc[mb][rb][0], bf);
+              else dmma(wacc2[mb][nb][0], wacc2[mb][nb][1], acc[mb][rb][1], bf);
+            }
           }
         }
       }
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          wacc[mb][nb][0] += wacc2[mb][nb][0];
+          wacc[mb][nb][1] += wacc2[mb][nb][1];
+        }
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
@@ -272,15 +310,19 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
     // ---- step C --------------------------------------------------------------
     if (phase != 0) {
       const int rb0 = LARFB ? (c0 >> 3) : 0;
+      // B-fragment (row 8rb+g, column k4+a): swizzle 4*(g>>1) for every rb
+      const double* pc = Vs + g * LDV;
+      const int sw = 4 * (g >> 1);
 #pragma unroll
       for (int k4 = 0; k4 < KW; k4 += 4) {
         double af[MB];
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) af[mb] = Wsw[(8 * mb + g) * LDW + q * KW + k4 + a];
+        const double* pck = pc + ((k4 + a) ^ sw);
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
           if (rb < rb0) continue;
-          const double bf = Vs[vsw(8 * rb + g, k4 + a, LDV)];
+          const double bf = pck[8 * rb * LDV];
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], af[mb], bf);
         }

@@ -50,6 +50,7 @@ _SIGS = {
     "tileqr_dist_local_cols": ([_i64, _i, _PI], _i),
     "tileqr_dist_fill_uniform": ([_i64, _i, _p, _u64, _p], _i),
     "tileqr_dist_factor": ([_i64, _p, _i, _i, _p, _p, _p], _i),
+    "tileqr_dist_plan_level": ([_i64, _i, _i, _i64, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)], _i),
     "tileqr_dist_finalize": ([], None),
     "tileqr_rng_uniform": ([_i64, _i64, _p, _i64, _u64, _u64, _p], _i),
     "tileqr_ssrfb_impl": ([_i, _i], ctypes.c_char_p),
@@ -232,11 +233,13 @@ def factor_plan(m: int, n: int, nb: int, ib: int) -> dict:
     return dict(zip(keys, list(out)))
 
 
-def set_kernel_timing(on: bool):
-    _lib.tileqr_set_kernel_timing(int(bool(on)))
-
-
 KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3}
+
+
+def set_kernel_timing(on, kinds=("geqrt", "tsqrt", "larfb", "ssrfb")):
+    """Enable CUDA-event timing of the given kernel kinds (False/0: off)."""
+    mask = 0 if not on else sum(1 << KINDS[k] for k in kinds)
+    _lib.tileqr_set_kernel_timing(mask)
 
 
 def kernel_times(m: int, n: int, nb: int, ib: int, kind: str):
@@ -249,3 +252,50 @@ def kernel_times(m: int, n: int, nb: int, ib: int, kind: str):
 
 def finalize():
     _lib.tileqr_finalize()
+
+
+# ---------------------------------------------------------------------------
+# multi-GPU (one process per GPU; 1D block-cyclic tile columns)
+# ---------------------------------------------------------------------------
+def dist_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.tileqr_dist_unique_id(buf), "tileqr_dist_unique_id")
+    return buf.raw
+
+
+def dist_init(nranks: int, rank: int, unique_id: bytes, device: int):
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _check(_lib.tileqr_dist_init(nranks, rank, buf, device), "tileqr_dist_init")
+
+
+def dist_local_cols(n: int, nb: int) -> int:
+    out = ctypes.c_int()
+    _check(_lib.tileqr_dist_local_cols(n, nb, ctypes.byref(out)), "tileqr_dist_local_cols")
+    return out.value
+
+
+def dist_fill_uniform(n: int, nb: int, A_local: torch.Tensor, seed: int, stream=None):
+    _check(_lib.tileqr_dist_fill_uniform(n, nb, A_local.data_ptr(), seed, _stream(stream)),
+           "tileqr_dist_fill_uniform")
+
+
+def dist_factor(n: int, A_local: torch.Tensor, nb: int, ib: int, T_local: torch.Tensor,
+                info: torch.Tensor | None = None, stream=None):
+    _check(_lib.tileqr_dist_factor(n, A_local.data_ptr(), nb, ib, T_local.data_ptr(),
+                                   info.data_ptr() if info is not None else None, _stream(stream)),
+           "tileqr_dist_factor")
+
+
+def dist_finalize():
+    _lib.tileqr_dist_finalize()
+
+
+def dist_plan_level(mt: int, nranks: int, rank: int, level: int):
+    """Host-only plan of one level: (panel, bcast, update) lists of
+    (kind, k, m, n, root) tuples."""
+    cap = 5 * (mt * mt + 4 * mt + 8)
+    out = (_i64 * cap)()
+    cnt = (_i64 * 3)()
+    _check(_lib.tileqr_dist_plan_level(mt, nranks, rank, level, out, cap, cnt), "tileqr_dist_plan_level")
+    tup = [tuple(out[5 * i: 5 * i + 5]) for i in range(cnt[0] + cnt[1] + cnt[2])]
+    return tup[:cnt[0]], tup[cnt[0]:cnt[0] + cnt[1]], tup[cnt[0] + cnt[1]:]
