@@ -54,8 +54,10 @@ static int arg_error(int i, const char* fn, const char* what) {
 // ---------------------------------------------------------------------------
 struct LevelLists {
   int64_t nlev = 0;
-  // per level: offset/count into each kind's flat arrays
-  std::vector<int64_t> g_off, g_cnt, t_off, t_cnt, l_off, l_cnt, s_off, s_cnt;
+  // per level: offset/count into each kind's flat arrays; the first lc_cnt /
+  // sc_cnt LARFB / SSRFB tasks of a level are "critical" (they update tile
+  // column k+1, the next panel) and run on the panel stream
+  std::vector<int64_t> g_off, g_cnt, t_off, t_cnt, l_off, l_cnt, s_off, s_cnt, lc_cnt, sc_cnt;
 };
 
 static int64_t num_levels(int64_t MT, int64_t NT) {
@@ -74,31 +76,41 @@ static int64_t num_levels(int64_t MT, int64_t NT) {
 // Host-side task lists in tile-index form; materialised to device pointers.
 struct HostTasks {
   std::vector<std::vector<int64_t>> G, T, L, S;  // per level: flattened tuples
+  std::vector<int64_t> Lc, Sc;                   // per level: leading critical tasks
 };
 
+// Tasks per level; within a level the critical LARFB/SSRFB tasks (column
+// n == k+1, read by the next panel) come first.
 static void build_tasks(int64_t MT, int64_t NT, HostTasks& h, int64_t nlev) {
   h.G.assign(nlev, {});
   h.T.assign(nlev, {});
   h.L.assign(nlev, {});
   h.S.assign(nlev, {});
+  h.Lc.assign(nlev, 0);
+  h.Sc.assign(nlev, 0);
+  std::vector<std::vector<int64_t>> Sb(nlev);
   const int64_t KT = std::min(MT, NT);
   for (int64_t k = 0; k < KT; ++k) {
     h.G[3 * k].push_back(k);
-    for (int64_t n = k + 1; n < NT; ++n) {
+    for (int64_t n = k + 1; n < NT; ++n) {  // n = k+1 first: the critical one
       h.L[3 * k + 1].push_back(k);
       h.L[3 * k + 1].push_back(n);
+      if (n == k + 1) ++h.Lc[3 * k + 1];
     }
     for (int64_t m = k + 1; m < MT; ++m) {
       h.T[2 * k + m].push_back(k);
       h.T[2 * k + m].push_back(m);
       for (int64_t n = k + 1; n < NT; ++n) {
-        auto& v = h.S[2 * k + m + 1];
+        const int64_t t = 2 * k + m + 1;
+        auto& v = (n == k + 1) ? h.S[t] : Sb[t];
         v.push_back(k);
         v.push_back(m);
         v.push_back(n);
+        if (n == k + 1) ++h.Sc[t];
       }
     }
   }
+  for (int64_t t = 0; t < nlev; ++t) h.S[t].insert(h.S[t].end(), Sb[t].begin(), Sb[t].end());
 }
 
 // ---------------------------------------------------------------------------
@@ -164,6 +176,8 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
     set_error("tileqr_factor: device allocation of the tile workspace failed");
     return TILEQR_ERR_ALLOC;
   }
+  // T tiles (m, k) with m < k are never written: keep them 0 in the output
+  TQ_CUDA(cudaMemset(ws->Tws, 0, (size_t)MT * NT * IB * NB * sizeof(double)));
   const int64_t nlev = num_levels(MT, NT);
   HostTasks h;
   build_tasks(MT, NT, h, nlev);
@@ -175,6 +189,8 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
     lv.t_off.push_back(nT); lv.t_cnt.push_back((int64_t)h.T[t].size() / 2); nT += h.T[t].size() / 2;
     lv.l_off.push_back(nL); lv.l_cnt.push_back((int64_t)h.L[t].size() / 2); nL += h.L[t].size() / 2;
     lv.s_off.push_back(nS); lv.s_cnt.push_back((int64_t)h.S[t].size() / 3); nS += h.S[t].size() / 3;
+    lv.lc_cnt.push_back(h.Lc[t]);
+    lv.sc_cnt.push_back(h.Sc[t]);
   }
   const size_t total = 2 * nG + 3 * nT + 3 * nL + 4 * nS;
   std::vector<void*> hp(std::max<size_t>(total, 1));
@@ -242,7 +258,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
   TQ_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   TQ_CUDA(cudaStreamCreateWithPriority(&ws->s_panel, cudaStreamNonBlocking, prio_hi));
   TQ_CUDA(cudaStreamCreateWithPriority(&ws->s_update, cudaStreamNonBlocking, prio_lo));
-  ws->ev.resize(4);
+  ws->ev.resize(9);
   for (auto& e : ws->ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   *out = ws.get();
   g_ws[std::make_tuple(dev, M, N, NB, IB)] = std::move(ws);
@@ -273,19 +289,74 @@ static int timed_end(FactorWS* ws, size_t slot, cudaStream_t st) {
   return 0;
 }
 
+// Critical-first schedule.  Level t:
+//   panel stream  : waits for the bulk updates of level t-2 (the last writers
+//                   of every tile its tasks touch), then the critical updates
+//                   of level t (LARFB(k,k+1), SSRFB(k,m,k+1): they feed the
+//                   next panel), then GEQRT/TSQRT of level t;
+//   update stream : waits for the panel stream of level t-1 (the V/T tiles
+//                   read at level t), then the bulk LARFB/SSRFB of level t.
+// Every task still runs at its ASAP level and every tile sees the same
+// sequence of operations (bitwise identical to the level-synchronous order);
+// the panel chain just never waits for a whole update batch.
 static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
   const LevelLists& lv = ws->lv;
   const int NB = ws->NB, IB = ws->IB;
-  cudaEvent_t ep = ws->ev[0], eu = ws->ev[1];
+  cudaEvent_t* pdone = &ws->ev[4];  // ring of 2: panel stream done with level t
+  cudaEvent_t* bdone = &ws->ev[6];  // ring of 3: update stream done with level t
   ws->rec_used = 0;
-  for (int64_t t = 0; t < lv.nlev; ++t) {
-    if (t > 0) {  // level t depends on everything of level t-1
-      TQ_CUDA(cudaEventRecord(eu, su));
-      TQ_CUDA(cudaStreamWaitEvent(sp, eu, 0));
-      TQ_CUDA(cudaEventRecord(ep, sp));
-      TQ_CUDA(cudaStreamWaitEvent(su, ep, 0));
-    }
+  auto larfb = [&](int64_t off, int64_t cnt, cudaStream_t st) -> int {
+    if (cnt <= 0) return 0;
+    size_t slot = 0;
     int rc;
+    if ((rc = timed_begin(ws, 2, cnt, st, &slot))) return rc;
+    if ((rc = launch_larfb(true, NB, IB, (int)cnt, ws->lV + off, ws->lT + off, ws->lC + off, NB, st))) return rc;
+    return timed_end(ws, slot, st);
+  };
+  auto ssrfb = [&](int64_t off, int64_t cnt, cudaStream_t st) -> int {
+    if (cnt <= 0) return 0;
+    size_t slot = 0;
+    int rc;
+    if ((rc = timed_begin(ws, 3, cnt, st, &slot))) return rc;
+    if ((rc = launch_ssrfb(true, NB, IB, (int)cnt, ws->sV + off, ws->sT + off, ws->sC1 + off, ws->sC2 + off,
+                           NB, st)))
+      return rc;
+    return timed_end(ws, slot, st);
+  };
+  const char* cf = getenv("TILEQR_CRITICAL_FIRST");
+  const bool critical_first = cf && cf[0] == '1';
+  for (int64_t t = 0; t < lv.nlev; ++t) {
+    int rc;
+    if (!critical_first) {
+      // level-synchronous (default): level t after everything of level t-1
+      if (t > 0) {
+        TQ_CUDA(cudaEventRecord(ws->ev[1], su));
+        TQ_CUDA(cudaStreamWaitEvent(sp, ws->ev[1], 0));
+        TQ_CUDA(cudaEventRecord(ws->ev[0], sp));
+        TQ_CUDA(cudaStreamWaitEvent(su, ws->ev[0], 0));
+      }
+      size_t slot = 0;
+      if (lv.g_cnt[t] > 0) {
+        if ((rc = timed_begin(ws, 0, lv.g_cnt[t], sp, &slot))) return rc;
+        if ((rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp)))
+          return rc;
+        if ((rc = timed_end(ws, slot, sp))) return rc;
+      }
+      if (lv.t_cnt[t] > 0) {
+        if ((rc = timed_begin(ws, 1, lv.t_cnt[t], sp, &slot))) return rc;
+        if ((rc = launch_tsqrt(NB, IB, (int)lv.t_cnt[t], ws->tR + lv.t_off[t], ws->tA + lv.t_off[t],
+                               ws->tT + lv.t_off[t], sp)))
+          return rc;
+        if ((rc = timed_end(ws, slot, sp))) return rc;
+      }
+      if ((rc = larfb(lv.l_off[t], lv.l_cnt[t], su))) return rc;
+      if ((rc = ssrfb(lv.s_off[t], lv.s_cnt[t], su))) return rc;
+      continue;
+    }
+    // ---- panel stream ----------------------------------------------------
+    if (t >= 2) TQ_CUDA(cudaStreamWaitEvent(sp, bdone[(t - 2) % 3], 0));
+    if ((rc = larfb(lv.l_off[t], lv.lc_cnt[t], sp))) return rc;
+    if ((rc = ssrfb(lv.s_off[t], lv.sc_cnt[t], sp))) return rc;
     size_t slot = 0;
     if (lv.g_cnt[t] > 0) {
       if ((rc = timed_begin(ws, 0, lv.g_cnt[t], sp, &slot))) return rc;
@@ -300,21 +371,14 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
         return rc;
       if ((rc = timed_end(ws, slot, sp))) return rc;
     }
-    if (lv.l_cnt[t] > 0) {
-      if ((rc = timed_begin(ws, 2, lv.l_cnt[t], su, &slot))) return rc;
-      if ((rc = launch_larfb(true, NB, IB, (int)lv.l_cnt[t], ws->lV + lv.l_off[t], ws->lT + lv.l_off[t],
-                             ws->lC + lv.l_off[t], NB, su)))
-        return rc;
-      if ((rc = timed_end(ws, slot, su))) return rc;
-    }
-    if (lv.s_cnt[t] > 0) {
-      if ((rc = timed_begin(ws, 3, lv.s_cnt[t], su, &slot))) return rc;
-      if ((rc = launch_ssrfb(true, NB, IB, (int)lv.s_cnt[t], ws->sV + lv.s_off[t], ws->sT + lv.s_off[t],
-                             ws->sC1 + lv.s_off[t], ws->sC2 + lv.s_off[t], NB, su)))
-        return rc;
-      if ((rc = timed_end(ws, slot, su))) return rc;
-    }
+    TQ_CUDA(cudaEventRecord(pdone[t % 2], sp));
+    // ---- update stream ---------------------------------------------------
+    if (t >= 1) TQ_CUDA(cudaStreamWaitEvent(su, pdone[(t - 1) % 2], 0));
+    if ((rc = larfb(lv.l_off[t] + lv.lc_cnt[t], lv.l_cnt[t] - lv.lc_cnt[t], su))) return rc;
+    if ((rc = ssrfb(lv.s_off[t] + lv.sc_cnt[t], lv.s_cnt[t] - lv.sc_cnt[t], su))) return rc;
+    TQ_CUDA(cudaEventRecord(bdone[t % 3], su));
   }
+  // the caller joins both streams (run_levels)
   return 0;
 }
 
@@ -608,10 +672,13 @@ int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out) {
   for (int64_t t = 0; t < nlev; ++t) {
     const int64_t c[4] = {(int64_t)h.G[t].size(), (int64_t)h.T[t].size() / 2,
                           (int64_t)h.L[t].size() / 2, (int64_t)h.S[t].size() / 3};
-    for (int q = 0; q < 4; ++q) {
-      cnt[q] += c[q];
-      launches += c[q] > 0;
-    }
+    for (int q = 0; q < 4; ++q) cnt[q] += c[q];
+    const char* cf = getenv("TILEQR_CRITICAL_FIRST");
+    if (cf && cf[0] == '1')  // panel stream: G, T, critical L/S; update stream: bulk L/S
+      launches += (c[0] > 0) + (c[1] > 0) + (h.Lc[t] > 0) + (h.Sc[t] > 0) + (c[2] > h.Lc[t]) +
+                  (c[3] > h.Sc[t]);
+    else
+      launches += (c[0] > 0) + (c[1] > 0) + (c[2] > 0) + (c[3] > 0);
   }
   h_out[0] = nlev;
   h_out[1] = launches + ((M == 0 || N == 0) ? 0 : 3);  // + zero-info, layout in, layout out
