@@ -21,6 +21,7 @@
 // TSQRT never writes the strict lower part of R (read concurrently by the
 // LARFB of the same DAG level).
 #include <math.h>
+#include <stdlib.h>
 
 #include "dmma.cuh"
 #include "internal.h"
@@ -28,8 +29,6 @@
 namespace tileqr {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = 8;
 constexpr int LDV = 40;   // >= 32, == 8 mod 16
 constexpr int LDT = 36;   // == 4 mod 16
 constexpr int LDW = 36;
@@ -38,7 +37,7 @@ constexpr int LDR = 33;
 
 __device__ unsigned long long g_panel_prof[16];  // diagnostic phase cycles (thread 0)
 
-template <int NB>
+template <int NB, int kWarps>
 struct FastSmem {
   double Vs[NB * LDV];
   double Ts[32 * LDT];
@@ -51,13 +50,14 @@ struct FastSmem {
   double Ws[kWarps][8 * LDW];
 };
 
-template <bool TS, int NB>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool TS, int NB, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1)
 panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* Tp) {
-  constexpr int RW = NB / 8;  // rows per warp in the factorization
-  constexpr int RB = NB / 8;  // 8-row blocks in the trailing update
+  constexpr int kThreads = kWarps * 32;
+  constexpr int RW = NB / kWarps;  // rows per warp in the factorization
+  constexpr int RB = NB / 8;       // 8-row blocks in the trailing update
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FastSmem<NB>& S = *reinterpret_cast<FastSmem<NB>*>(smem_raw);
+  FastSmem<NB, kWarps>& S = *reinterpret_cast<FastSmem<NB, kWarps>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int a = lane & 3, g = lane >> 2;
   double* const R = Rp[blockIdx.x];              // TSQRT: R tile; GEQRT: the tile
@@ -111,8 +111,14 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
         ps[w] = S.red[buf][w][jj];
         pd[w] = S.red[buf][w][lane];
       }
-      const double sigma = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
-      const double d = ((pd[0] + pd[1]) + (pd[2] + pd[3])) + ((pd[4] + pd[5]) + (pd[6] + pd[7]));
+#pragma unroll
+      for (int h = kWarps / 2; h > 0; h >>= 1)  // pairwise tree (fixed order: deterministic)
+#pragma unroll
+        for (int w = 0; w < h; ++w) {
+          ps[w] += ps[w + h];
+          pd[w] += pd[w + h];
+        }
+      const double sigma = ps[0], d = pd[0];
       const double alpha = TS ? S.Rin[jj * LDR + jj] : S.rowj[buf][jj];
       const double rjl = TS ? S.Rin[jj * LDR + lane] : S.rowj[buf][lane];
       double tau = 0.0, scal = 0.0, beta = alpha;
@@ -126,13 +132,16 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
       }
       const double w = fma(scal, d, rjl);
       const double tw = lane < IB ? tau * w : 0.0;
+      // select-free rank-1 update of the reflector rows: x = keep*x + coef*vj with
+      //   lane == jj: keep 0, coef scal (x becomes v2 = x2/(alpha-beta));
+      //   lane >  jj: keep 1, coef -tw*scal;   lane < jj: keep 1, coef 0.
+      const double keep = (lane == jj) ? 0.0 : 1.0;
+      const double coef = (lane == jj) ? scal : (lane > jj ? -tw * scal : 0.0);
 #pragma unroll
       for (int q = 0; q < RW; ++q) {
         const int r = warp * RW + q;
         if (TS || r > j) {
-          const double v = vj[q] * scal;
-          if (lane > jj) x[q] = fma(-tw, v, x[q]);
-          else if (lane == jj) x[q] = v;
+          x[q] = fma(coef, vj[q], keep * x[q]);
         } else if (r == j) {
           if (lane > jj) x[q] -= tw;
           else if (lane == jj) x[q] = beta;
@@ -189,20 +198,21 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
     // pairwise merges T12 = -T11 G12 T22 (Q1 Q2 = I - [V1 V2] [T11 T12; 0 T22]
     // [V1 V2]^T), log2(IB/8) levels.
     if (tid < IB) {
-      const int b0 = tid & ~7, r = tid;
-      for (int i = b0; i < b0 + 8; ++i) {
-        double v;
-        if (i < r) {
-          v = 0.0;
-        } else if (i == r) {
-          v = S.tau[i];
-        } else {
-          double acc = 0.0;
-          for (int l = r; l < i; ++l) acc = fma(S.Ts[r + l * LDT], S.Gs[l * LDG + i], acc);
-          v = -S.tau[i] * acc;
-        }
-        S.Ts[r + i * LDT] = v;
+      // thread r: row r of its 8x8 diagonal block, fully unrolled in registers
+      // (the G and tau loads do not depend on the recurrence and are hoisted)
+      const int b0 = tid & ~7, rr = tid & 7;
+      double tr[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < i; ++l)
+          if (l >= rr) acc = fma(tr[l], S.Gs[(b0 + l) * LDG + b0 + i], acc);
+        const double ti = S.tau[b0 + i];
+        tr[i] = (i < rr) ? 0.0 : (i == rr ? ti : -ti * acc);
       }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) S.Ts[tid + (b0 + i) * LDT] = tr[i];
     }
     __syncthreads();
     TQ_PHASE(6);
@@ -236,6 +246,14 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
       const int i = e / IB, r = e - i * IB;
       Tg[(size_t)(c0 + i) * IB + r] = (r <= i) ? S.Ts[r + i * LDT] : 0.0;
     }
+    __syncthreads();
+    TQ_PHASE(8);
+    for (int e = tid; e < IB * IB; e += kThreads) {  // DIAGNOSTIC: same loop again (warm I-cache)
+      const int i = e / IB, r = e - i * IB;
+      Tg[(size_t)(c0 + i) * IB + r] = (r <= i) ? S.Ts[r + i * LDT] : 0.0;
+    }
+    __syncthreads();
+    TQ_PHASE(9);
 
     __syncthreads();
     TQ_PHASE(3);
@@ -311,15 +329,32 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
 #undef TQ_PHASE
 }
 
+template <bool TS, int NB, int NW>
+int launch_fast_w(int IB, int batch, double* const* R, double* const* B, double* const* T,
+                  cudaStream_t s) {
+  auto kern = panel_fast_kernel<TS, NB, NW>;
+  const size_t bytes = sizeof(FastSmem<NB, NW>);
+  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  kern<<<batch, NW * 32, bytes, s>>>(IB, R, B, T);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+int panel_warps() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TILEQR_PANEL_WARPS");
+    v = e ? atoi(e) : 8;
+    if (v != 4 && v != 8) v = 8;
+  }
+  return v;
+}
+
 template <bool TS, int NB>
 int launch_fast_t(int IB, int batch, double* const* R, double* const* B, double* const* T,
                   cudaStream_t s) {
-  auto kern = panel_fast_kernel<TS, NB>;
-  const size_t bytes = sizeof(FastSmem<NB>);
-  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  kern<<<batch, kThreads, bytes, s>>>(IB, R, B, T);
-  TQ_LAUNCH_CHECK();
-  return 0;
+  return panel_warps() == 8 ? launch_fast_w<TS, NB, 8>(IB, batch, R, B, T, s)
+                            : launch_fast_w<TS, NB, 4>(IB, batch, R, B, T, s);
 }
 
 template <bool TS>

@@ -29,9 +29,16 @@ namespace upd {
 constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
 
+// Row-major V chunk, ld = LDV (a multiple of 16, no padding): element (r, i)
+// lives at r*LDV + (i ^ usw(r)) with usw(r) = 4*((r>>1)&3) ^ 8*(r&1).  Every
+// access pattern below touches 16 distinct 8-byte bank pairs per half warp:
+// staging writes (4 rows x 8 columns), step A (row 8rb+2t+j, column 8nb+g)
+// and step C (row 8rb+g, column k4+t).
+__host__ __device__ constexpr int usw(int r) { return (((r >> 1) & 3) << 2) ^ ((r & 1) << 3); }
+
 template <int KW>
 struct Geo {
-  static constexpr int LDV = (KW <= 16 ? 16 : 32) + 8;  // == 8 mod 16, >= swizzled column
+  static constexpr int LDV = (KW <= 16 ? 16 : 32);
   static constexpr int LDT = (KW <= 16 ? 16 : 32) + 4;  // == 4 mod 16
   static constexpr int LDC = (KW <= 16 ? 16 : 32) + 4;  // C1 rows per column, == 4 mod 16
 };
@@ -89,7 +96,7 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
   // 8*(4*it / RG) + [0,8); the swizzle of those rows is a per-thread constant.
   constexpr int RG = NB / 4;  // 4-row groups (NB % 16 == 0, so RG % 4 == 0)
   const int st_r = 4 * warp + (lane & 3), st_c = lane >> 2;
-  const int st_sw = (((st_r >> 1) & 3) << 2);
+  const int st_sw = usw(st_r);
   auto stage = [&](int idx, int slot) {
     const int p = item_p(idx), q = item_q(idx), phase = item_phase(idx);
     const int c0 = p * IB;
@@ -112,7 +119,7 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
       const int blk = e >> 5, l = e & 31;
       const int r = 4 * (blk % RG) + (l & 3), ii = 8 * (blk / RG) + (l >> 2);
       const int i = q * KW + ii;  // column within the panel
-      double* dst = vb + vsw(r, ii, LDV);
+      double* dst = vb + r * LDV + (ii ^ usw(r));
       if (i >= IB) {
         *dst = 0.0;
       } else if (LARFB) {
@@ -192,13 +199,13 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
             wacc2[mb][nb][j] = 0.0;
           }
       const int rb0 = LARFB ? (c0 >> 3) : 0;  // V_p is zero above row c0
-      // B-fragment (row 8rb+2a+j, column 8nb+g): its swizzle is 4a for every rb,
-      // so one per-thread base per (j, nb) and a compile-time offset per rb.
+      // B-fragment (row 8rb+2a+j, column 8nb+g): its swizzle usw = 4a ^ 8j for
+      // every rb, so one per-thread base per (j, nb) and a compile-time offset per rb.
       const double* pa[2][NBK];
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int nb = 0; nb < NBK; ++nb) pa[j][nb] = Vs + (2 * a + j) * LDV + ((8 * nb + g) ^ (4 * a));
+        for (int nb = 0; nb < NBK; ++nb) pa[j][nb] = Vs + (2 * a + j) * LDV + ((8 * nb + g) ^ usw(2 * a + j));
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         if (rb < rb0) continue;
@@ -310,9 +317,9 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
     // ---- step C --------------------------------------------------------------
     if (phase != 0) {
       const int rb0 = LARFB ? (c0 >> 3) : 0;
-      // B-fragment (row 8rb+g, column k4+a): swizzle 4*(g>>1) for every rb
+      // B-fragment (row 8rb+g, column k4+a): swizzle usw(g) for every rb
       const double* pc = Vs + g * LDV;
-      const int sw = 4 * (g >> 1);
+      const int sw = usw(g);
 #pragma unroll
       for (int k4 = 0; k4 < KW; k4 += 4) {
         double af[MB];

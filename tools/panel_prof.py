@@ -10,4 +10,4 @@ for nb, ib in [(64,16),(128,32)]:
         r = time_panel(nb, ib, reps=20, kind=kind)
         f(out, 1)
         reps = 21
-        print(r, "cycles/launch [stage, factor, writeV, G, trailing, base, merge, Twrite..]:", [round(out[i]/reps) for i in range(8)])
+        print(r, "cycles/launch [stage, factor, writeV, G, trailing, base, merge, Twrite, sync, Twrite2+sync]:", [round(out[i]/reps) for i in range(10)])
