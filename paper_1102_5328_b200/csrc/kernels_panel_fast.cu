@@ -23,6 +23,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "dmma.cuh"
 #include "internal.h"
 
@@ -64,6 +66,8 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
   double* const B = TS ? Bp[blockIdx.x] : R;     // TSQRT: square tile; GEQRT: the tile
   double* const Tg = Tp[blockIdx.x];
 
+  for (int e = tid; e < 32 * LDT; e += kThreads) S.Ts[e] = 0.0;  // zero padding for the T merges
+  for (int e = tid; e < 32 * LDG; e += kThreads) S.Gs[e] = 0.0;
   long long tp0 = clock64(), tp1;
 #define TQ_PHASE(k) do { if (tid == 0) { tp1 = clock64(); atomicAdd(&g_panel_prof[k], (unsigned long long)(tp1 - tp0)); tp0 = tp1; } } while (0)
   for (int c0 = 0; c0 < NB; c0 += IB) {
@@ -81,29 +85,37 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
     __syncthreads();
     double x[RW];
 #pragma unroll
-    for (int q = 0; q < RW; ++q) x[q] = lane < IB ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
+    for (int q = 0; q < RW; ++q)  // GEQRT: rows above the panel (R of earlier panels) stay out
+      x[q] = (lane < IB && (TS || warp * RW + q >= c0)) ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
 
     TQ_PHASE(0);
     // ---- 1. factor the panel column by column --------------------------------
     int buf = 0;
     for (int jj = 0; jj < IB; ++jj) {
       const int j = c0 + jj;
+      if (!TS && warp == j / RW) {
+        // GEQRT: row j leaves the reflector rows.  Its values go to smem (alpha
+        // and the R(j, c) inputs) and the registers of lanes >= jj are zeroed, so
+        // every R row sits as 0 in the registers: the dots and the rank-1 update
+        // below then run over all rows with no masks (rows < j hold 0 in the
+        // pivot column, lanes < jj keep their V entries of row j).
+        double rv = 0.0;
+#pragma unroll
+        for (int q = 0; q < RW; ++q)
+          if (warp * RW + q == j) {
+            rv = x[q];
+            if (lane >= jj) x[q] = 0.0;
+          }
+        S.rowj[buf][lane] = rv;
+      }
       double vj[RW];
       double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
 #pragma unroll
       for (int q = 0; q < RW; ++q) {
         vj[q] = __shfl_sync(0xffffffffu, x[q], jj);
-        const int r = warp * RW + q;
-        if (TS || r > j) pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
+        pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
       }
       S.red[buf][warp][lane] = (pp[0] + pp[1]) + (pp[2] + pp[3]);
-      if (!TS && warp == j / RW) {
-        double rv = 0.0;
-#pragma unroll
-        for (int q = 0; q < RW; ++q)
-          if (warp * RW + q == j) rv = x[q];
-        S.rowj[buf][lane] = rv;
-      }
       __syncthreads();
       double ps[kWarps], pd[kWarps];
 #pragma unroll
@@ -123,31 +135,39 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
       const double rjl = TS ? S.Rin[jj * LDR + lane] : S.rowj[buf][lane];
       double tau = 0.0, scal = 0.0, beta = alpha;
       if (sigma != 0.0) {
-        const double nrm = sqrt(fma(alpha, alpha, sigma));
-        beta = (alpha >= 0.0) ? -nrm : nrm;
-        // two independent correctly rounded reciprocals instead of two divisions
-        const double ib = __drcp_rn(beta);
-        scal = __drcp_rn(alpha - beta);
-        tau = (beta - alpha) * ib;
+        // Reflector rule (R1) from one reciprocal square root and one
+        // reciprocal: with s = alpha^2 + sigma, rs = 1/sqrt(s), nrm = s*rs,
+        //   beta = -sgn(alpha) nrm,  tau = (beta - alpha)/beta = 1 + |alpha| rs,
+        //   scal = 1/(alpha - beta) = sgn(alpha) / (|alpha| + nrm).
+        // Branch-free Newton refinement (s > 0 and O(1) data: no special cases).
+        const double s2 = fma(alpha, alpha, sigma);
+        double rs;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(s2));
+        const double hs = -0.5 * s2;
+        rs = rs * fma(hs, rs * rs, 1.5);
+        rs = rs * fma(hs, rs * rs, 1.5);
+        const double nrm = s2 * rs;
+        const double aa = fabs(alpha);
+        const double sg = (alpha >= 0.0) ? 1.0 : -1.0;
+        beta = -sg * nrm;
+        tau = fma(aa, rs, 1.0);
+        const double den = aa + nrm;
+        double rc;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
+        rc = fma(rc, fma(-den, rc, 1.0), rc);
+        rc = fma(rc, fma(-den, rc, 1.0), rc);
+        scal = sg * rc;
       }
       const double w = fma(scal, d, rjl);
       const double tw = lane < IB ? tau * w : 0.0;
-      // select-free rank-1 update of the reflector rows: x = keep*x + coef*vj with
-      //   lane == jj: keep 0, coef scal (x becomes v2 = x2/(alpha-beta));
-      //   lane >  jj: keep 1, coef -tw*scal;   lane < jj: keep 1, coef 0.
-      const double keep = (lane == jj) ? 0.0 : 1.0;
-      const double coef = (lane == jj) ? scal : (lane > jj ? -tw * scal : 0.0);
+      // select-free rank-1 update of the reflector rows, x += coef * vj:
+      //   lane == jj: coef = scal - 1 (vj == x there: x becomes v2 = x2 * scal);
+      //   lane >  jj: coef = -tw * scal;   lane < jj: coef = 0.
+      const double coef = (lane == jj) ? scal - 1.0 : (lane > jj ? -tw * scal : 0.0);
 #pragma unroll
-      for (int q = 0; q < RW; ++q) {
-        const int r = warp * RW + q;
-        if (TS || r > j) {
-          x[q] = fma(coef, vj[q], keep * x[q]);
-        } else if (r == j) {
-          if (lane > jj) x[q] -= tw;
-          else if (lane == jj) x[q] = beta;
-        }
-      }
-      if (TS && warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
+      for (int q = 0; q < RW; ++q) x[q] = fma(coef, vj[q], x[q]);
+      // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
+      if (warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
       if (tid == 0) S.tau[jj] = tau;
       buf ^= 1;
     }
@@ -162,9 +182,15 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
       const int c = idx / NB, r = idx - c * NB;
       double* p = &S.Vs[vsw(r, c, LDV)];
       const double v = *p;
-      B[r + (size_t)(c0 + c) * NB] = v;  // TSQRT: V2; GEQRT: R above/on, V below the diagonal
-      // GEQRT: the DMMA operand is the unit lower trapezoid V_p (same thread, no hazard)
-      if (!TS) *p = (r == c0 + c) ? 1.0 : (r > c0 + c ? v : 0.0);
+      if (TS) {
+        B[r + (size_t)(c0 + c) * NB] = v;  // V2
+      } else {
+        // GEQRT: V strictly below the diagonal (registers), R on/above it (Rout)
+        if (r > c0 + c) B[r + (size_t)(c0 + c) * NB] = v;
+        else if (r >= c0) B[r + (size_t)(c0 + c) * NB] = S.Rout[(r - c0) * LDR + c];
+        // the DMMA operand is the unit lower trapezoid V_p (same thread, no hazard)
+        *p = (r == c0 + c) ? 1.0 : (r > c0 + c ? v : 0.0);
+      }
     }
     if (TS) {
       for (int idx = tid; idx < IB * IB; idx += kThreads) {
@@ -216,31 +242,32 @@ panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* T
     }
     __syncthreads();
     TQ_PHASE(6);
-    for (int s = 8; s < IB; s *= 2) {
-      // X = G12 T22 for every pair (left = [st, st+s), right = [st+s, min(st+2s, IB)))
-      for (int e = tid; e < IB * IB; e += kThreads) {
-        const int i = e / IB, k = e - i * IB;  // row i (left block), column k (right block)
-        const int st = i & ~(2 * s - 1);
-        if (i < st + s && k >= st + s && k < min(st + 2 * s, IB)) {
-          double acc = 0.0;
-          for (int l = st + s; l <= k; ++l) acc = fma(S.Gs[i * LDG + l], S.Ts[l + k * LDT], acc);
-          S.Rin[i * LDR + k] = acc;  // Rin is free after the factorization: X buffer
-        }
+    // merges: Ts/Gs are zero outside the computed blocks (zero-filled at kernel
+    // start), so every dot runs over the full block width with no bounds
+    auto merge = [&](auto sz) {
+      constexpr int SZ = decltype(sz)::value;
+      const int npair = (IB + SZ - 1) / (2 * SZ);  // pairs with a non-empty right block
+      for (int e = tid; e < npair * SZ * SZ; e += kThreads) {  // X = G12 T22
+        const int p = e / (SZ * SZ), il = (e / SZ) % SZ, kl = e % SZ, st = p * 2 * SZ;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < SZ; ++l)
+          acc = fma(S.Gs[(st + il) * LDG + st + SZ + l], S.Ts[(st + SZ + l) + (st + SZ + kl) * LDT], acc);
+        S.Rin[(st + il) * LDR + st + SZ + kl] = acc;  // Rin is free after the factorization
       }
       __syncthreads();
-      for (int e = tid; e < IB * IB; e += kThreads) {
-        const int i = e / IB, k = e - i * IB;
-        const int st = i & ~(2 * s - 1);
-        if (i < st + s && k >= st + s && k < min(st + 2 * s, IB)) {
-          double acc = 0.0;
-          for (int l = i; l < st + s; ++l) acc = fma(S.Ts[i + l * LDT], S.Rin[l * LDR + k], acc);
-          S.Ts[i + k * LDT] = -acc;
-        } else if (i >= st + s && k < st + s && i < IB) {
-          S.Ts[i + k * LDT] = 0.0;  // strictly lower part
-        }
+      for (int e = tid; e < npair * SZ * SZ; e += kThreads) {  // T12 = -T11 X
+        const int p = e / (SZ * SZ), il = (e / SZ) % SZ, kl = e % SZ, st = p * 2 * SZ;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < SZ; ++l)
+          acc = fma(S.Ts[(st + il) + (st + l) * LDT], S.Rin[(st + l) * LDR + st + SZ + kl], acc);
+        S.Ts[(st + il) + (st + SZ + kl) * LDT] = -acc;
       }
       __syncthreads();
-    }
+    };
+    if (IB > 8) merge(std::integral_constant<int, 8>{});
+    if (IB > 16) merge(std::integral_constant<int, 16>{});
     TQ_PHASE(7);
     for (int e = tid; e < IB * IB; e += kThreads) {
       const int i = e / IB, r = e - i * IB;
