@@ -130,6 +130,26 @@ int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* co
                          const double* const* T, double* const* C1, double* const* C2,
                          int ncols, tileqr_stream_t stream);
 
+/* Packed reflector tiles -- the operand format of the factorization's
+ * trailing-update kernel for NB in {32, 64, 96, 128}, IB in {8, 16, 24, 32}
+ * (IB | NB): the V_p / T_p of a tile in the shared-memory image the
+ * barrier-free DMMA update loads with TMA bulk copies (layout: DESIGN.md §5,
+ * csrc/update_v2.cuh).  tileqr_factor writes them itself from its GEQRT /
+ * TSQRT kernels; these entry points expose the same kernels for tests and
+ * for the tuner's Step-1 timing.
+ *   tileqr_packed_size: doubles per packed tile (0 if (NB, IB) unsupported).
+ *   tileqr_pack_batched: Pk[i] <- pack(V[i], T[i]); larfb != 0 reads V as a
+ *     GEQRT tile (unit lower trapezoid implied), else as a full TSQRT V2.
+ *   tileqr_update_packed_batched: the Q^T update ('T' only, full NB x NB
+ *     tiles): larfb != 0: C2[i] <- Q^T C2[i] (C1 ignored, may be NULL);
+ *     else [C1[i]; C2[i]] <- Q^T [C1[i]; C2[i]].
+ * Errors: -1 NB/IB unsupported, -3 batch < 0, -4.. NULL arrays. */
+int tileqr_packed_size(int NB, int IB, size_t* n_doubles);
+int tileqr_pack_batched(int larfb, int NB, int IB, int batch, const double* const* V,
+                        const double* const* T, double* const* Pk, tileqr_stream_t stream);
+int tileqr_update_packed_batched(int larfb, int NB, int IB, int batch, const double* const* Pk,
+                                 double* const* C1, double* const* C2, tileqr_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * tileqr_tune -- the paper's two-step empirical tuning:
  *   Step 1: time tileqr_ssrfb_batched for every (NB, IB)
@@ -228,6 +248,14 @@ void tileqr_set_kernel_timing(int mask);
  * the most recent run, the number of launches and of tasks. */
 int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
                         int64_t* h_launches, int64_t* h_tasks);
+
+/* Launch trace of the most recent timed tileqr_factor(M, N, NB, IB): for
+ * up to max_recs timed launches, start/end in ms relative to the first timed
+ * launch's start event, kernel kind, DAG level and task count (host arrays,
+ * each nullable except h_count, which receives the number of records). */
+int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, double* h_t0_ms,
+                        double* h_t1_ms, int* h_kind, int64_t* h_level, int64_t* h_tasks,
+                        int64_t* h_count);
 
 /* Release all cached workspaces, graphs and communicators. */
 void tileqr_finalize(void);

@@ -26,9 +26,32 @@
 #include <tuple>
 #include <vector>
 
+#include "dag_item.h"
 #include "internal.h"
 
 namespace tileqr {
+
+#define TQ_DECL_DAG(nb)                                                                        \
+  int launch_dag_nb##nb(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm, \
+                        unsigned long long* prof, cudaStream_t s);
+TQ_DECL_DAG(32) TQ_DECL_DAG(64) TQ_DECL_DAG(96) TQ_DECL_DAG(128) TQ_DECL_DAG(160) TQ_DECL_DAG(192)
+TQ_DECL_DAG(224) TQ_DECL_DAG(256)
+#undef TQ_DECL_DAG
+
+static int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
+                      unsigned long long* prof, cudaStream_t s) {
+  switch (NB) {
+    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s);
+    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s);
+    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s);
+    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s);
+    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s);
+    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s);
+    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s);
+    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s);
+    default: return TILEQR_ERR_CUDA;
+  }
+}
 
 static thread_local std::string g_last_error;
 
@@ -129,12 +152,26 @@ struct FactorWS {
   double** tR = nullptr; double** tA = nullptr; double** tT = nullptr;
   double** lV = nullptr; double** lT = nullptr; double** lC = nullptr;
   double** sV = nullptr; double** sT = nullptr; double** sC1 = nullptr; double** sC2 = nullptr;
+  double** gP = nullptr; double** tP = nullptr; double** lP = nullptr; double** sP = nullptr;  // packed tiles
+  bool v2 = false;          // packed-reflector update path (update_v2.cuh)
+  double* Vpk = nullptr;    // MT x KT packed reflector tiles
+  size_t pk_dbl = 0;
   cudaStream_t s_panel = nullptr, s_update = nullptr;
   std::vector<cudaEvent_t> ev;
   cudaGraphExec_t graph = nullptr;
   int graph_timed = 0;
+  // dataflow DAG kernel (dag.cuh): items in claim order, counters [next | done per task]
+  dag::Item* d_items = nullptr;
+  int nitems = 0, ntasks = 0, nsm = 0;
+  int* d_ctr = nullptr;
+  unsigned long long* d_prof = nullptr;  // per-item claim/start/end (tileqr_set_kernel_timing)
+  cudaEvent_t dag_ev[2] = {nullptr, nullptr};
+  bool use_dag = false, dag_timed = false;
+  std::vector<unsigned char> item_kind;  // host copies for the diagnostics
+  std::vector<int> item_level;
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
-  struct Rec { int kind; int64_t tasks; cudaEvent_t a, b; };
+  struct Rec { int kind; int64_t tasks; int64_t level; cudaEvent_t a, b; };
+  int64_t cur_level = 0;
   std::vector<Rec> recs;
   size_t rec_used = 0;
   ~FactorWS() {
@@ -146,6 +183,11 @@ struct FactorWS {
     cudaFree(tiles);
     cudaFree(Tws);
     cudaFree(dptr);
+    cudaFree(d_items);
+    cudaFree(Vpk);
+    cudaFree(d_ctr);
+    cudaFree(d_prof);
+    for (auto e : dag_ev) if (e) cudaEventDestroy(e);
   }
 };
 
@@ -157,6 +199,169 @@ static int g_timing = 0;  // bit k: time launches of kernel kind k
 static bool use_graph() {
   const char* e = getenv("TILEQR_NO_GRAPH");
   return !(e && e[0] == '1');
+}
+
+// ---------------------------------------------------------------------------
+// Dataflow DAG: tasks, dependencies, priority order, work items (dag.cuh)
+// ---------------------------------------------------------------------------
+static bool dag_enabled(int NB, int IB) {
+  const char* e = getenv("TILEQR_SCHED");
+  if (e && strcmp(e, "levels") == 0) return false;
+  // the DAG kernel's update items for NB <= 128 are the packed-reflector body
+  return dag::dag_supported(NB, IB) && (NB > 128 || v2_supported(NB, IB));
+}
+
+// Tasks of the flat-tree tile QR with their dependencies:
+//   G(k) <- S(k-1,k,k);  L(k,n) <- G(k), S(k-1,k,n);
+//   T(k,m) <- (m == k+1 ? G(k) : T(k,m-1)), S(k-1,m,k);
+//   S(k,m,n) <- T(k,m), (m == k+1 ? L(k,n) : S(k,m-1,n)), S(k-1,m,n).
+// Claim order: bottom level (longest weighted path to the end of the DAG)
+// descending -- a topological order, since a task's bottom level exceeds
+// each successor's -- ties by ASAP level, then task id.
+static int build_dag(FactorWS* ws) {
+  const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT);
+  const int NB = ws->NB, IB = ws->IB;
+  std::vector<int64_t> offL(KT + 1), offT(KT + 1), offS(KT + 1);
+  int64_t nG = KT, nL = 0, nT = 0, nS = 0;
+  for (int64_t k = 0; k < KT; ++k) {
+    offL[k] = nL; nL += NT - k - 1;
+    offT[k] = nT; nT += MT - k - 1;
+    offS[k] = nS; nS += (MT - k - 1) * (NT - k - 1);
+  }
+  const int64_t ntask = nG + nL + nT + nS;
+  if (ntask > (int64_t)1 << 30) {
+    set_error("tileqr_factor: DAG too large for the dataflow kernel");
+    return TILEQR_ERR_ALLOC;
+  }
+  auto idG = [&](int64_t k) { return k; };
+  auto idL = [&](int64_t k, int64_t n) { return nG + offL[k] + (n - k - 1); };
+  auto idT = [&](int64_t k, int64_t m) { return nG + nL + offT[k] + (m - k - 1); };
+  auto idS = [&](int64_t k, int64_t m, int64_t n) {
+    return nG + nL + nT + offS[k] + (m - k - 1) * (NT - k - 1) + (n - k - 1);
+  };
+  struct Task { int kind; int k, m, n; int level; int ndep; int dep[3]; };
+  std::vector<Task> tk(ntask);
+  for (int64_t k = 0; k < KT; ++k) {
+    Task g{dag::kGeqrt, (int)k, (int)k, (int)k, (int)(3 * k), 0, {0, 0, 0}};
+    if (k > 0) g.dep[g.ndep++] = (int)idS(k - 1, k, k);
+    tk[idG(k)] = g;
+    for (int64_t n = k + 1; n < NT; ++n) {
+      Task l{dag::kLarfb, (int)k, (int)k, (int)n, (int)(3 * k + 1), 0, {0, 0, 0}};
+      l.dep[l.ndep++] = (int)idG(k);
+      if (k > 0) l.dep[l.ndep++] = (int)idS(k - 1, k, n);
+      tk[idL(k, n)] = l;
+    }
+    for (int64_t m = k + 1; m < MT; ++m) {
+      Task t{dag::kTsqrt, (int)k, (int)m, (int)k, (int)(2 * k + m), 0, {0, 0, 0}};
+      t.dep[t.ndep++] = (int)(m == k + 1 ? idG(k) : idT(k, m - 1));
+      if (k > 0) t.dep[t.ndep++] = (int)idS(k - 1, m, k);
+      tk[idT(k, m)] = t;
+      for (int64_t n = k + 1; n < NT; ++n) {
+        Task u{dag::kSsrfb, (int)k, (int)m, (int)n, (int)(2 * k + m + 1), 0, {0, 0, 0}};
+        u.dep[u.ndep++] = (int)idT(k, m);
+        u.dep[u.ndep++] = (int)(m == k + 1 ? idL(k, n) : idS(k, m - 1, n));
+        if (k > 0) u.dep[u.ndep++] = (int)idS(k - 1, m, n);
+        tk[idS(k, m, n)] = u;
+      }
+    }
+  }
+  // weights (ns, rough B200 per-SM durations): update work at ~150 GFLOP/s
+  // per SM, panel latency ~1.2 us per column
+  const double wS = 4.0 * NB * NB * NB / 150.0, wL = wS / 2, wP = 1200.0 * NB;
+  auto weight = [&](int kind) { return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : wP; };
+  std::vector<int> byLevel(ntask);
+  {
+    int maxl = 0;
+    for (const Task& t : tk) maxl = std::max(maxl, t.level);
+    std::vector<int64_t> cnt(maxl + 2, 0);
+    for (const Task& t : tk) ++cnt[t.level + 1];
+    for (int l = 0; l <= maxl; ++l) cnt[l + 1] += cnt[l];
+    for (int64_t i = 0; i < ntask; ++i) byLevel[cnt[tk[i].level]++] = (int)i;
+  }
+  std::vector<double> bl(ntask, 0.0), succ(ntask, 0.0);
+  for (int64_t q = ntask - 1; q >= 0; --q) {  // reverse topological (successors sit at higher levels)
+    const int i = byLevel[q];
+    bl[i] = weight(tk[i].kind) + succ[i];
+    for (int d = 0; d < tk[i].ndep; ++d) succ[tk[i].dep[d]] = std::max(succ[tk[i].dep[d]], bl[i]);
+  }
+  std::vector<int> order(ntask);
+  for (int64_t i = 0; i < ntask; ++i) order[i] = (int)i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    if (bl[a] != bl[b]) return bl[a] > bl[b];
+    if (tk[a].level != tk[b].level) return tk[a].level < tk[b].level;
+    return a < b;
+  });
+  const int cols = dag::dag_cols(NB);
+  const int nslab = (NB + cols - 1) / cols;
+  auto parts = [&](int kind) { return (kind == dag::kLarfb || kind == dag::kSsrfb) ? nslab : 1; };
+  const size_t tile = (size_t)NB * NB;
+  double* A = ws->tiles;
+  double* Tw = ws->Tws;
+  auto tp = [&](int64_t m, int64_t n) { return A + (size_t)(m + n * MT) * tile; };
+  auto tt = [&](int64_t m, int64_t k) { return Tw + (size_t)(m + k * MT) * IB * NB; };
+  auto pkp = [&](int64_t m, int64_t k) { return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr; };
+  std::vector<dag::Item> items;
+  items.reserve(nG + nT + (size_t)(nL + nS) * nslab);
+  for (int i : order) {
+    const Task& t = tk[i];
+    dag::Item it{};
+    it.kind = t.kind;
+    it.task = i;
+    it.ndep = t.ndep;
+    for (int d = 0; d < t.ndep; ++d) {
+      it.dep[d] = t.dep[d];
+      it.need[d] = parts(tk[t.dep[d]].kind);
+    }
+    switch (t.kind) {
+      case dag::kGeqrt: it.p[0] = tp(t.k, t.k); it.p[2] = tt(t.k, t.k); it.pk = pkp(t.k, t.k); break;
+      case dag::kTsqrt:
+        it.p[0] = tp(t.k, t.k); it.p[1] = tp(t.m, t.k); it.p[2] = tt(t.m, t.k); it.pk = pkp(t.m, t.k);
+        break;
+      case dag::kLarfb:
+        it.p[0] = tp(t.k, t.k); it.p[1] = tt(t.k, t.k); it.p[2] = tp(t.k, t.n); it.pk = pkp(t.k, t.k);
+        break;
+      default:
+        it.p[0] = tp(t.m, t.k); it.p[1] = tt(t.m, t.k); it.p[2] = tp(t.k, t.n); it.p[3] = tp(t.m, t.n);
+        it.pk = pkp(t.m, t.k);
+        break;
+    }
+    for (int sl = 0; sl < parts(t.kind); ++sl) {
+      it.col0 = sl * cols;
+      items.push_back(it);
+      ws->item_kind.push_back((unsigned char)t.kind);
+      ws->item_level.push_back(t.level);
+    }
+  }
+  ws->nitems = (int)items.size();
+  ws->ntasks = (int)ntask;
+  int dev = 0;
+  TQ_CUDA(cudaGetDevice(&dev));
+  TQ_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, dev));
+  if (cudaMalloc(&ws->d_items, std::max<size_t>(items.size(), 1) * sizeof(dag::Item)) != cudaSuccess ||
+      cudaMalloc(&ws->d_ctr, (size_t)(ntask + 1) * sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("tileqr_factor: device allocation of the DAG work list failed");
+    return TILEQR_ERR_ALLOC;
+  }
+  TQ_CUDA(cudaMemcpy(ws->d_items, items.data(), items.size() * sizeof(dag::Item), cudaMemcpyHostToDevice));
+  for (auto& e : ws->dag_ev) TQ_CUDA(cudaEventCreate(&e));
+  return 0;
+}
+
+static int run_dag(FactorWS* ws, cudaStream_t stream) {
+  TQ_CUDA(cudaMemsetAsync(ws->d_ctr, 0, (size_t)(ws->ntasks + 1) * sizeof(int), stream));
+  unsigned long long* prof = nullptr;
+  if (g_timing) {
+    if (!ws->d_prof) TQ_CUDA(cudaMalloc(&ws->d_prof, (size_t)ws->nitems * 3 * sizeof(unsigned long long)));
+    prof = ws->d_prof;
+    TQ_CUDA(cudaEventRecord(ws->dag_ev[0], stream));
+  }
+  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, ws->nitems, ws->d_ctr, ws->d_ctr + 1, ws->nsm, prof,
+                      stream);
+  if (rc) return rc;
+  if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
+  ws->dag_timed = g_timing != 0;
+  return 0;
 }
 
 static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** out) {
@@ -192,23 +397,38 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
     lv.lc_cnt.push_back(h.Lc[t]);
     lv.sc_cnt.push_back(h.Sc[t]);
   }
-  const size_t total = 2 * nG + 3 * nT + 3 * nL + 4 * nS;
+  // packed reflector tiles (update_v2.cuh): one per (m, k), m >= k
+  ws->v2 = v2_supported(NB, IB);
+  const int64_t KT = std::min(MT, NT);
+  if (ws->v2) {
+    ws->pk_dbl = v2_pk_doubles(NB, IB);
+    if (cudaMalloc(&ws->Vpk, ws->pk_dbl * MT * KT * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("tileqr_factor: device allocation of the packed reflector tiles failed");
+      return TILEQR_ERR_ALLOC;
+    }
+  }
+  const size_t total = 3 * nG + 4 * nT + 4 * nL + 5 * nS;
   std::vector<void*> hp(std::max<size_t>(total, 1));
   double* A = ws->tiles;
   double* T = ws->Tws;
   auto tp = [&](int64_t m, int64_t n) { return A + (size_t)(m + n * MT) * tile; };
   auto tt = [&](int64_t m, int64_t k) { return T + (size_t)(m + k * MT) * IB * NB; };
+  auto pk = [&](int64_t m, int64_t k) -> void* {
+    return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr;
+  };
   size_t o = 0;
-  const size_t oG = o; o += 2 * nG;
-  const size_t oT = o; o += 3 * nT;
-  const size_t oL = o; o += 3 * nL;
-  const size_t oS = o; o += 4 * nS;
+  const size_t oG = o; o += 3 * nG;
+  const size_t oT = o; o += 4 * nT;
+  const size_t oL = o; o += 4 * nL;
+  const size_t oS = o; o += 5 * nS;
   {
     size_t i = 0;
     for (int64_t t = 0; t < nlev; ++t)
       for (int64_t k : h.G[t]) {
         hp[oG + i] = tp(k, k);
         hp[oG + nG + i] = tt(k, k);
+        hp[oG + 2 * nG + i] = pk(k, k);
         ++i;
       }
     i = 0;
@@ -218,6 +438,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
         hp[oT + i] = tp(k, k);
         hp[oT + nT + i] = tp(m, k);
         hp[oT + 2 * nT + i] = tt(m, k);
+        hp[oT + 3 * nT + i] = pk(m, k);
         ++i;
       }
     i = 0;
@@ -227,6 +448,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
         hp[oL + i] = tp(k, k);
         hp[oL + nL + i] = tt(k, k);
         hp[oL + 2 * nL + i] = tp(k, n);
+        hp[oL + 3 * nL + i] = pk(k, k);
         ++i;
       }
     i = 0;
@@ -237,6 +459,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
         hp[oS + nS + i] = tt(m, k);
         hp[oS + 2 * nS + i] = tp(k, n);
         hp[oS + 3 * nS + i] = tp(m, n);
+        hp[oS + 4 * nS + i] = pk(m, k);
         ++i;
       }
   }
@@ -247,10 +470,11 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
   }
   TQ_CUDA(cudaMemcpy(ws->dptr, hp.data(), hp.size() * sizeof(void*), cudaMemcpyHostToDevice));
   double** d = reinterpret_cast<double**>(ws->dptr);
-  ws->gA = d + oG; ws->gT = d + oG + nG;
-  ws->tR = d + oT; ws->tA = d + oT + nT; ws->tT = d + oT + 2 * nT;
-  ws->lV = d + oL; ws->lT = d + oL + nL; ws->lC = d + oL + 2 * nL;
+  ws->gA = d + oG; ws->gT = d + oG + nG; ws->gP = d + oG + 2 * nG;
+  ws->tR = d + oT; ws->tA = d + oT + nT; ws->tT = d + oT + 2 * nT; ws->tP = d + oT + 3 * nT;
+  ws->lV = d + oL; ws->lT = d + oL + nL; ws->lC = d + oL + 2 * nL; ws->lP = d + oL + 3 * nL;
   ws->sV = d + oS; ws->sT = d + oS + nS; ws->sC1 = d + oS + 2 * nS; ws->sC2 = d + oS + 3 * nS;
+  ws->sP = d + oS + 4 * nS;
   // The panel kernels (GEQRT/TSQRT) are the DAG's critical path: their stream
   // gets the highest priority so their CTAs are dispatched ahead of queued
   // update CTAs whenever an SM frees up (kept per node in the CUDA graph).
@@ -260,6 +484,11 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
   TQ_CUDA(cudaStreamCreateWithPriority(&ws->s_update, cudaStreamNonBlocking, prio_lo));
   ws->ev.resize(9);
   for (auto& e : ws->ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  ws->use_dag = dag_enabled(NB, IB);
+  if (ws->use_dag) {
+    int rc = build_dag(ws.get());
+    if (rc) return rc;
+  }
   *out = ws.get();
   g_ws[std::make_tuple(dev, M, N, NB, IB)] = std::move(ws);
   return 0;
@@ -272,7 +501,7 @@ static int timed_begin(FactorWS* ws, int kind, int64_t tasks, cudaStream_t st, s
   *slot = (size_t)-1;
   if (!(g_timing & (1 << kind))) return 0;
   if (ws->rec_used == ws->recs.size()) {
-    FactorWS::Rec r{kind, tasks, nullptr, nullptr};
+    FactorWS::Rec r{kind, tasks, 0, nullptr, nullptr};
     TQ_CUDA(cudaEventCreate(&r.a));
     TQ_CUDA(cudaEventCreate(&r.b));
     ws->recs.push_back(r);
@@ -280,6 +509,7 @@ static int timed_begin(FactorWS* ws, int kind, int64_t tasks, cudaStream_t st, s
   *slot = ws->rec_used++;
   ws->recs[*slot].kind = kind;
   ws->recs[*slot].tasks = tasks;
+  ws->recs[*slot].level = ws->cur_level;
   TQ_CUDA(cudaEventRecordWithFlags(ws->recs[*slot].a, st, cudaEventRecordExternal));
   return 0;
 }
@@ -310,7 +540,9 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
     size_t slot = 0;
     int rc;
     if ((rc = timed_begin(ws, 2, cnt, st, &slot))) return rc;
-    if ((rc = launch_larfb(true, NB, IB, (int)cnt, ws->lV + off, ws->lT + off, ws->lC + off, NB, st))) return rc;
+    if (ws->v2) rc = launch_update_pk(true, NB, IB, (int)cnt, ws->lP + off, nullptr, ws->lC + off, st);
+    else rc = launch_larfb(true, NB, IB, (int)cnt, ws->lV + off, ws->lT + off, ws->lC + off, NB, st);
+    if (rc) return rc;
     return timed_end(ws, slot, st);
   };
   auto ssrfb = [&](int64_t off, int64_t cnt, cudaStream_t st) -> int {
@@ -318,15 +550,18 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
     size_t slot = 0;
     int rc;
     if ((rc = timed_begin(ws, 3, cnt, st, &slot))) return rc;
-    if ((rc = launch_ssrfb(true, NB, IB, (int)cnt, ws->sV + off, ws->sT + off, ws->sC1 + off, ws->sC2 + off,
-                           NB, st)))
-      return rc;
+    if (ws->v2)
+      rc = launch_update_pk(false, NB, IB, (int)cnt, ws->sP + off, ws->sC1 + off, ws->sC2 + off, st);
+    else
+      rc = launch_ssrfb(true, NB, IB, (int)cnt, ws->sV + off, ws->sT + off, ws->sC1 + off, ws->sC2 + off, NB, st);
+    if (rc) return rc;
     return timed_end(ws, slot, st);
   };
   const char* cf = getenv("TILEQR_CRITICAL_FIRST");
   const bool critical_first = cf && cf[0] == '1';
   for (int64_t t = 0; t < lv.nlev; ++t) {
     int rc;
+    ws->cur_level = t;
     if (!critical_first) {
       // level-synchronous (default): level t after everything of level t-1
       if (t > 0) {
@@ -338,14 +573,15 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
       size_t slot = 0;
       if (lv.g_cnt[t] > 0) {
         if ((rc = timed_begin(ws, 0, lv.g_cnt[t], sp, &slot))) return rc;
-        if ((rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp)))
+        if ((rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp,
+                              ws->v2 ? ws->gP + lv.g_off[t] : nullptr)))
           return rc;
         if ((rc = timed_end(ws, slot, sp))) return rc;
       }
       if (lv.t_cnt[t] > 0) {
         if ((rc = timed_begin(ws, 1, lv.t_cnt[t], sp, &slot))) return rc;
         if ((rc = launch_tsqrt(NB, IB, (int)lv.t_cnt[t], ws->tR + lv.t_off[t], ws->tA + lv.t_off[t],
-                               ws->tT + lv.t_off[t], sp)))
+                               ws->tT + lv.t_off[t], sp, ws->v2 ? ws->tP + lv.t_off[t] : nullptr)))
           return rc;
         if ((rc = timed_end(ws, slot, sp))) return rc;
       }
@@ -360,14 +596,15 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
     size_t slot = 0;
     if (lv.g_cnt[t] > 0) {
       if ((rc = timed_begin(ws, 0, lv.g_cnt[t], sp, &slot))) return rc;
-      if ((rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp)))
+      if ((rc = launch_geqrt(NB, IB, (int)lv.g_cnt[t], ws->gA + lv.g_off[t], ws->gT + lv.g_off[t], sp,
+                              ws->v2 ? ws->gP + lv.g_off[t] : nullptr)))
         return rc;
       if ((rc = timed_end(ws, slot, sp))) return rc;
     }
     if (lv.t_cnt[t] > 0) {
       if ((rc = timed_begin(ws, 1, lv.t_cnt[t], sp, &slot))) return rc;
       if ((rc = launch_tsqrt(NB, IB, (int)lv.t_cnt[t], ws->tR + lv.t_off[t], ws->tA + lv.t_off[t],
-                             ws->tT + lv.t_off[t], sp)))
+                             ws->tT + lv.t_off[t], sp, ws->v2 ? ws->tP + lv.t_off[t] : nullptr)))
         return rc;
       if ((rc = timed_end(ws, slot, sp))) return rc;
     }
@@ -384,6 +621,7 @@ static int issue_levels(FactorWS* ws, cudaStream_t sp, cudaStream_t su) {
 
 // Run the level sequence ordered after `stream` and before subsequent work on it.
 static int run_levels(FactorWS* ws, cudaStream_t stream) {
+  if (ws->use_dag) return run_dag(ws, stream);
   if (use_graph()) {
     if (ws->graph && ws->graph_timed != g_timing) {
       cudaGraphExecDestroy(ws->graph);
@@ -577,6 +815,23 @@ int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double
   return rc;
 }
 
+// Batched Q^T update through the factorization's packed-reflector kernel:
+// pack (V, T) into stream-ordered scratch, then run update_v2.
+static int packed_update(bool larfb, int NB, int IB, int batch, const double* const* V, const double* const* T,
+                         double* const* C1, double* const* C2, cudaStream_t s) {
+  const size_t pd = v2_pk_doubles(NB, IB);
+  double* buf = nullptr;
+  double** ptr = nullptr;
+  TQ_CUDA(cudaMallocAsync(&buf, pd * batch * sizeof(double), s));
+  TQ_CUDA(cudaMallocAsync(&ptr, (size_t)batch * sizeof(double*), s));
+  int rc = launch_fill_ptrs(ptr, buf, pd, batch, s);
+  if (!rc) rc = launch_pack(larfb, NB, IB, batch, V, T, ptr, s);
+  if (!rc) rc = launch_update_pk(larfb, NB, IB, batch, ptr, C1, C2, s);
+  cudaFreeAsync(buf, s);
+  cudaFreeAsync(ptr, s);
+  return rc;
+}
+
 static int check_batched(const char* fn, int NB, int IB, int batch) {
   if (NB < 1 || NB > 512) return arg_error(1, fn, "NB not in [1, 512]");
   if (IB < 1 || IB > NB || NB % IB) return arg_error(2, fn, "IB must divide NB");
@@ -619,8 +874,11 @@ int tileqr_larfb_batched(char trans, int NB, int IB, int batch, const double* co
   if (!T) return arg_error(6, fn, "T is NULL");
   if (!C) return arg_error(7, fn, "C is NULL");
   if (ncols < 1 || ncols > NB) return arg_error(8, fn, "ncols not in [1, NB]");
-  return launch_larfb(trans == 'T' || trans == 't', NB, IB, batch, V, T, C, ncols,
-                      reinterpret_cast<cudaStream_t>(stream));
+  const bool tr = trans == 'T' || trans == 't';
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (tr && ncols == NB && v2_supported(NB, IB))  // the factorization's kernel: pack, then update
+    return packed_update(true, NB, IB, batch, V, T, nullptr, C, s);
+  return launch_larfb(tr, NB, IB, batch, V, T, C, ncols, s);
 }
 
 int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* const* V2,
@@ -638,8 +896,41 @@ int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* co
   if (!C1) return arg_error(7, fn, "C1 is NULL");
   if (!C2) return arg_error(8, fn, "C2 is NULL");
   if (ncols < 1 || ncols > NB) return arg_error(9, fn, "ncols not in [1, NB]");
-  return launch_ssrfb(trans == 'T' || trans == 't', NB, IB, batch, V2, T, C1, C2, ncols,
-                      reinterpret_cast<cudaStream_t>(stream));
+  const bool tr = trans == 'T' || trans == 't';
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (tr && ncols == NB && v2_supported(NB, IB))
+    return packed_update(false, NB, IB, batch, V2, T, C1, C2, s);
+  return launch_ssrfb(tr, NB, IB, batch, V2, T, C1, C2, ncols, s);
+}
+
+int tileqr_packed_size(int NB, int IB, size_t* n_doubles) {
+  if (!n_doubles) return arg_error(3, "tileqr_packed_size", "NULL output");
+  *n_doubles = (valid_nb_ib(NB, IB) && v2_supported(NB, IB)) ? v2_pk_doubles(NB, IB) : 0;
+  return 0;
+}
+
+int tileqr_pack_batched(int larfb, int NB, int IB, int batch, const double* const* V, const double* const* T,
+                        double* const* Pk, tileqr_stream_t stream) {
+  static const char* fn = "tileqr_pack_batched";
+  if (!valid_nb_ib(NB, IB) || !v2_supported(NB, IB)) return arg_error(1, fn, "(NB, IB) has no packed form");
+  if (batch < 0) return arg_error(3, fn, "batch < 0");
+  if (batch == 0) return 0;
+  if (!V) return arg_error(4, fn, "V is NULL");
+  if (!T) return arg_error(5, fn, "T is NULL");
+  if (!Pk) return arg_error(6, fn, "Pk is NULL");
+  return launch_pack(larfb != 0, NB, IB, batch, V, T, Pk, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int tileqr_update_packed_batched(int larfb, int NB, int IB, int batch, const double* const* Pk,
+                                 double* const* C1, double* const* C2, tileqr_stream_t stream) {
+  static const char* fn = "tileqr_update_packed_batched";
+  if (!valid_nb_ib(NB, IB) || !v2_supported(NB, IB)) return arg_error(1, fn, "(NB, IB) has no packed form");
+  if (batch < 0) return arg_error(3, fn, "batch < 0");
+  if (batch == 0) return 0;
+  if (!Pk) return arg_error(4, fn, "Pk is NULL");
+  if (!larfb && !C1) return arg_error(5, fn, "C1 is NULL");
+  if (!C2) return arg_error(6, fn, "C2 is NULL");
+  return launch_update_pk(larfb != 0, NB, IB, batch, Pk, C1, C2, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int tileqr_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t seed,
@@ -696,7 +987,7 @@ void tileqr_set_kernel_timing(int mask) {
 int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
                         int64_t* h_launches, int64_t* h_tasks) {
   static const char* fn = "tileqr_kernel_times";
-  if (kind < 0 || kind > 3) return arg_error(5, fn, "kind not in 0..3");
+  if (kind < 0 || kind > 4) return arg_error(5, fn, "kind not in 0..4");
   if (!h_total_ms || !h_launches || !h_tasks) return arg_error(6, fn, "NULL output");
   int dev;
   TQ_CUDA(cudaGetDevice(&dev));
@@ -709,6 +1000,36 @@ int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* 
   FactorWS* ws = it->second.get();
   double tot = 0.0;
   int64_t nl = 0, nt = 0;
+  if (ws->use_dag) {
+    // dataflow kernel: busy time of the items of this kind summed over CTAs
+    // (inputs ready -> completion published); kind 4 = the whole DAG kernel
+    if (!ws->dag_timed) {
+      set_error("tileqr_kernel_times: the last run was not timed");
+      return TILEQR_ERR_NOT_INIT;
+    }
+    if (kind == 4) {
+      float ms = 0.f;
+      TQ_CUDA(cudaEventElapsedTime(&ms, ws->dag_ev[0], ws->dag_ev[1]));
+      *h_total_ms = ms;
+      *h_launches = 1;
+      *h_tasks = ws->ntasks;
+      return 0;
+    }
+    std::vector<unsigned long long> pr((size_t)ws->nitems * 3);
+    TQ_CUDA(cudaMemcpy(pr.data(), ws->d_prof, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    const int cols = dag::dag_cols(ws->NB);
+    const int nslab = (ws->NB + cols - 1) / cols;
+    for (int i = 0; i < ws->nitems; ++i) {
+      if (ws->item_kind[i] != kind) continue;
+      tot += (double)(pr[3 * i + 2] - pr[3 * i + 1]) * 1e-6;
+      ++nl;
+    }
+    nt = (kind >= 2) ? nl / nslab : nl;
+    *h_total_ms = tot;
+    *h_launches = nl;
+    *h_tasks = nt;
+    return 0;
+  }
   for (size_t i = 0; i < ws->rec_used; ++i) {
     const FactorWS::Rec& r = ws->recs[i];
     if (r.kind != kind) continue;
@@ -721,6 +1042,59 @@ int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* 
   *h_total_ms = tot;
   *h_launches = nl;
   *h_tasks = nt;
+  return 0;
+}
+
+int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, double* h_t0_ms,
+                        double* h_t1_ms, int* h_kind, int64_t* h_level, int64_t* h_tasks,
+                        int64_t* h_count) {
+  static const char* fn = "tileqr_kernel_trace";
+  if (max_recs < 0) return arg_error(5, fn, "max_recs < 0");
+  if (!h_count) return arg_error(11, fn, "NULL output");
+  int dev;
+  TQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  if (it == g_ws.end()) {
+    set_error("tileqr_kernel_trace: no factorization of this shape has run");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  FactorWS* ws = it->second.get();
+  if (ws->use_dag) {
+    // per work item: start = inputs ready, end = completion published (ns
+    // clock of the device), relative to the earliest claim
+    if (!ws->dag_timed) {
+      set_error("tileqr_kernel_trace: the last run was not timed");
+      return TILEQR_ERR_NOT_INIT;
+    }
+    std::vector<unsigned long long> pr((size_t)ws->nitems * 3);
+    TQ_CUDA(cudaMemcpy(pr.data(), ws->d_prof, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (int i = 0; i < ws->nitems; ++i) t0 = std::min(t0, pr[3 * i]);
+    *h_count = ws->nitems;
+    for (int64_t i = 0; i < ws->nitems && i < max_recs; ++i) {
+      if (h_t0_ms) h_t0_ms[i] = (double)(pr[3 * i + 1] - t0) * 1e-6;
+      if (h_t1_ms) h_t1_ms[i] = (double)(pr[3 * i + 2] - t0) * 1e-6;
+      if (h_kind) h_kind[i] = ws->item_kind[i];
+      if (h_level) h_level[i] = ws->item_level[i];
+      if (h_tasks) h_tasks[i] = 1;
+    }
+    return 0;
+  }
+  *h_count = (int64_t)ws->rec_used;
+  if (ws->rec_used == 0) return 0;
+  const cudaEvent_t origin = ws->recs[0].a;
+  for (size_t i = 0; i < ws->rec_used && (int64_t)i < max_recs; ++i) {
+    const FactorWS::Rec& r = ws->recs[i];
+    float a = 0.f, b = 0.f;
+    TQ_CUDA(cudaEventElapsedTime(&a, origin, r.a));
+    TQ_CUDA(cudaEventElapsedTime(&b, origin, r.b));
+    if (h_t0_ms) h_t0_ms[i] = a;
+    if (h_t1_ms) h_t1_ms[i] = b;
+    if (h_kind) h_kind[i] = r.kind;
+    if (h_level) h_level[i] = r.level;
+    if (h_tasks) h_tasks[i] = r.tasks;
+  }
   return 0;
 }
 

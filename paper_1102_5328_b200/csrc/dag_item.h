@@ -1,0 +1,34 @@
+// dag_item.h -- work-item descriptor of the dataflow DAG kernel (dag.cuh),
+// built on the host by api.cu.
+#pragma once
+
+namespace tileqr {
+namespace dag {
+
+constexpr int kWarps = 8;  // warps per CTA of the DAG kernel
+
+enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3 };
+
+// One work item: a whole panel task, or a column slab of an update task.
+struct Item {
+  int kind;
+  int task;      // completion counter index
+  int col0;      // first column of the slab (LARFB / SSRFB)
+  int ndep;
+  int dep[3];    // tasks whose counters must reach need[] before the item runs
+  int need[3];
+  double* p[4];  // GEQRT: A, -, T; TSQRT: R, A2, T; LARFB: V, T, C; SSRFB: V2, T, C1, C2
+  double* pk;    // packed reflector tile (NB <= 128): written by GEQRT/TSQRT, read by LARFB/SSRFB
+};
+
+// Update columns per item for tile order NB: 8 warps x 8*MB columns.
+__host__ __device__ constexpr int dag_mb(int NB) { return (NB == 96 || NB == 128) ? 2 : 1; }
+__host__ __device__ constexpr int dag_cols(int NB) { return kWarps * 8 * dag_mb(NB); }
+
+// DAG kernel supported for these (NB, IB): the fast panel set.
+inline bool dag_supported(int NB, int IB) {
+  return NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB >= 8 && IB <= 32;
+}
+
+}  // namespace dag
+}  // namespace tileqr

@@ -115,6 +115,9 @@ struct DistState {
   double* T_cached = nullptr;
   double* pbuf = nullptr;  // V tiles of every panel: slot(k, m) = off(k) + (m - k)
   double* pT = nullptr;    // T tiles of every panel
+  double* ppk = nullptr;   // packed reflector tiles (update_v2.cuh) of every panel, same slots
+  bool v2 = false;
+  size_t pk_dbl = 0;
   void** dptr = nullptr;   // all levels' pointer arrays
   std::vector<LevelPlan> plan;
 };
@@ -126,6 +129,8 @@ int64_t slot_off(int64_t MT, int64_t k) { return k * MT - k * (k - 1) / 2; }
 void free_shape() {
   cudaFree(g_d.pbuf);
   cudaFree(g_d.pT);
+  cudaFree(g_d.ppk);
+  g_d.ppk = nullptr;
   cudaFree(g_d.dptr);
   g_d.pbuf = nullptr;
   g_d.pT = nullptr;
@@ -260,14 +265,20 @@ int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_loc
   auto locT = [&](int64_t m, int64_t n) { return T_local + (size_t)(m + (n / P) * MT) * ttile; };
   auto pv = [&](int64_t k, int64_t m) { return g_d.pbuf + (size_t)(slot_off(MT, k) + (m - k)) * tile; };
   auto pt = [&](int64_t k, int64_t m) { return g_d.pT + (size_t)(slot_off(MT, k) + (m - k)) * ttile; };
+  auto pp = [&](int64_t k, int64_t m) { return g_d.ppk + (size_t)(slot_off(MT, k) + (m - k)) * g_d.pk_dbl; };
   const int64_t nlev = dist_levels(MT);
 
   // ---- per-shape workspace: panel buffers and every level's pointer arrays ----
   if (g_d.N != N || g_d.NB != NB || g_d.IB != IB || g_d.A_cached != A_local || g_d.T_cached != T_local) {
     free_shape();
     const int64_t nslots = slot_off(MT, MT);
-    if (cudaMalloc(&g_d.pbuf, nslots * tile * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&g_d.pT, nslots * ttile * sizeof(double)) != cudaSuccess) {
+    // packed path (as tileqr_factor): panel kernels write the packed reflector
+    // tile into the slot, which is what gets broadcast and what updates read
+    g_d.v2 = v2_supported(NB, IB);
+    g_d.pk_dbl = g_d.v2 ? v2_pk_doubles(NB, IB) : 0;
+    if ((g_d.v2 && cudaMalloc(&g_d.ppk, nslots * g_d.pk_dbl * sizeof(double)) != cudaSuccess) ||
+        (!g_d.v2 && cudaMalloc(&g_d.pbuf, nslots * tile * sizeof(double)) != cudaSuccess) ||
+        (!g_d.v2 && cudaMalloc(&g_d.pT, nslots * ttile * sizeof(double)) != cudaSuccess)) {
       cudaGetLastError();
       free_shape();
       set_error("tileqr_dist_factor: panel buffer allocation failed");
@@ -281,20 +292,30 @@ int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_loc
       LevelPlan& L = g_d.plan[t];
       L.panel = panel;
       L.bcast = bc;
-      std::vector<void*> gA, gT, tR, tA, tT, lV, lT, lC, sV, sT, s1, s2;
+      std::vector<void*> gA, gT, gP, tR, tA, tT, tP, lV, lT, lC, lP, sV, sT, s1, s2, sP;
+      const bool v2 = g_d.v2;
       for (const Task& q : panel) {
-        if (q.kind == 0) { gA.push_back(loc(q.k, q.k)); gT.push_back(locT(q.k, q.k)); }
-        else { tR.push_back(loc(q.k, q.k)); tA.push_back(loc(q.m, q.k)); tT.push_back(locT(q.m, q.k)); }
+        if (q.kind == 0) {
+          gA.push_back(loc(q.k, q.k)); gT.push_back(locT(q.k, q.k)); gP.push_back(v2 ? pp(q.k, q.k) : nullptr);
+        } else {
+          tR.push_back(loc(q.k, q.k)); tA.push_back(loc(q.m, q.k)); tT.push_back(locT(q.m, q.k));
+          tP.push_back(v2 ? pp(q.k, q.m) : nullptr);
+        }
       }
       for (const Task& q : upd) {
-        if (q.kind == 2) { lV.push_back(pv(q.k, q.k)); lT.push_back(pt(q.k, q.k)); lC.push_back(loc(q.k, q.n)); }
-        else { sV.push_back(pv(q.k, q.m)); sT.push_back(pt(q.k, q.m)); s1.push_back(loc(q.k, q.n)); s2.push_back(loc(q.m, q.n)); }
+        if (q.kind == 2) {
+          lV.push_back(v2 ? nullptr : pv(q.k, q.k)); lT.push_back(v2 ? nullptr : pt(q.k, q.k));
+          lC.push_back(loc(q.k, q.n)); lP.push_back(v2 ? pp(q.k, q.k) : nullptr);
+        } else {
+          sV.push_back(v2 ? nullptr : pv(q.k, q.m)); sT.push_back(v2 ? nullptr : pt(q.k, q.m));
+          s1.push_back(loc(q.k, q.n)); s2.push_back(loc(q.m, q.n)); sP.push_back(v2 ? pp(q.k, q.m) : nullptr);
+        }
       }
       auto put = [&](std::vector<void*>& v) { size_t o = hp.size(); hp.insert(hp.end(), v.begin(), v.end()); return o; };
-      L.nG = (int)gA.size(); L.oG = put(gA); put(gT);
-      L.nT = (int)tR.size(); L.oT = put(tR); put(tA); put(tT);
-      L.nL = (int)lV.size(); L.oL = put(lV); put(lT); put(lC);
-      L.nS = (int)sV.size(); L.oS = put(sV); put(sT); put(s1); put(s2);
+      L.nG = (int)gA.size(); L.oG = put(gA); put(gT); put(gP);
+      L.nT = (int)tR.size(); L.oT = put(tR); put(tA); put(tT); put(tP);
+      L.nL = (int)lV.size(); L.oL = put(lV); put(lT); put(lC); put(lP);
+      L.nS = (int)sV.size(); L.oS = put(sV); put(sT); put(s1); put(s2); put(sP);
     }
     if (cudaMalloc(&g_d.dptr, std::max<size_t>(hp.size(), 1) * sizeof(void*)) != cudaSuccess) {
       cudaGetLastError();
@@ -329,18 +350,27 @@ int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_loc
     }
     int rc;
     // ---- panel kernels on the owner, snapshot of V_kk into its panel slot ----
-    if (L.nG && (rc = launch_geqrt(NB, IB, L.nG, d + L.oG, d + L.oG + L.nG, g_d.sp))) return rc;
-    if (L.nT && (rc = launch_tsqrt(NB, IB, L.nT, d + L.oT, d + L.oT + L.nT, d + L.oT + 2 * L.nT, g_d.sp))) return rc;
-    for (const Task& q : L.panel)
-      if (q.kind == 0)  // before TSQRT(k, k+1) rewrites the upper part of tile (k, k)
-        TQ_CUDA(cudaMemcpyAsync(pv(q.k, q.k), loc(q.k, q.k), tile * sizeof(double),
-                                cudaMemcpyDeviceToDevice, g_d.sp));
+    const bool v2 = g_d.v2;
+    if (L.nG && (rc = launch_geqrt(NB, IB, L.nG, d + L.oG, d + L.oG + L.nG, g_d.sp, v2 ? d + L.oG + 2 * L.nG : nullptr)))
+      return rc;
+    if (L.nT && (rc = launch_tsqrt(NB, IB, L.nT, d + L.oT, d + L.oT + L.nT, d + L.oT + 2 * L.nT, g_d.sp,
+                                   v2 ? d + L.oT + 3 * L.nT : nullptr)))
+      return rc;
+    if (!v2)
+      for (const Task& q : L.panel)
+        if (q.kind == 0)  // before TSQRT(k, k+1) rewrites the upper part of tile (k, k)
+          TQ_CUDA(cudaMemcpyAsync(pv(q.k, q.k), loc(q.k, q.k), tile * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, g_d.sp));
     // ---- one grouped broadcast of this level's new V/T tiles -----------------
     if (!L.bcast.empty()) {
       TQ_CUDA(cudaEventRecord(g_d.ep, g_d.sp));
       TQ_CUDA(cudaStreamWaitEvent(g_d.sc, g_d.ep, 0));
       TQ_NCCL(ncclGroupStart());
       for (const Task& q : L.bcast) {
+        if (v2) {  // the packed tile (V and T) in its slot, in place on the root
+          TQ_NCCL(ncclBroadcast(pp(q.k, q.m), pp(q.k, q.m), g_d.pk_dbl, ncclDouble, q.root, g_d.comm, g_d.sc));
+          continue;
+        }
         const bool root = q.root == me;
         const double* sv = root ? (q.m == q.k ? pv(q.k, q.k) : loc(q.m, q.k)) : pv(q.k, q.m);
         const double* st = root ? locT(q.m, q.k) : pt(q.k, q.m);
@@ -350,6 +380,15 @@ int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_loc
       TQ_NCCL(ncclGroupEnd());
     }
     // ---- update kernels on the local columns ---------------------------------
+    if (v2) {
+      if (L.nL && (rc = launch_update_pk(true, NB, IB, L.nL, d + L.oL + 3 * L.nL, nullptr, d + L.oL + 2 * L.nL,
+                                         g_d.su)))
+        return rc;
+      if (L.nS && (rc = launch_update_pk(false, NB, IB, L.nS, d + L.oS + 4 * L.nS, d + L.oS + 2 * L.nS,
+                                         d + L.oS + 3 * L.nS, g_d.su)))
+        return rc;
+      continue;
+    }
     if (L.nL && (rc = launch_larfb(true, NB, IB, L.nL, d + L.oL, d + L.oL + L.nL, d + L.oL + 2 * L.nL, NB, g_d.su)))
       return rc;
     if (L.nS && (rc = launch_ssrfb(true, NB, IB, L.nS, d + L.oS, d + L.oS + L.nS, d + L.oS + 2 * L.nS,

@@ -44,17 +44,32 @@ int launch_v_to_tiles(int64_t M, int64_t K, const double* A, int64_t lda, int NB
 int launch_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t seed, uint64_t offset,
                        cudaStream_t s);
 int launch_zero_int(int* p, cudaStream_t s);
+// out[i] = base + i*stride, i < n (device pointer arrays for batched calls)
+int launch_fill_ptrs(double** out, double* base, size_t stride, int n, cudaStream_t s);
 
 // ---- tile kernels ---------------------------------------------------------
 // All take device arrays of device pointers (tiles NB x NB, ld NB; T IB x NB, ld IB).
-int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s);
+// Pk (nullable): per task, a packed copy of the reflector tile (V_p, T_p) for
+// the barrier-free update (update_v2.cuh; written when v2_supported(NB, IB)).
+int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s,
+                 double* const* Pk = nullptr);
 int launch_tsqrt(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
-                 cudaStream_t s);
+                 cudaStream_t s, double* const* Pk = nullptr);
 int launch_larfb(bool trans, int NB, int IB, int batch, const double* const* V,
                  const double* const* T, double* const* C, int ncols, cudaStream_t s);
 int launch_ssrfb(bool trans, int NB, int IB, int batch, const double* const* V2,
                  const double* const* T, double* const* C1, double* const* C2, int ncols,
                  cudaStream_t s);
+
+// Packed-reflector update path (update_v2.cuh): Q^T form, full tiles,
+// NB in {32, 64, 96, 128}, IB in {8, 16, 24, 32}, IB | NB.
+bool v2_supported(int NB, int IB);
+size_t v2_pk_doubles(int NB, int IB);  // doubles per packed reflector tile
+int launch_update_pk(bool larfb, int NB, int IB, int batch, const double* const* Pk, double* const* C1,
+                     double* const* C2, cudaStream_t s);
+// standard V (GEQRT form if larfb) / T tiles -> packed tiles
+int launch_pack(bool larfb, int NB, int IB, int batch, const double* const* V, const double* const* T,
+                double* const* Pk, cudaStream_t s);
 
 // Which SSRFB implementation a (NB, IB) pair uses ("dmma" or "simt").
 const char* ssrfb_impl_name(int NB, int IB);

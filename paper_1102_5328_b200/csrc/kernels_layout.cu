@@ -212,6 +212,18 @@ int launch_nonfinite_check(const double* A, int64_t n, int* d_info, cudaStream_t
   return 0;
 }
 
+__global__ void fill_ptrs_kernel(double** out, double* base, size_t stride, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = base + stride * i;
+}
+
+int launch_fill_ptrs(double** out, double* base, size_t stride, int n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  fill_ptrs_kernel<<<(n + 255) / 256, 256, 0, s>>>(out, base, stride, n);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
 int launch_zero_int(int* p, cudaStream_t s) {
   zero_int_kernel<<<1, 1, 0, s>>>(p);
   TQ_LAUNCH_CHECK();

@@ -296,9 +296,10 @@ int launch_panel(int NB, int IB, int batch, double* const* R, double* const* B, 
 }  // namespace
 
 bool panel_fast_supported(int NB, int IB);
-int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s);
+int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s,
+                      double* const* Pk);
 int launch_tsqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
-                      double* const* T, cudaStream_t s);
+                      double* const* T, cudaStream_t s, double* const* Pk);
 
 static bool generic_panel_forced() {
   static int v = -1;
@@ -309,19 +310,24 @@ static bool generic_panel_forced() {
   return v == 1;
 }
 
-int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s) {
+int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s,
+                 double* const* Pk) {
   if (batch <= 0) return 0;
   if (panel_fast_supported(NB, IB) && !generic_panel_forced())
-    return launch_geqrt_fast(NB, IB, batch, A, T, s);
-  return launch_panel<false>(NB, IB, batch, A, nullptr, T, s);
+    return launch_geqrt_fast(NB, IB, batch, A, T, s, Pk);
+  int rc = launch_panel<false>(NB, IB, batch, A, nullptr, T, s);
+  if (!rc && Pk) rc = launch_pack(true, NB, IB, batch, A, T, Pk, s);
+  return rc;
 }
 
 int launch_tsqrt(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
-                 cudaStream_t s) {
+                 cudaStream_t s, double* const* Pk) {
   if (batch <= 0) return 0;
   if (panel_fast_supported(NB, IB) && !generic_panel_forced())
-    return launch_tsqrt_fast(NB, IB, batch, R, A2, T, s);
-  return launch_panel<true>(NB, IB, batch, R, A2, T, s);
+    return launch_tsqrt_fast(NB, IB, batch, R, A2, T, s, Pk);
+  int rc = launch_panel<true>(NB, IB, batch, R, A2, T, s);
+  if (!rc && Pk) rc = launch_pack(false, NB, IB, batch, A2, T, Pk, s);
+  return rc;
 }
 
 }  // namespace tileqr

@@ -1,368 +1,33 @@
-// kernels_panel_fast.cu -- low-latency GEQRT / TSQRT for the critical path of
-// the tile QR: NB % 32 == 0,
-// NB <= 256, IB in {8, 16, 24, 32}.  Every other (NB, IB) uses the generic
-// panel kernel (kernels_panel.cu).
-//
-// One CTA of 8 warps per task.  For each inner panel p (IB columns):
-//  1. Factor: the NB x IB panel lives in registers, lane l holding column l
-//     and warp w rows [w*NB/8, (w+1)*NB/8).  Per column j ONE pass of partial
-//     dot products gives sigma = ||x2||^2 and every d_c = x2 . P(:,c) (the
-//     pivot column is broadcast with warp shuffles), one CTA barrier combines
-//     the 8 warp partials (double-buffered, so no second barrier), and every
-//     thread forms beta/tau (R1) and applies the rank-1 update to
-//     its own registers.
-//  2. T_p: the Gram matrix V_p^T V_p on DMMA (mma.sync.m8n8k4.f64) from the
-//     staged panel, then the forward recurrence
-//     T[0:i,i] = -tau_i T[0:i,0:i] G[0:i,i], one thread per row of T.
-//  3. Trailing columns: each warp takes 8-column blocks, holds them for all
-//     NB rows in registers (transposed accumulator) and applies
-//     W = [R_p; C]^T-part ... exactly the SSRFB/LARFB steps A/B/C of
-//     kernels_update.cu on DMMA, reading V_p (swizzled) and T_p from smem.
-// TSQRT never writes the strict lower part of R (read concurrently by the
-// LARFB of the same DAG level).
-#include <math.h>
+// kernels_panel_fast.cu -- batched launch of the low-latency GEQRT / TSQRT
+// (body in panel_fast.cuh): one CTA of 8 warps per task.
 #include <stdlib.h>
 
-#include <type_traits>
-
-#include "dmma.cuh"
-#include "internal.h"
+#include "panel_fast.cuh"
 
 namespace tileqr {
+
+#ifndef TILEQR_PANEL_PROF
+__device__ unsigned long long g_panel_prof[16];  // phase cycles; filled only with -DTILEQR_PANEL_PROF
+#endif
+
 namespace {
-
-constexpr int LDV = 40;   // >= 32, == 8 mod 16
-constexpr int LDT = 36;   // == 4 mod 16
-constexpr int LDW = 36;
-constexpr int LDG = 33;
-constexpr int LDR = 33;
-
-__device__ unsigned long long g_panel_prof[16];  // diagnostic phase cycles (thread 0)
-
-template <int NB, int kWarps>
-struct FastSmem {
-  double Vs[NB * LDV];
-  double Ts[32 * LDT];
-  double Gs[32 * LDG];
-  double Rin[32 * LDR];
-  double Rout[32 * LDR];
-  double red[2][kWarps][32];
-  double rowj[2][32];
-  double tau[32];
-  double Ws[kWarps][8 * LDW];
-};
+using pf::FastSmem;
 
 template <bool TS, int NB, int kWarps>
 __global__ void __launch_bounds__(kWarps * 32, 1)
-panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* Tp) {
-  constexpr int kThreads = kWarps * 32;
-  constexpr int RW = NB / kWarps;  // rows per warp in the factorization
-  constexpr int RB = NB / 8;       // 8-row blocks in the trailing update
+panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* Tp, double* const* Pk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FastSmem<NB, kWarps>& S = *reinterpret_cast<FastSmem<NB, kWarps>*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int a = lane & 3, g = lane >> 2;
-  double* const R = Rp[blockIdx.x];              // TSQRT: R tile; GEQRT: the tile
-  double* const B = TS ? Bp[blockIdx.x] : R;     // TSQRT: square tile; GEQRT: the tile
-  double* const Tg = Tp[blockIdx.x];
-
-  for (int e = tid; e < 32 * LDT; e += kThreads) S.Ts[e] = 0.0;  // zero padding for the T merges
-  for (int e = tid; e < 32 * LDG; e += kThreads) S.Gs[e] = 0.0;
-  long long tp0 = clock64(), tp1;
-#define TQ_PHASE(k) do { if (tid == 0) { tp1 = clock64(); atomicAdd(&g_panel_prof[k], (unsigned long long)(tp1 - tp0)); tp0 = tp1; } } while (0)
-  for (int c0 = 0; c0 < NB; c0 += IB) {
-    // ---- stage the panel (coalesced) and, for TSQRT, the R block -------------
-    for (int idx = tid; idx < NB * IB; idx += kThreads) {
-      const int c = idx / NB, r = idx - c * NB;
-      S.Vs[vsw(r, c, LDV)] = B[r + (size_t)(c0 + c) * NB];
-    }
-    if (TS) {
-      for (int idx = tid; idx < IB * IB; idx += kThreads) {
-        const int c = idx / IB, i = idx - c * IB;
-        S.Rin[i * LDR + c] = (i <= c) ? R[(c0 + i) + (size_t)(c0 + c) * NB] : 0.0;
-      }
-    }
-    __syncthreads();
-    double x[RW];
-#pragma unroll
-    for (int q = 0; q < RW; ++q)  // GEQRT: rows above the panel (R of earlier panels) stay out
-      x[q] = (lane < IB && (TS || warp * RW + q >= c0)) ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
-
-    TQ_PHASE(0);
-    // ---- 1. factor the panel column by column --------------------------------
-    int buf = 0;
-    for (int jj = 0; jj < IB; ++jj) {
-      const int j = c0 + jj;
-      if (!TS && warp == j / RW) {
-        // GEQRT: row j leaves the reflector rows.  Its values go to smem (alpha
-        // and the R(j, c) inputs) and the registers of lanes >= jj are zeroed, so
-        // every R row sits as 0 in the registers: the dots and the rank-1 update
-        // below then run over all rows with no masks (rows < j hold 0 in the
-        // pivot column, lanes < jj keep their V entries of row j).
-        double rv = 0.0;
-#pragma unroll
-        for (int q = 0; q < RW; ++q)
-          if (warp * RW + q == j) {
-            rv = x[q];
-            if (lane >= jj) x[q] = 0.0;
-          }
-        S.rowj[buf][lane] = rv;
-      }
-      double vj[RW];
-      double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
-#pragma unroll
-      for (int q = 0; q < RW; ++q) {
-        vj[q] = __shfl_sync(0xffffffffu, x[q], jj);
-        pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
-      }
-      S.red[buf][warp][lane] = (pp[0] + pp[1]) + (pp[2] + pp[3]);
-      __syncthreads();
-      double ps[kWarps], pd[kWarps];
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        ps[w] = S.red[buf][w][jj];
-        pd[w] = S.red[buf][w][lane];
-      }
-#pragma unroll
-      for (int h = kWarps / 2; h > 0; h >>= 1)  // pairwise tree (fixed order: deterministic)
-#pragma unroll
-        for (int w = 0; w < h; ++w) {
-          ps[w] += ps[w + h];
-          pd[w] += pd[w + h];
-        }
-      const double sigma = ps[0], d = pd[0];
-      const double alpha = TS ? S.Rin[jj * LDR + jj] : S.rowj[buf][jj];
-      const double rjl = TS ? S.Rin[jj * LDR + lane] : S.rowj[buf][lane];
-      double tau = 0.0, scal = 0.0, beta = alpha;
-      if (sigma != 0.0) {
-        // Reflector rule (R1) from one reciprocal square root and one
-        // reciprocal: with s = alpha^2 + sigma, rs = 1/sqrt(s), nrm = s*rs,
-        //   beta = -sgn(alpha) nrm,  tau = (beta - alpha)/beta = 1 + |alpha| rs,
-        //   scal = 1/(alpha - beta) = sgn(alpha) / (|alpha| + nrm).
-        // Branch-free Newton refinement (s > 0 and O(1) data: no special cases).
-        const double s2 = fma(alpha, alpha, sigma);
-        double rs;
-        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(s2));
-        const double hs = -0.5 * s2;
-        rs = rs * fma(hs, rs * rs, 1.5);
-        rs = rs * fma(hs, rs * rs, 1.5);
-        const double nrm = s2 * rs;
-        const double aa = fabs(alpha);
-        const double sg = (alpha >= 0.0) ? 1.0 : -1.0;
-        beta = -sg * nrm;
-        tau = fma(aa, rs, 1.0);
-        const double den = aa + nrm;
-        double rc;
-        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
-        rc = fma(rc, fma(-den, rc, 1.0), rc);
-        rc = fma(rc, fma(-den, rc, 1.0), rc);
-        scal = sg * rc;
-      }
-      const double w = fma(scal, d, rjl);
-      const double tw = lane < IB ? tau * w : 0.0;
-      // select-free rank-1 update of the reflector rows, x += coef * vj:
-      //   lane == jj: coef = scal - 1 (vj == x there: x becomes v2 = x2 * scal);
-      //   lane >  jj: coef = -tw * scal;   lane < jj: coef = 0.
-      const double coef = (lane == jj) ? scal - 1.0 : (lane > jj ? -tw * scal : 0.0);
-#pragma unroll
-      for (int q = 0; q < RW; ++q) x[q] = fma(coef, vj[q], x[q]);
-      // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
-      if (warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
-      if (tid == 0) S.tau[jj] = tau;
-      buf ^= 1;
-    }
-    __syncthreads();  // everyone done reading Vs (panel values) and red
-    TQ_PHASE(1);
-
-    // ---- write the factored panel: registers -> smem -> global (coalesced) ----
-#pragma unroll
-    for (int q = 0; q < RW; ++q) S.Vs[vsw(warp * RW + q, lane, LDV)] = lane < IB ? x[q] : 0.0;
-    __syncthreads();
-    for (int idx = tid; idx < NB * IB; idx += kThreads) {
-      const int c = idx / NB, r = idx - c * NB;
-      double* p = &S.Vs[vsw(r, c, LDV)];
-      const double v = *p;
-      if (TS) {
-        B[r + (size_t)(c0 + c) * NB] = v;  // V2
-      } else {
-        // GEQRT: V strictly below the diagonal (registers), R on/above it (Rout)
-        if (r > c0 + c) B[r + (size_t)(c0 + c) * NB] = v;
-        else if (r >= c0) B[r + (size_t)(c0 + c) * NB] = S.Rout[(r - c0) * LDR + c];
-        // the DMMA operand is the unit lower trapezoid V_p (same thread, no hazard)
-        *p = (r == c0 + c) ? 1.0 : (r > c0 + c ? v : 0.0);
-      }
-    }
-    if (TS) {
-      for (int idx = tid; idx < IB * IB; idx += kThreads) {
-        const int c = idx / IB, i = idx - c * IB;
-        if (i <= c) R[(c0 + i) + (size_t)(c0 + c) * NB] = S.Rout[i * LDR + c];
-      }
-    }
-
-    __syncthreads();  // GEQRT rewrote Vs in place: complete before the Gram product
-    TQ_PHASE(2);
-    // ---- 2. T_p: G = V_p^T V_p (DMMA), recurrence ---------------------------
-    {
-      const int nbk = IB / 8;
-      int blk = 0;
-      for (int mb = 0; mb < nbk; ++mb)
-        for (int nb = mb; nb < nbk; ++nb, ++blk) {
-          if (blk % kWarps != warp) continue;
-          double g0 = 0.0, g1 = 0.0;
-          const int k0 = TS ? 0 : (c0 & ~3);
-          for (int k4 = k0; k4 < NB; k4 += 4) {
-            const int r = k4 + a;
-            dmma(g0, g1, S.Vs[vsw(r, 8 * mb + g, LDV)], S.Vs[vsw(r, 8 * nb + g, LDV)]);
-          }
-          S.Gs[(8 * mb + g) * LDG + 8 * nb + 2 * a] = g0;
-          S.Gs[(8 * mb + g) * LDG + 8 * nb + 2 * a + 1] = g1;
-        }
-    }
-    __syncthreads();
-    TQ_PHASE(5);
-    // T_p in parallel: 8x8 diagonal blocks by the column recurrence, then
-    // pairwise merges T12 = -T11 G12 T22 (Q1 Q2 = I - [V1 V2] [T11 T12; 0 T22]
-    // [V1 V2]^T), log2(IB/8) levels.
-    if (tid < IB) {
-      // thread r: row r of its 8x8 diagonal block, fully unrolled in registers
-      // (the G and tau loads do not depend on the recurrence and are hoisted)
-      const int b0 = tid & ~7, rr = tid & 7;
-      double tr[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < i; ++l)
-          if (l >= rr) acc = fma(tr[l], S.Gs[(b0 + l) * LDG + b0 + i], acc);
-        const double ti = S.tau[b0 + i];
-        tr[i] = (i < rr) ? 0.0 : (i == rr ? ti : -ti * acc);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) S.Ts[tid + (b0 + i) * LDT] = tr[i];
-    }
-    __syncthreads();
-    TQ_PHASE(6);
-    // merges: Ts/Gs are zero outside the computed blocks (zero-filled at kernel
-    // start), so every dot runs over the full block width with no bounds
-    auto merge = [&](auto sz) {
-      constexpr int SZ = decltype(sz)::value;
-      const int npair = (IB + SZ - 1) / (2 * SZ);  // pairs with a non-empty right block
-      for (int e = tid; e < npair * SZ * SZ; e += kThreads) {  // X = G12 T22
-        const int p = e / (SZ * SZ), il = (e / SZ) % SZ, kl = e % SZ, st = p * 2 * SZ;
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < SZ; ++l)
-          acc = fma(S.Gs[(st + il) * LDG + st + SZ + l], S.Ts[(st + SZ + l) + (st + SZ + kl) * LDT], acc);
-        S.Rin[(st + il) * LDR + st + SZ + kl] = acc;  // Rin is free after the factorization
-      }
-      __syncthreads();
-      for (int e = tid; e < npair * SZ * SZ; e += kThreads) {  // T12 = -T11 X
-        const int p = e / (SZ * SZ), il = (e / SZ) % SZ, kl = e % SZ, st = p * 2 * SZ;
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < SZ; ++l)
-          acc = fma(S.Ts[(st + il) + (st + l) * LDT], S.Rin[(st + l) * LDR + st + SZ + kl], acc);
-        S.Ts[(st + il) + (st + SZ + kl) * LDT] = -acc;
-      }
-      __syncthreads();
-    };
-    if (IB > 8) merge(std::integral_constant<int, 8>{});
-    if (IB > 16) merge(std::integral_constant<int, 16>{});
-    TQ_PHASE(7);
-    for (int e = tid; e < IB * IB; e += kThreads) {
-      const int i = e / IB, r = e - i * IB;
-      Tg[(size_t)(c0 + i) * IB + r] = (r <= i) ? S.Ts[r + i * LDT] : 0.0;
-    }
-    __syncthreads();
-    TQ_PHASE(8);
-    for (int e = tid; e < IB * IB; e += kThreads) {  // DIAGNOSTIC: same loop again (warm I-cache)
-      const int i = e / IB, r = e - i * IB;
-      Tg[(size_t)(c0 + i) * IB + r] = (r <= i) ? S.Ts[r + i * LDT] : 0.0;
-    }
-    __syncthreads();
-    TQ_PHASE(9);
-
-    __syncthreads();
-    TQ_PHASE(3);
-    // ---- 3. trailing columns [c0+IB, NB): 8-column blocks per warp ------------
-    double* Wsw = S.Ws[warp];
-    const int nbi = IB / 8;
-    for (int cb = c0 + IB + 8 * warp; cb < NB; cb += 8 * kWarps) {
-      const int col = cb + g;
-      double acc[RB][2];
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        const double2 v = *reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)col * NB);
-        acc[rb][0] = v.x;
-        acc[rb][1] = v.y;
-      }
-      // step A: W^T(col, i) = [TS: R(c0+i, col)] + sum_r C^T(col, r) V_p(r, i)
-      double wacc[4][2];
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-          wacc[nb][j] = (TS && nb < nbi) ? R[(c0 + 8 * nb + 2 * a + j) + (size_t)col * NB] : 0.0;
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        if (!TS && 8 * rb + 7 < c0) continue;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int r = 8 * rb + 2 * a + j;
-#pragma unroll
-          for (int nb = 0; nb < 4; ++nb)
-            if (nb < nbi) dmma(wacc[nb][0], wacc[nb][1], acc[rb][j], S.Vs[vsw(r, 8 * nb + g, LDV)]);
-        }
-      }
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
-        if (nb < nbi) {
-          Wsw[g * LDW + 8 * nb + 2 * a] = wacc[nb][0];
-          Wsw[g * LDW + 8 * nb + 2 * a + 1] = wacc[nb][1];
-        }
-      __syncwarp();
-      // step B: W'^T = W^T T_p (descending blocks, in place); TS: R(c0+i, col) -= W'
-      for (int nb = nbi - 1; nb >= 0; --nb) {
-        double o0 = 0.0, o1 = 0.0;
-        for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
-          dmma(o0, o1, Wsw[g * LDW + k4 + a], S.Ts[(k4 + a) + (8 * nb + g) * LDT]);
-        __syncwarp();
-        Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
-        Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
-        if (TS) {
-          R[(c0 + 8 * nb + 2 * a) + (size_t)col * NB] -= o0;
-          R[(c0 + 8 * nb + 2 * a + 1) + (size_t)col * NB] -= o1;
-        }
-        __syncwarp();
-      }
-      // step C: C^T(col, r) += (-W'^T)(col, i) V_p(r, i)
-      for (int k4 = 0; k4 < IB; k4 += 4) {
-        const double af = Wsw[g * LDW + k4 + a];
-#pragma unroll
-        for (int rb = 0; rb < RB; ++rb) {
-          if (!TS && 8 * rb + 7 < c0) continue;
-          dmma(acc[rb][0], acc[rb][1], af, S.Vs[vsw(8 * rb + g, k4 + a, LDV)]);
-        }
-      }
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb)
-        *reinterpret_cast<double2*>(B + 8 * rb + 2 * a + (size_t)col * NB) =
-            make_double2(acc[rb][0], acc[rb][1]);
-      __syncwarp();
-    }
-    __syncthreads();  // trailing writes visible before the next panel is staged
-    TQ_PHASE(4);
-  }
-#undef TQ_PHASE
+  pf::panel_fast_body<TS, NB, kWarps>(IB, Rp[blockIdx.x], TS ? Bp[blockIdx.x] : nullptr, Tp[blockIdx.x],
+                                      smem_raw, Pk ? Pk[blockIdx.x] : nullptr);
 }
 
 template <bool TS, int NB, int NW>
 int launch_fast_w(int IB, int batch, double* const* R, double* const* B, double* const* T,
-                  cudaStream_t s) {
+                  cudaStream_t s, double* const* Pk) {
   auto kern = panel_fast_kernel<TS, NB, NW>;
   const size_t bytes = sizeof(FastSmem<NB, NW>);
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  kern<<<batch, NW * 32, bytes, s>>>(IB, R, B, T);
+  kern<<<batch, NW * 32, bytes, s>>>(IB, R, B, T, Pk);
   TQ_LAUNCH_CHECK();
   return 0;
 }
@@ -379,23 +44,23 @@ int panel_warps() {
 
 template <bool TS, int NB>
 int launch_fast_t(int IB, int batch, double* const* R, double* const* B, double* const* T,
-                  cudaStream_t s) {
-  return panel_warps() == 8 ? launch_fast_w<TS, NB, 8>(IB, batch, R, B, T, s)
-                            : launch_fast_w<TS, NB, 4>(IB, batch, R, B, T, s);
+                  cudaStream_t s, double* const* Pk) {
+  return panel_warps() == 8 ? launch_fast_w<TS, NB, 8>(IB, batch, R, B, T, s, Pk)
+                            : launch_fast_w<TS, NB, 4>(IB, batch, R, B, T, s, Pk);
 }
 
 template <bool TS>
 int launch_fast(int NB, int IB, int batch, double* const* R, double* const* B, double* const* T,
-                cudaStream_t s) {
+                cudaStream_t s, double* const* Pk) {
   switch (NB) {
-    case 32: return launch_fast_t<TS, 32>(IB, batch, R, B, T, s);
-    case 64: return launch_fast_t<TS, 64>(IB, batch, R, B, T, s);
-    case 96: return launch_fast_t<TS, 96>(IB, batch, R, B, T, s);
-    case 128: return launch_fast_t<TS, 128>(IB, batch, R, B, T, s);
-    case 160: return launch_fast_t<TS, 160>(IB, batch, R, B, T, s);
-    case 192: return launch_fast_t<TS, 192>(IB, batch, R, B, T, s);
-    case 224: return launch_fast_t<TS, 224>(IB, batch, R, B, T, s);
-    case 256: return launch_fast_t<TS, 256>(IB, batch, R, B, T, s);
+    case 32: return launch_fast_t<TS, 32>(IB, batch, R, B, T, s, Pk);
+    case 64: return launch_fast_t<TS, 64>(IB, batch, R, B, T, s, Pk);
+    case 96: return launch_fast_t<TS, 96>(IB, batch, R, B, T, s, Pk);
+    case 128: return launch_fast_t<TS, 128>(IB, batch, R, B, T, s, Pk);
+    case 160: return launch_fast_t<TS, 160>(IB, batch, R, B, T, s, Pk);
+    case 192: return launch_fast_t<TS, 192>(IB, batch, R, B, T, s, Pk);
+    case 224: return launch_fast_t<TS, 224>(IB, batch, R, B, T, s, Pk);
+    case 256: return launch_fast_t<TS, 256>(IB, batch, R, B, T, s, Pk);
     default: return -1;
   }
 }
@@ -415,13 +80,14 @@ bool panel_fast_supported(int NB, int IB) {
   return NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB <= 32;
 }
 
-int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s) {
-  return launch_fast<false>(NB, IB, batch, A, nullptr, T, s);
+int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const* T, cudaStream_t s,
+                      double* const* Pk) {
+  return launch_fast<false>(NB, IB, batch, A, nullptr, T, s, Pk);
 }
 
 int launch_tsqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
-                      double* const* T, cudaStream_t s) {
-  return launch_fast<true>(NB, IB, batch, R, A2, T, s);
+                      double* const* T, cudaStream_t s, double* const* Pk) {
+  return launch_fast<true>(NB, IB, batch, R, A2, T, s, Pk);
 }
 
 }  // namespace tileqr

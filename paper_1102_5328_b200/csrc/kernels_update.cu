@@ -203,4 +203,51 @@ int launch_ssrfb(bool trans, int NB, int IB, int batch, const double* const* V2,
   return launch_simt<false>(trans, NB, IB, batch, V2, T, C1, C2, ncols, s);
 }
 
+// ---- packed-reflector (barrier-free) path: update_v2.cuh ----------------------
+#define TQ_DECL_PK(nb)                                                                              \
+  int launch_update_pk_nb##nb(bool larfb, int IB, int batch, const double* const* Pk, double* const* C1, \
+                              double* const* C2, cudaStream_t s);                                   \
+  int launch_pack_nb##nb(bool larfb, int IB, int batch, const double* const* V, const double* const* T, \
+                         double* const* Pk, cudaStream_t s);
+TQ_DECL_PK(32) TQ_DECL_PK(64) TQ_DECL_PK(96) TQ_DECL_PK(128)
+#undef TQ_DECL_PK
+
+bool v2_supported(int NB, int IB) {
+  if (force_simt()) return false;
+  const char* e = getenv("TILEQR_NO_V2");
+  if (e && e[0] == '1') return false;
+  return (NB == 32 || NB == 64 || NB == 96 || NB == 128) && IB % 8 == 0 && IB >= 8 && IB <= 32 && NB % IB == 0;
+}
+
+size_t v2_pk_doubles(int NB, int IB) {
+  if (IB % 8 || IB < 8 || IB > 32 || NB % IB) return 0;
+  const int GW = IB <= 16 ? 16 : 32, PW = IB == 8 ? 8 : GW, PPG = GW / PW, NP = NB / IB;
+  const int NG = (NP + PPG - 1) / PPG, LDT2 = IB <= 16 ? 18 : 34;
+  return (size_t)NG * NB * GW + (size_t)NP * IB * LDT2;
+}
+
+int launch_update_pk(bool larfb, int NB, int IB, int batch, const double* const* Pk, double* const* C1,
+                     double* const* C2, cudaStream_t s) {
+  if (batch <= 0) return 0;
+  switch (NB) {
+    case 32: return launch_update_pk_nb32(larfb, IB, batch, Pk, C1, C2, s);
+    case 64: return launch_update_pk_nb64(larfb, IB, batch, Pk, C1, C2, s);
+    case 96: return launch_update_pk_nb96(larfb, IB, batch, Pk, C1, C2, s);
+    case 128: return launch_update_pk_nb128(larfb, IB, batch, Pk, C1, C2, s);
+    default: set_error("packed update: NB not in {32, 64, 96, 128}"); return TILEQR_ERR_CUDA;
+  }
+}
+
+int launch_pack(bool larfb, int NB, int IB, int batch, const double* const* V, const double* const* T,
+                double* const* Pk, cudaStream_t s) {
+  if (batch <= 0) return 0;
+  switch (NB) {
+    case 32: return launch_pack_nb32(larfb, IB, batch, V, T, Pk, s);
+    case 64: return launch_pack_nb64(larfb, IB, batch, V, T, Pk, s);
+    case 96: return launch_pack_nb96(larfb, IB, batch, V, T, Pk, s);
+    case 128: return launch_pack_nb128(larfb, IB, batch, V, T, Pk, s);
+    default: set_error("pack: NB not in {32, 64, 96, 128}"); return TILEQR_ERR_CUDA;
+  }
+}
+
 }  // namespace tileqr

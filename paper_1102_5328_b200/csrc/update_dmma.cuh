@@ -26,7 +26,7 @@
 namespace tileqr {
 namespace upd {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 4;  // warps per CTA of the batched kernels (the DAG kernel uses 8)
 constexpr int kThreads = kWarps * 32;
 
 // Row-major V chunk, ld = LDV (a multiple of 16, no padding): element (r, i)
@@ -44,43 +44,39 @@ struct Geo {
 };
 
 // smem doubles of one stage buffer set and of the per-warp W^T
-template <int NB, int MB, int KW, bool LARFB, bool MULTI>
+template <int NB, int MB, int KW, bool LARFB, bool MULTI, int W = kWarps>
 struct Layout {
   static constexpr int CHUNK = NB * Geo<KW>::LDV;
   static constexpr int TBUF = MULTI ? 0 : KW * Geo<KW>::LDT;
-  static constexpr int CBUF = LARFB ? 0 : kWarps * 8 * MB * Geo<KW>::LDC;
+  static constexpr int CBUF = LARFB ? 0 : W * 8 * MB * Geo<KW>::LDC;
   static constexpr int STAGE = CHUNK + TBUF + CBUF;
 };
 
 // MULTI: IBp > 32, processed as nch chunks of KW = 32 columns (last chunk
 // zero-padded); V_p is staged twice per panel (for step A and for step C) and
 // T_p is read from global memory.
-template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI>
-__global__ void __launch_bounds__(kThreads)
-update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double* const* Tp,
-              double* const* C1p, double* const* C2p, int twobuf) {
-  using L = Layout<NB, MB, KW, LARFB, MULTI>;
+// Body of one CTA (W warps): columns [col0, col0 + W*8*MB) of one task.
+template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI, int W>
+__device__ __forceinline__ void update_body(int IB, int IBp, int ncols, const double* __restrict__ V,
+                                            const double* __restrict__ T, double* __restrict__ C1,
+                                            double* __restrict__ C2, int twobuf, int col0,
+                                            double* __restrict__ smem) {
+  constexpr int kThreads = W * 32;
+  using L = Layout<NB, MB, KW, LARFB, MULTI, W>;
   constexpr int RB = NB / 8;
   constexpr int LDV = Geo<KW>::LDV;
   constexpr int LDT = Geo<KW>::LDT;
   constexpr int LDC = Geo<KW>::LDC;
   constexpr int NBK = KW / 8;  // 8-column blocks per chunk
-  constexpr int CPC = kWarps * 8 * MB;  // columns per CTA
   const int LDW = MULTI ? IBp + 4 : KW + 4;  // == 4 mod 16 (IBp % 32 == 0 when MULTI)
-  extern __shared__ __align__(16) double smem[];
   // [stage 0: V | T | C1][stage 1: V | T | C1][W^T per warp] (one stage if !twobuf)
   const int nbuf = twobuf ? 2 : 1;
   double* const Wsw = smem + nbuf * L::STAGE + (threadIdx.x >> 5) * 8 * MB * LDW;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int a = lane & 3, g = lane >> 2;
-  const int b = blockIdx.y;
-  const int col0 = blockIdx.x * CPC;                    // first column of this CTA
-  const int wcl0 = warp * 8 * MB;                       // first column of this warp (CTA-local)
-  const double* __restrict__ V = Vp[b];
-  const double* __restrict__ T = Tp[b];
-  double* __restrict__ C1 = LARFB ? nullptr : C1p[b];
-  double* __restrict__ C2 = C2p[b];
+  constexpr int CPC = W * 8 * MB;  // columns per CTA
+  const int wcl0 = warp * 8 * MB;  // first column of this warp (CTA-local)
 
   const int np = NB / IB;
   const int nch = MULTI ? (IBp + KW - 1) / KW : 1;
@@ -92,9 +88,10 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
   auto item_phase = [&](int idx) { if (!MULTI) return 2; return (idx % (2 * nch)) < nch ? 0 : 1; };
 
   // Per-thread constants of the fast V staging (SSRFB, one chunk per panel):
-  // warp instruction `it` moves rows 4*((4*it % RG) + warp) + [0,4) of columns
-  // 8*(4*it / RG) + [0,8); the swizzle of those rows is a per-thread constant.
-  constexpr int RG = NB / 4;  // 4-row groups (NB % 16 == 0, so RG % 4 == 0)
+  // warp instruction `it` moves rows 4*((W*it % RG) + warp) + [0,4) of columns
+  // 8*(W*it / RG) + [0,8); the swizzle of those rows is a per-thread constant.
+  constexpr int RG = NB / 4;  // 4-row groups (NB % 32 == 0, so RG % W == 0)
+  static_assert(RG % W == 0, "row groups per warp instruction");
   const int st_r = 4 * warp + (lane & 3), st_c = lane >> 2;
   const int st_sw = usw(st_r);
   auto stage = [&](int idx, int slot) {
@@ -106,7 +103,7 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
       double* dst = vb + st_r * LDV + (st_c ^ st_sw);
 #pragma unroll
       for (int it = 0; it < NB * KW / kThreads; ++it) {
-        const int rg0 = (4 * it) % RG, cg = (4 * it) / RG;  // compile-time
+        const int rg0 = (W * it) % RG, cg = (W * it) / RG;  // compile-time
         const int ii = 8 * cg + st_c;
         double* d = dst + 4 * rg0 * LDV + (((8 * cg) ^ (st_c ^ st_sw)) - (st_c ^ st_sw));
         if (ii < IB) cp_async8(d, src + 4 * rg0 + (size_t)(8 * cg) * NB);
@@ -350,6 +347,16 @@ update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double*
             make_double2(acc[mb][rb][0], acc[mb][rb][1]);
     }
   }
+}
+
+template <int NB, int MB, int KW, bool TRANS, bool LARFB, bool MULTI>
+__global__ void __launch_bounds__(kThreads)
+update_kernel(int IB, int IBp, int ncols, const double* const* Vp, const double* const* Tp,
+              double* const* C1p, double* const* C2p, int twobuf) {
+  extern __shared__ __align__(16) double smem[];
+  const int b = blockIdx.y;
+  update_body<NB, MB, KW, TRANS, LARFB, MULTI, kWarps>(IB, IBp, ncols, Vp[b], Tp[b], LARFB ? nullptr : C1p[b],
+                                                       C2p[b], twobuf, blockIdx.x * kWarps * 8 * MB, smem);
 }
 
 inline int round_up8(int x) { return (x + 7) / 8 * 8; }

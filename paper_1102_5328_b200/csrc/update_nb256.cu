@@ -1,5 +1,7 @@
-// update_nb256.cu -- instantiation of the DMMA update kernels for NB = 256
-// (one translation unit per NB so the build compiles them in parallel).
+// update_nb256.cu -- instantiation of the DMMA update kernels and of the
+// dataflow DAG kernel for NB = 256 (one translation unit per NB so the build
+// compiles them in parallel).
+#include "dag.cuh"
 #include "update_dmma.cuh"
 
 namespace tileqr {
@@ -7,5 +9,9 @@ int launch_update_nb256(bool trans, bool larfb, int IB, int batch, const double*
                         const double* const* T, double* const* C1, double* const* C2, int ncols,
                         cudaStream_t s) {
   return upd::launch_update_dmma<256>(trans, larfb, IB, batch, V, T, C1, C2, ncols, s);
+}
+int launch_dag_nb256(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
+                     unsigned long long* prof, cudaStream_t s) {
+  return dag::launch_dag_nb<256>(IB, items, nitems, next, done, nsm, prof, s);
 }
 }  // namespace tileqr

@@ -1,0 +1,430 @@
+// update_v2.cuh -- barrier-free DMMA trailing update (SSRFB / LARFB, Q^T
+// form) of the tile QR,
+// fed by a PACKED copy of the reflector tile that the panel kernels write.
+//
+// For every inner panel p of IB reflectors, ascending:
+//   step A  W^T  = C1[p rows]^T + C2^T V_p          (LARFB: C^T V_p)
+//   step B  W'^T = W^T T_p                           (W' = T_p^T W)
+//   C1[p rows] -= W'                                 (SSRFB only)
+//   step C  C2^T -= W'^T V_p^T                       (LARFB: C^T -= W'^T V_p^T)
+//
+// Design (B200, FP64 mma.sync.m8n8k4 = SASS DMMA.8x8x4; tcgen05 has no f64):
+//  * Each warp owns 8*MB columns of C2 for ALL NB rows, in registers, as the
+//    transposed accumulator C2^T, for the whole task (C2 crosses HBM once).
+//  * The k index of every m8n8k4 step is permuted so that the A fragment of
+//    a step is an accumulator register: step A feeds C2^T (k = rows
+//    8rb+2t+j), step B feeds W^T (k = reflectors 8kb+2t+s) and step C feeds
+//    W'^T (same).  W never leaves registers: no shared-memory round trip, no
+//    __syncwarp, no CTA barrier anywhere in the task.
+//  * V and T come from the packed tile (below), a smem image that TMA bulk
+//    copies (cp.async.bulk + mbarrier complete_tx) land in one piece per
+//    column group; each warp waits on the group's mbarrier and then runs all
+//    its panels independently of the other warps.
+//  * C1 rows of panel p+1 are prefetched into registers during panel p.
+//
+// Packed reflector tile (written by the GEQRT/TSQRT kernels, panel_fast.cuh):
+//   V: NG column groups of GW columns (GW = 16 for IB in {8,16}, 32 for IB in
+//   {24,32}), each an NB x GW row-major block; element (r, c) of a group at
+//   r*GW + (c ^ pk_f(r & 7)), pk_f(r) = (r&1) | (r&2)<<2 | (r&4).  Panel p
+//   occupies group p / PPG, columns (p % PPG)*PW + [0, IB).  This XOR swizzle
+//   makes both DMMA B-fragment patterns conflict free: step A reads
+//   (row 8rb+2t+j, col 8nb+g), step C reads (row 8rb+g, col 8nb+2t+s).
+//   GEQRT tiles store the unit lower trapezoid V (explicit 0 / 1).
+//   T: after V, panel p at TOFF + p*IB*LDT2, T_p(l, i) at l*LDT2 + i
+//   (LDT2 == 2 mod 16: conflict free for step B's (l = 8kb+2t+s, i = 8nb+g)).
+#pragma once
+
+#include <stdint.h>
+
+#include "dmma.cuh"
+#include "internal.h"
+
+namespace tileqr {
+namespace v2 {
+
+template <int NB, int IB>
+struct Pk {
+  static constexpr int GW = IB <= 16 ? 16 : 32;           // group width
+  static constexpr int PW = IB == 8 ? 8 : GW;             // packed panel width
+  static constexpr int PPG = GW / PW;                     // panels per group
+  static constexpr int NP = NB / IB;                      // panels
+  static constexpr int NG = (NP + PPG - 1) / PPG;         // groups
+  static constexpr int LDT2 = IB <= 16 ? 18 : 34;
+  static constexpr int GDBL = NB * GW;                    // doubles per V group
+  static constexpr int TOFF = NG * GDBL;
+  static constexpr int TP = IB * LDT2;                    // doubles per T_p
+  static constexpr int TOTAL = TOFF + NP * TP;            // doubles per packed tile
+  static constexpr int NBK = IB / 8;
+  static_assert(IB % 8 == 0 && IB <= 32 && NB % IB == 0, "packed tile geometry");
+};
+
+__host__ __device__ constexpr int pk_f(int r) { return (r & 1) | ((r & 2) << 2) | (r & 4); }
+
+// packed-tile size in doubles for a runtime (NB, IB) (0 if unsupported)
+inline size_t pk_doubles(int NB, int IB) {
+  if (IB % 8 || IB > 32 || NB % IB) return 0;
+  const int GW = IB <= 16 ? 16 : 32, PW = IB == 8 ? 8 : GW, PPG = GW / PW, NP = NB / IB;
+  const int NG = (NP + PPG - 1) / PPG, LDT2 = IB <= 16 ? 18 : 34;
+  return (size_t)NG * NB * GW + (size_t)NP * IB * LDT2;
+}
+
+// ---- mbarrier / bulk-copy helpers -------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "TQ_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra TQ_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy accesses before / async-proxy (TMA) accesses after
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// One thread: (re)arm the NG group barriers and issue the bulk copies of a
+// packed tile (each group: its V block + the T_p of its panels).  The caller
+// orders this before the other threads' waits (CTA barrier).
+template <int NB, int IB>
+__device__ __forceinline__ void issue_packed_loads(const double* __restrict__ gpk, double* spk, uint64_t* bars) {
+  using P = Pk<NB, IB>;
+  fence_proxy_async();
+  for (int q = 0; q < P::NG; ++q) mbar_init(&bars[q], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (int q = 0; q < P::NG; ++q) {
+    const int p0 = q * P::PPG;
+    const int np = (P::NP - p0) < P::PPG ? (P::NP - p0) : P::PPG;
+    const uint32_t vb = P::GDBL * 8, tb = np * P::TP * 8;
+    mbar_expect_tx(&bars[q], vb + tb);
+    bulk_g2s(spk + q * P::GDBL, gpk + q * P::GDBL, vb, &bars[q]);
+    bulk_g2s(spk + P::TOFF + p0 * P::TP, gpk + P::TOFF + p0 * P::TP, tb, &bars[q]);
+  }
+}
+
+// All threads of a CTA (kThreads): write panel p of the packed tile from
+// accessor callbacks v(r, i) (reflector matrix V_p, row r < NB, column i < IB,
+// unit / zero entries included) and t(l, i) (T_p, upper triangle).
+template <int NB, int IB, int kThreads, class VF, class TF>
+__device__ __forceinline__ void pack_panel(double* __restrict__ gpk, int p, VF v, TF t) {
+  using P = Pk<NB, IB>;
+  const int q = p / P::PPG, cb = (p % P::PPG) * P::PW;
+  double* gv = gpk + q * P::GDBL;
+  // each packed row of the group holds PW (of GW) columns of this panel; for
+  // PPG == 1 write the whole row (padding columns of IB = 24 as 0)
+  constexpr int WC = P::PPG == 1 ? P::GW : P::PW;
+  for (int e = threadIdx.x; e < NB * WC; e += kThreads) {
+    const int r = e / WC, x = e - r * WC;
+    int pos, i;
+    if (P::PPG == 1) {
+      pos = x;
+      i = x ^ pk_f(r & 7);
+    } else {
+      i = x;
+      pos = (cb + x) ^ pk_f(r & 7);
+    }
+    gv[r * P::GW + pos] = (i < IB) ? v(r, i) : 0.0;
+  }
+  double* gt = gpk + P::TOFF + p * P::TP;
+  for (int e = threadIdx.x; e < IB * P::LDT2; e += kThreads) {
+    const int l = e / P::LDT2, i = e - l * P::LDT2;
+    gt[e] = (i < IB && l <= i) ? t(l, i) : 0.0;
+  }
+}
+
+// ---- the update body ---------------------------------------------------------
+// Columns [col0, col0 + W*8*MB) of one task; spk = the smem packed tile whose
+// group barriers `bars` were armed by issue_packed_loads (parity `par`).
+template <int NB, int IB, int MB, bool LARFB, int W>
+__device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, uint64_t* bars, uint32_t par,
+                                               double* __restrict__ C1, double* __restrict__ C2, int col0) {
+  using P = Pk<NB, IB>;
+  constexpr int RB = NB / 8;
+  constexpr int NBK = P::NBK;
+  constexpr bool SPLIT = NBK * MB < 4;  // two partial sums per step-A block when chains are few
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = lane & 3, g = lane >> 2;
+  const int wc0 = col0 + warp * 8 * MB;  // first column of this warp
+  if (wc0 >= NB) return;                 // idle warp (8*MB*W > NB): no CTA barrier follows
+
+  // ---- C2 slab -> registers: acc[mb][rb][j] = C2(8rb+2t+j, wc0+8mb+g) --------
+  double acc[MB][RB][2];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    const double* src = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {
+      const double2 v = *reinterpret_cast<const double2*>(src + 8 * rb);
+      acc[mb][rb][0] = v.x;
+      acc[mb][rb][1] = v.y;
+    }
+  }
+  // C1 rows of panel 0 (SSRFB): c1n[mb][nb][j] = C1(c0 + 8nb+2t+j, col)
+  double c1n[MB][NBK][2];
+  if (!LARFB) {
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NBK; ++nb) {
+        const double2 v = *reinterpret_cast<const double2*>(C1 + 8 * nb + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB);
+        c1n[mb][nb][0] = v.x;
+        c1n[mb][nb][1] = v.y;
+      }
+  }
+
+#pragma unroll 1
+  for (int p = 0; p < P::NP; ++p) {
+    const int c0 = p * IB;
+    const int q = p / P::PPG, cb = (p % P::PPG) * P::PW;
+    if (p % P::PPG == 0) mbar_wait(&bars[q], par);
+    const double* Vq = spk + q * P::GDBL;
+    const double* Tp = spk + P::TOFF + p * P::TP;
+
+    // ---- step A: W^T = C1p^T + C2^T V_p ----------------------------------------
+    double w[MB][NBK][2], w2[MB][NBK][2];
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NBK; ++nb)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          w[mb][nb][j] = LARFB ? 0.0 : c1n[mb][nb][j];
+          w2[mb][nb][j] = 0.0;
+        }
+    if (!LARFB && p + 1 < P::NP) {  // prefetch the C1 rows of panel p+1
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          const double2 v = *reinterpret_cast<const double2*>(C1 + c0 + IB + 8 * nb + 2 * t +
+                                                             (size_t)(wc0 + 8 * mb + g) * NB);
+          c1n[mb][nb][0] = v.x;
+          c1n[mb][nb][1] = v.y;
+        }
+    }
+    // B fragment (row 8rb+2t+j, col cb+8nb+g): per-thread base per (j, nb), the
+    // row block rb is a compile-time offset
+    const int rb0 = LARFB ? (c0 >> 3) : 0;  // V_p is zero above row c0
+    const double* pa[2][NBK];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int nb = 0; nb < NBK; ++nb) pa[j][nb] = Vq + (2 * t + j) * P::GW + ((cb + 8 * nb + g) ^ pk_f(2 * t + j));
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {
+      if (rb < rb0) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          const double bf = pa[j][nb][8 * rb * P::GW];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) {
+            if (SPLIT && j == 1) dmma(w2[mb][nb][0], w2[mb][nb][1], acc[mb][rb][1], bf);
+            else dmma(w[mb][nb][0], w[mb][nb][1], acc[mb][rb][j], bf);
+          }
+        }
+    }
+    if (SPLIT) {
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          w[mb][nb][0] += w2[mb][nb][0];
+          w[mb][nb][1] += w2[mb][nb][1];
+        }
+    }
+
+    // ---- step B: W'^T(:, i) = sum_{l <= i} W^T(:, l) T_p(l, i), in place ---------
+#pragma unroll
+    for (int nb = NBK - 1; nb >= 0; --nb) {
+      double o[MB][2];
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) o[mb][0] = o[mb][1] = 0.0;
+#pragma unroll
+      for (int kb = 0; kb <= nb; ++kb)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const double bf = Tp[(8 * kb + 2 * t + s) * P::LDT2 + 8 * nb + g];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) dmma(o[mb][0], o[mb][1], w[mb][kb][s], bf);
+        }
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) {
+        w[mb][nb][0] = o[mb][0];
+        w[mb][nb][1] = o[mb][1];
+      }
+    }
+
+    // ---- C1[p rows] -= W' (re-read C1: an L1/L2 hit) --------------------------
+    if (!LARFB) {
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb) {
+          double* dst = C1 + c0 + 8 * nb + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
+          const double2 v = *reinterpret_cast<const double2*>(dst);
+          *reinterpret_cast<double2*>(dst) = make_double2(v.x - w[mb][nb][0], v.y - w[mb][nb][1]);
+        }
+    }
+
+    // ---- step C: C2^T(:, r) -= sum_i W'^T(:, i) V_p(r, i) -----------------------
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < NBK; ++nb) {
+        w[mb][nb][0] = -w[mb][nb][0];
+        w[mb][nb][1] = -w[mb][nb][1];
+      }
+    const int fg = pk_f(g);
+#pragma unroll
+    for (int nb = 0; nb < NBK; ++nb)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const double* pc = Vq + g * P::GW + ((cb + 8 * nb + 2 * t + s) ^ fg);
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          if (rb < rb0) continue;
+          const double bf = pc[8 * rb * P::GW];
+#pragma unroll
+          for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], w[mb][nb][s], bf);
+        }
+      }
+  }
+
+  // ---- registers -> C2 ----------------------------------------------------------
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    double* dst = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb)
+      *reinterpret_cast<double2*>(dst + 8 * rb) = make_double2(acc[mb][rb][0], acc[mb][rb][1]);
+  }
+}
+
+// ---- batched kernels -----------------------------------------------------------
+constexpr int kWarpsB = 8;  // warps per CTA of the batched v2 kernels (same geometry as the DAG kernel)
+
+__host__ __device__ constexpr int v2_mb(int NB) { return (NB == 96 || NB == 128) ? 2 : 1; }
+
+template <int NB, int IB>
+constexpr size_t v2_smem_bytes() { return (size_t)Pk<NB, IB>::TOTAL * sizeof(double); }
+
+// grid (slabs, batch): task b, columns [blockIdx.x * 64*MB, ...)
+template <int NB, int IB, bool LARFB>
+__global__ void __launch_bounds__(kWarpsB * 32, 1)
+update_v2_kernel(const double* const* Pkp, double* const* C1p, double* const* C2p) {
+  constexpr int MB = v2_mb(NB);
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bars[Pk<NB, IB>::NG];
+  const int b = blockIdx.y;
+  if (threadIdx.x == 0) issue_packed_loads<NB, IB>(Pkp[b], smem, bars);
+  __syncthreads();
+  update_v2_body<NB, IB, MB, LARFB, kWarpsB>(smem, bars, 0, LARFB ? nullptr : C1p[b], C2p[b],
+                                             blockIdx.x * kWarpsB * 8 * MB);
+}
+
+// grid (batch): standard V (NB x NB, GEQRT form if LARFB: unit lower
+// trapezoid implied) and T (IB x NB) -> packed tile (the layout transform the
+// panel kernels apply when they write the packed copy themselves)
+template <int NB, int IB, bool LARFB>
+__global__ void __launch_bounds__(256)
+pack_kernel(const double* const* Vp, const double* const* Tp, double* const* Pkp) {
+  const double* V = Vp[blockIdx.x];
+  const double* T = Tp[blockIdx.x];
+  double* pk = Pkp[blockIdx.x];
+  for (int p = 0; p < NB / IB; ++p) {
+    const int c0 = p * IB;
+    pack_panel<NB, IB, 256>(
+        pk, p,
+        [&](int r, int i) {
+          const int col = c0 + i;
+          if (LARFB) return r > col ? V[r + (size_t)col * NB] : (r == col ? 1.0 : 0.0);
+          return V[r + (size_t)col * NB];
+        },
+        [&](int l, int i) { return T[l + (size_t)(c0 + i) * IB]; });
+  }
+}
+
+template <int NB, int IB, bool LARFB>
+int launch_update_v2_t(int batch, const double* const* Pk_, double* const* C1, double* const* C2,
+                       cudaStream_t s) {
+  auto kern = update_v2_kernel<NB, IB, LARFB>;
+  const size_t bytes = v2_smem_bytes<NB, IB>();
+  static_assert(v2_smem_bytes<NB, IB>() <= 227 * 1024, "packed tile exceeds shared memory");
+  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  constexpr int cols = kWarpsB * 8 * v2_mb(NB);
+  dim3 grid((NB + cols - 1) / cols, batch);
+  kern<<<grid, kWarpsB * 32, bytes, s>>>(Pk_, C1, C2);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int NB>
+int launch_update_v2(bool larfb, int IB, int batch, const double* const* Pk_, double* const* C1,
+                     double* const* C2, cudaStream_t s) {
+  if (batch <= 0) return 0;
+#define TQ_V2(ib)                                                                              \
+  case ib:                                                                                     \
+    return larfb ? launch_update_v2_t<NB, ib, true>(batch, Pk_, C1, C2, s)                     \
+                 : launch_update_v2_t<NB, ib, false>(batch, Pk_, C1, C2, s);
+  switch (IB) {
+    TQ_V2(8) TQ_V2(16) TQ_V2(32)
+    case 24:
+      if constexpr (NB % 24 == 0)
+        return larfb ? launch_update_v2_t<NB, 24, true>(batch, Pk_, C1, C2, s)
+                     : launch_update_v2_t<NB, 24, false>(batch, Pk_, C1, C2, s);
+      [[fallthrough]];
+    default:
+      set_error("update_v2: unsupported IB");
+      return TILEQR_ERR_CUDA;
+  }
+#undef TQ_V2
+}
+
+template <int NB>
+int launch_pack(bool larfb, int IB, int batch, const double* const* V, const double* const* T,
+                double* const* Pk_, cudaStream_t s) {
+  if (batch <= 0) return 0;
+#define TQ_PK(ib)                                                                             \
+  case ib:                                                                                    \
+    if (larfb) pack_kernel<NB, ib, true><<<batch, 256, 0, s>>>(V, T, Pk_);                    \
+    else pack_kernel<NB, ib, false><<<batch, 256, 0, s>>>(V, T, Pk_);                         \
+    break;
+  switch (IB) {
+    TQ_PK(8) TQ_PK(16) TQ_PK(32)
+    case 24:
+      if constexpr (NB % 24 == 0) {
+        if (larfb) pack_kernel<NB, 24, true><<<batch, 256, 0, s>>>(V, T, Pk_);
+        else pack_kernel<NB, 24, false><<<batch, 256, 0, s>>>(V, T, Pk_);
+        break;
+      }
+      [[fallthrough]];
+    default:
+      set_error("pack: unsupported IB");
+      return TILEQR_ERR_CUDA;
+  }
+#undef TQ_PK
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace v2
+}  // namespace tileqr

@@ -41,6 +41,9 @@ _SIGS = {
     "tileqr_tsqrt_batched": ([_i, _i, _i, _p, _p, _p, _p], _i),
     "tileqr_larfb_batched": ([_c, _i, _i, _i, _p, _p, _p, _i, _p], _i),
     "tileqr_ssrfb_batched": ([_c, _i, _i, _i, _p, _p, _p, _p, _i, _p], _i),
+    "tileqr_packed_size": ([_i, _i, ctypes.POINTER(_sz)], _i),
+    "tileqr_pack_batched": ([_i, _i, _i, _i, _p, _p, _p, _p], _i),
+    "tileqr_update_packed_batched": ([_i, _i, _i, _i, _p, _p, _p, _p], _i),
     "tileqr_tune": ([_i64, _i64, _i, _i, _i, _PI, _PI, ctypes.c_char_p], _i),
     "tileqr_preselect": ([_i, _PI, _PI, _PD, _i, _i, _PI, _PI, _PD, _PI], _i),
     "tileqr_payg_prune": ([_i, _PI, _PD, _PI], _i),
@@ -57,6 +60,8 @@ _SIGS = {
     "tileqr_factor_plan": ([_i64, _i64, _i, _i, ctypes.POINTER(_i64)], _i),
     "tileqr_set_kernel_timing": ([_i], None),
     "tileqr_kernel_times": ([_i64, _i64, _i, _i, _i, _PD, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
+    "tileqr_kernel_trace": ([_i64, _i64, _i, _i, _i64, _PD, _PD, _PI, ctypes.POINTER(_i64),
+                             ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
     "tileqr_finalize": ([], None),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -187,6 +192,24 @@ def ssrfb_batched(trans: str, nb: int, ib: int, V2_ptrs, T_ptrs, C1_ptrs, C2_ptr
                                      ncols, _stream(stream)), "tileqr_ssrfb_batched")
 
 
+def packed_size(nb: int, ib: int) -> int:
+    out = _sz()
+    _check(_lib.tileqr_packed_size(nb, ib, ctypes.byref(out)), "tileqr_packed_size")
+    return out.value
+
+
+def pack_batched(larfb: bool, nb: int, ib: int, V_ptrs, T_ptrs, Pk_ptrs, stream=None):
+    _check(_lib.tileqr_pack_batched(int(larfb), nb, ib, V_ptrs.numel(), V_ptrs.data_ptr(), T_ptrs.data_ptr(),
+                                    Pk_ptrs.data_ptr(), _stream(stream)), "tileqr_pack_batched")
+
+
+def update_packed_batched(larfb: bool, nb: int, ib: int, Pk_ptrs, C1_ptrs, C2_ptrs, stream=None):
+    _check(_lib.tileqr_update_packed_batched(int(larfb), nb, ib, Pk_ptrs.numel(), Pk_ptrs.data_ptr(),
+                                             C1_ptrs.data_ptr() if C1_ptrs is not None else None,
+                                             C2_ptrs.data_ptr(), _stream(stream)),
+           "tileqr_update_packed_batched")
+
+
 def rng_uniform(A: torch.Tensor, m: int, n: int, seed: int, offset: int = 0, lda: int | None = None,
                 stream=None):
     _check(_lib.tileqr_rng_uniform(m, n, A.data_ptr(), lda if lda is not None else max(1, m), seed,
@@ -233,7 +256,7 @@ def factor_plan(m: int, n: int, nb: int, ib: int) -> dict:
     return dict(zip(keys, list(out)))
 
 
-KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3}
+KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3, "dag": 4}
 
 
 def set_kernel_timing(on, kinds=("geqrt", "tsqrt", "larfb", "ssrfb")):
@@ -248,6 +271,20 @@ def kernel_times(m: int, n: int, nb: int, ib: int, kind: str):
     _check(_lib.tileqr_kernel_times(m, n, nb, ib, KINDS[kind], ctypes.byref(tot), ctypes.byref(nl),
                                     ctypes.byref(nt)), "tileqr_kernel_times")
     return tot.value, nl.value, nt.value
+
+
+def kernel_trace(m: int, n: int, nb: int, ib: int, max_recs: int = 1 << 16):
+    """Per-launch records of the last timed factor: list of (t0_ms, t1_ms, kind, level, tasks)."""
+    t0 = (ctypes.c_double * max_recs)()
+    t1 = (ctypes.c_double * max_recs)()
+    kd = (ctypes.c_int * max_recs)()
+    lv = (ctypes.c_int64 * max_recs)()
+    nt = (ctypes.c_int64 * max_recs)()
+    cnt = _i64()
+    _check(_lib.tileqr_kernel_trace(m, n, nb, ib, max_recs, t0, t1, kd, lv, nt, ctypes.byref(cnt)),
+           "tileqr_kernel_trace")
+    names = {v: k for k, v in KINDS.items()}
+    return [(t0[i], t1[i], names[kd[i]], lv[i], nt[i]) for i in range(min(cnt.value, max_recs))]
 
 
 def finalize():

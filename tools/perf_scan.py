@@ -70,6 +70,32 @@ def time_ssrfb(nb, ib, batch=4096, reps=20):
             "tflops_executed": round(batch * (4 * nb ** 3 + ib * nb * nb) / (ms * 1e-3) / 1e12, 2)}
 
 
+def time_ssrfb_packed(nb, ib, batch=4096, reps=20):
+    """The factorization's kernel alone: packed reflector tiles prepared once."""
+    tile = nb * nb
+    pk = tq.packed_size(nb, ib)
+    buf = torch.empty(batch * 5 * tile, dtype=torch.float64, device="cuda")
+    tq.rng_uniform(buf, tile, batch * 5, seed=2)
+    pbuf = torch.empty(batch * pk, dtype=torch.float64, device="cuda")
+    base = buf.data_ptr()
+    idx = torch.arange(batch, dtype=torch.int64, device="cuda") * 5 * tile * 8 + base
+    R, V, C1, C2, T = (idx + j * tile * 8 for j in range(5))
+    P = torch.arange(batch, dtype=torch.int64, device="cuda") * pk * 8 + pbuf.data_ptr()
+    tq.tsqrt_batched(nb, ib, R, V, T)
+    tq.pack_batched(False, nb, ib, V, T, P)
+    tq.update_packed_batched(False, nb, ib, P, C1, C2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        tq.update_packed_batched(False, nb, ib, P, C1, C2)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"kernel": "packed", "nb": nb, "ib": ib, "batch": batch, "ms": round(ms, 3),
+            "tflops_nominal": round(batch * 4 * nb ** 3 / (ms * 1e-3) / 1e12, 2)}
+
+
 def time_panel(nb, ib, batch=1, reps=50, kind="tsqrt"):
     tile = nb * nb
     buf = torch.empty(batch * 3 * tile, dtype=torch.float64, device="cuda")
@@ -108,7 +134,11 @@ def main():
                 print(json.dumps(time_panel(nb, ib, kind=kind)), flush=True)
     if a.ssrfb:
         for nb, ib in pairs:
+            if tq.packed_size(nb, ib):
+                print(json.dumps(time_ssrfb_packed(nb, ib)), flush=True)
+            os.environ["TILEQR_NO_V2"] = "1"
             print(json.dumps(time_ssrfb(nb, ib)), flush=True)
+            os.environ.pop("TILEQR_NO_V2")
     for n in a.n:
         for nb, ib in pairs:
             print(json.dumps(time_factor(n, nb, ib, timing=a.timing)), flush=True)
