@@ -173,6 +173,88 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _traffic(key, nb, ib):
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        return json.load(open(prof)).get(key, {}).get(f"{nb}:{ib}")
+    return None
+
+
+def measure_dag(tq, m, n, nb, ib, step, step_ms):
+    """Roofline of the persistent dataflow kernel (the one launch that runs the
+    whole DAG): algorithmic flops = the factorization's useful flops
+     per launch / the kernel's duration (CUDA events around
+    the launch on its stream), in one measurement step after the timed region.
+    Per-kind item busy times come from the device clock (globaltimer) in the
+    same step."""
+    tq.set_kernel_timing(True)
+    step()
+    import torch
+    torch.cuda.synchronize()
+    dag_ms = tq.kernel_times(m, n, nb, ib, "dag")[0]
+    kinds = {"note": "dataflow kernel: per kind, items, busy ms summed over CTAs (inputs ready -> done), "
+                     "one step after the timed region"}
+    busy = {}
+    for k in ("geqrt", "tsqrt", "larfb", "ssrfb"):
+        tk, lk, nk = tq.kernel_times(m, n, nb, ib, k)
+        busy[k] = tk
+        kinds[k] = {"busy_ms_sum": round(tk, 3), "items": lk, "tasks": nk}
+    tq.set_kernel_timing(False)
+    nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    s_tasks = kinds["ssrfb"]["tasks"]
+    kinds["ssrfb"]["tflops_while_running"] = round(
+        s_tasks * 4.0 * nb ** 3 / (busy["ssrfb"] * 1e-3 / nsm) / 1e12, 3) if busy["ssrfb"] else None
+    kinds["sm_busy_frac"] = round(sum(busy.values()) / (nsm * dag_ms), 4) if dag_ms else None
+    flops = qr_flops(m, n)
+    achieved = flops / (dag_ms * 1e-3) / 1e12 if dag_ms > 0 else 0.0
+    roofline = {"kernel": "dag_kernel (persistent dataflow: GEQRT/TSQRT/LARFB/SSRFB items)",
+                "bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": _traffic("dag", nb, ib),
+                "flops_per_launch": flops, "avg_launch_ms": round(dag_ms, 4),
+                "peak_source": FP64_PEAK_SRC, "share_of_step": round(dag_ms / step_ms, 4),
+                "measured": "CUDA events around the single dag_kernel launch (on the caller's stream) in the "
+                            "step right after the timed region; flops = useful 4/3 N^3 (2MN^2-2N^3/3); "
+                            "traffic = ncu dram read+write bytes of one launch (profiles/ncu_traffic.json)"}
+    return roofline, kinds
+
+
+def measure_levels(tq, m, n, nb, ib, step, step_ms):
+    """Roofline of the SSRFB launches of the level-synchronous schedule."""
+    import torch
+    # SSRFB launch durations: CUDA events (event-record nodes in the captured graph,
+    # on the update stream the kernels run on) in one measurement step right after
+    # the timed region -- the nodes cost ~5% of a step, so the timed region has none
+    tq.set_kernel_timing(True, kinds=("ssrfb",))
+    step()
+    torch.cuda.synchronize()
+    tot, nl, nt = tq.kernel_times(m, n, nb, ib, "ssrfb")
+    s = {"ms": round(tot, 3), "launches": nl, "tasks": nt}
+    # per-kind breakdown from one more step with events around every launch
+    tq.set_kernel_timing(True)
+    step()
+    torch.cuda.synchronize()
+    kinds = {"note": "one extra step after the timed region, events around every launch"}
+    for k in ("geqrt", "tsqrt", "larfb", "ssrfb"):
+        tk, lk, nk = tq.kernel_times(m, n, nb, ib, k)
+        kinds[k] = {"ms": round(tk, 3), "launches": lk, "tasks": nk}
+    tq.set_kernel_timing(False)
+    ssrfb_flops = s["tasks"] * 4.0 * nb ** 3          # SURVEY §8(d): useful 4 NB^3 per pair
+    achieved = ssrfb_flops / (s["ms"] * 1e-3) / 1e12 if s["ms"] > 0 else 0.0
+    per_task = _traffic("ssrfb_per_task", nb, ib)
+    traffic = per_task * s["tasks"] / s["launches"] if (per_task and s["launches"]) else None
+    roofline = {"kernel": "ssrfb (update kernel)", "bound": "tensor",
+                "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
+                "flops_per_launch": ssrfb_flops / max(1, s["launches"]),
+                "avg_launch_ms": round(s["ms"] / max(1, s["launches"]), 4),
+                "peak_source": FP64_PEAK_SRC,
+                "share_of_step": round(s["ms"] / step_ms, 4),
+                "measured": "CUDA events around each SSRFB launch (graph event-record nodes on the update "
+                            "stream) in the step right after the timed region; traffic = ncu dram bytes per "
+                            "task (profiles/ncu_traffic.json) x this run's tasks per launch"}
+    return roofline, kinds
+
+
 def run_tileqr(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -222,42 +304,11 @@ def run_tileqr(args, rank, world, local_rank):
     flops = qr_flops(m, n)
     value = flops / (ms * 1e-3) / 1e9
 
-    # SSRFB launch durations: CUDA events (event-record nodes in the captured graph,
-    # on the update stream the kernels run on) in one measurement step right after
-    # the timed region -- the nodes cost ~5% of a step, so the timed region has none
-    tq.set_kernel_timing(True, kinds=("ssrfb",))
-    step()
-    torch.cuda.synchronize()
-    tot, nl, nt = tq.kernel_times(m, n, nb, ib, "ssrfb")
-    s = {"ms": round(tot, 3), "launches": nl, "tasks": nt}
-    # per-kind breakdown from one more step with events around every launch
-    tq.set_kernel_timing(True)
-    step()
-    torch.cuda.synchronize()
-    kinds = {"note": "one extra step after the timed region, events around every launch"}
-    for k in ("geqrt", "tsqrt", "larfb", "ssrfb"):
-        tk, lk, nk = tq.kernel_times(m, n, nb, ib, k)
-        kinds[k] = {"ms": round(tk, 3), "launches": lk, "tasks": nk}
-    tq.set_kernel_timing(False)
-    ssrfb_flops = s["tasks"] * 4.0 * nb ** 3          # useful 4 NB^3 per pair
-    achieved = ssrfb_flops / (s["ms"] * 1e-3) / 1e12 if s["ms"] > 0 else 0.0
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_ssrfb_traffic.json")
-    if os.path.exists(prof):
-        p = json.load(open(prof))
-        key = f"{nb}:{ib}"
-        if key in p.get("per_task_bytes", {}) and s["launches"]:
-            traffic = p["per_task_bytes"][key] * s["tasks"] / s["launches"]
-    roofline = {"kernel": "ssrfb (dmma_update_kernel)", "bound": "tensor",
-                "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
-                "flops_per_launch": ssrfb_flops / max(1, s["launches"]),
-                "avg_launch_ms": round(s["ms"] / max(1, s["launches"]), 4),
-                "peak_source": FP64_PEAK_SRC,
-                "share_of_step": round(s["ms"] / ms, 4),
-                "measured": "CUDA events around each SSRFB launch (graph event-record nodes on the update "
-                            "stream) in the step right after the timed region; traffic = ncu dram bytes per "
-                            "task (profiles/ncu_ssrfb_traffic.json) x this run's tasks per launch"}
+    sched = tq.factor_schedule(nb, ib)
+    if sched == "dag":
+        roofline, kinds = measure_dag(tq, m, n, nb, ib, step, ms)
+    else:
+        roofline, kinds = measure_levels(tq, m, n, nb, ib, step, ms)
 
     # e2e: same metric through the public API with host buffers (pinned), H2D of
     # the input and D2H of the result (R/V and T) inside the timed region
@@ -297,7 +348,7 @@ def run_tileqr(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic: i.i.d. uniform(-0.5,0.5), splitmix64 counter generator, seed {seed}",
             "config": {"workload": wl["name"], "M": m, "N": n, "NB": nb, "IB": ib, "nb_ib_source": src,
-                       "parallelism": "single GPU", "levels": plan["levels"],
+                       "parallelism": "single GPU", "levels": plan["levels"], "schedule": sched,
                        "l2": f"input {m * n * 8 / 1e6:.0f} MB > 126 MB L2; A restored from a pristine "
                              "device copy at the start of every step (inside the timed region)"},
             "pct_fp64_peak": round(100 * value / (FP64_PEAK_TFLOPS * 1e3), 2),

@@ -236,6 +236,11 @@ const char* tileqr_ssrfb_impl(int NB, int IB);
 
 /* Static plan of tileqr_factor(M, N, NB, IB): h_out[8] = {levels, kernel
  * launches per call, #GEQRT, #TSQRT, #LARFB, #SSRFB tasks, MT, NT}. */
+/* How tileqr_factor executes the DAG for this (NB, IB): "dag" = one
+ * persistent dataflow kernel (NB % 32 == 0, NB <= 256, IB in {8,16,24,32};
+ * environment TILEQR_SCHED=levels forces the other), "levels" = one batched
+ * launch per kernel kind and DAG level, captured in a CUDA graph. */
+const char* tileqr_factor_schedule(int NB, int IB);
 int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out);
 
 /* Kernel timing for measurement (bench.py): bit k of `mask` (k = 0 GEQRT,
@@ -252,7 +257,10 @@ int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* 
 /* Launch trace of the most recent timed tileqr_factor(M, N, NB, IB): for
  * up to max_recs timed launches, start/end in ms relative to the first timed
  * launch's start event, kernel kind, DAG level and task count (host arrays,
- * each nullable except h_count, which receives the number of records). */
+ * each nullable except h_count, which receives the number of records).
+ * Dataflow schedule ("dag"): one record per work item in claim order, start
+ * = inputs ready, end = completion published (device ns clock, relative to
+ * the first claim), h_tasks = the item's claim time in ns. */
 int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, double* h_t0_ms,
                         double* h_t1_ms, int* h_kind, int64_t* h_level, int64_t* h_tasks,
                         int64_t* h_count);

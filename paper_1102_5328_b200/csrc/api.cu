@@ -948,6 +948,11 @@ const char* tileqr_ssrfb_impl(int NB, int IB) { return ssrfb_impl_name(NB, IB); 
 // Diagnostic (not in the header): accumulated phase cycles of the fast panel kernel.
 int tileqr_debug_panel_prof(unsigned long long* out, int reset) { return tileqr::panel_prof_read(out, reset); }
 
+const char* tileqr_factor_schedule(int NB, int IB) {
+  if (!valid_nb_ib(NB, IB)) return "invalid";
+  return dag_enabled(NB, IB) ? "dag" : "levels";
+}
+
 int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out) {
   static const char* fn = "tileqr_factor_plan";
   if (M < 0) return arg_error(1, fn, "M < 0");
@@ -971,6 +976,7 @@ int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out) {
     else
       launches += (c[0] > 0) + (c[1] > 0) + (c[2] > 0) + (c[3] > 0);
   }
+  if (dag_enabled(NB, IB)) launches = nlev > 0 ? 1 : 0;  // one persistent dataflow kernel
   h_out[0] = nlev;
   h_out[1] = launches + ((M == 0 || N == 0) ? 0 : 3);  // + zero-info, layout in, layout out
   for (int q = 0; q < 4; ++q) h_out[2 + q] = cnt[q];
@@ -1077,7 +1083,7 @@ int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, 
       if (h_t1_ms) h_t1_ms[i] = (double)(pr[3 * i + 2] - t0) * 1e-6;
       if (h_kind) h_kind[i] = ws->item_kind[i];
       if (h_level) h_level[i] = ws->item_level[i];
-      if (h_tasks) h_tasks[i] = 1;
+      if (h_tasks) h_tasks[i] = (int64_t)(pr[3 * i] - t0);  // DAG: claim time (ns from origin)
     }
     return 0;
   }

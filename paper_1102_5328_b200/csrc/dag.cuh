@@ -60,39 +60,84 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// 16-byte async copy global -> shared (L2 only), for the item descriptors
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc)
+               : "memory");
+}
+
 // prof (nullable, diagnostics): per item i, prof[3i .. 3i+2] = claim time,
 // start time (inputs ready), end time in globaltimer ns.
+//
+// Claims overlap the tail of the running item: during the second-to-last
+// inner panel of an update item thread 0 claims the next item (atomicAdd),
+// during the last one its descriptor is copied into the other smem slot, so
+// at the end only the dependency check remains.  A claimed item is held for
+// about two inner panels.  Items are claimed in list order and a CTA's held
+// item always follows its running one, so the smallest unfinished item is
+// always running or about to (no deadlock).
 template <int NB, int KW>
 __global__ void __launch_bounds__(kThreads, 1)
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
            unsigned long long* prof) {
   constexpr int MB = dag_mb(NB);
+  static_assert(sizeof(Item) % 16 == 0, "Item is copied in 16-byte chunks");
   extern __shared__ __align__(128) double smem[];
-  __shared__ int s_item;
+  __shared__ __align__(16) Item s_desc[2];
+  __shared__ int s_cur;
   __shared__ __align__(8) uint64_t bars[8];
   constexpr bool V2 = dag_v2<NB>();
+  int nxt = -1;   // thread 0: item claimed ahead (-1: none)
+  int slot = 0;   // descriptor slot of the running item (all threads)
+  auto fetch_desc = [&](int i, int sl) {
+    if (prof) prof[3 * (size_t)i] = globaltimer();
+    for (int c = 0; c < (int)(sizeof(Item) / 16); ++c)
+      cp_async16(reinterpret_cast<char*>(&s_desc[sl]) + 16 * c, reinterpret_cast<const char*>(items + i) + 16 * c);
+    cp_async_commit();
+  };
   for (;;) {
     if (threadIdx.x == 0) {
-      const int i = atomicAdd(next, 1);
-      s_item = i;
-      if (i < nitems) {
-        if (prof) prof[3 * (size_t)i] = globaltimer();
-        const Item& it = items[i];
-        for (int d = 0; d < it.ndep; ++d) {
-          const int* c = done + it.dep[d];
-          const int need = it.need[d];
-          while (ld_acquire(c) < need) __nanosleep(64);
+      int cur = nxt;
+      if (cur < 0) {
+        cur = atomicAdd(next, 1);
+        if (cur < nitems) fetch_desc(cur, slot);
+      }
+      nxt = -1;
+      s_cur = cur;
+      if (cur < nitems) {
+        cp_async_wait<0>();
+        const Item& it = s_desc[slot];
+        int need[3], got[3];
+        const int nd = it.ndep;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {  // all flags in flight at once
+          need[d] = d < nd ? it.need[d] : 0;
+          got[d] = d < nd ? ld_acquire(done + it.dep[d]) : 0;
         }
-        if (prof) prof[3 * (size_t)i + 1] = globaltimer();
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          while (got[d] < need[d]) {
+            __nanosleep(64);
+            got[d] = ld_acquire(done + it.dep[d]);
+          }
+        if (prof) prof[3 * (size_t)cur + 1] = globaltimer();
         if constexpr (V2) {
           if (it.kind == kLarfb || it.kind == kSsrfb) v2::issue_packed_loads<NB, KW>(it.pk, smem, bars);
         }
       }
     }
     __syncthreads();
-    const int i = s_item;
-    if (i >= nitems) return;
-    const Item it = items[i];
+    if (s_cur >= nitems) return;
+    const int i = s_cur;
+    const Item it = s_desc[slot];
+    // claim-ahead hook of the update bodies (thread 0)
+    constexpr int NPAN = NB / KW;
+    auto hook = [&](int p) {
+      if (threadIdx.x != 0) return;
+      if (p == (NPAN >= 2 ? NPAN - 2 : 0)) nxt = atomicAdd(next, 1);
+      if (p == NPAN - 1 && nxt < nitems) fetch_desc(nxt, slot ^ 1);
+    };
     switch (it.kind) {
       case kGeqrt:
         pf::panel_fast_body<false, NB, kWarps>(IB, it.p[0], nullptr, it.p[2],
@@ -103,12 +148,14 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
                                               reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr);
         break;
       case kLarfb:
-        if constexpr (V2) v2::update_v2_body<NB, KW, MB, true, kWarps>(smem, bars, 0, nullptr, it.p[2], it.col0);
+        if constexpr (V2)
+          v2::update_v2_body<NB, KW, MB, true, kWarps>(smem, bars, 0, nullptr, it.p[2], it.col0, hook);
         else upd::update_body<NB, MB, KW, true, true, false, kWarps>(IB, KW, NB, it.p[0], it.p[1], nullptr,
                                                                      it.p[2], 1, it.col0, smem);
         break;
       default:
-        if constexpr (V2) v2::update_v2_body<NB, KW, MB, false, kWarps>(smem, bars, 0, it.p[2], it.p[3], it.col0);
+        if constexpr (V2)
+          v2::update_v2_body<NB, KW, MB, false, kWarps>(smem, bars, 0, it.p[2], it.p[3], it.col0, hook);
         else upd::update_body<NB, MB, KW, true, false, false, kWarps>(IB, KW, NB, it.p[0], it.p[1], it.p[2],
                                                                       it.p[3], 1, it.col0, smem);
         break;
@@ -119,6 +166,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       atomicAdd(done + it.task, 1);
       if (prof) prof[3 * (size_t)i + 2] = globaltimer();
     }
+    slot ^= 1;
   }
 }
 

@@ -20,7 +20,8 @@
 //    copies (cp.async.bulk + mbarrier complete_tx) land in one piece per
 //    column group; each warp waits on the group's mbarrier and then runs all
 //    its panels independently of the other warps.
-//  * C1 rows of panel p+1 are prefetched into registers during panel p.
+//  * C1 rows of panel p+1 are prefetched into registers during step C of
+//    panel p and serve both as W's initial value and for C1 -= W'.
 //
 // Packed reflector tile (written by the GEQRT/TSQRT kernels, panel_fast.cuh):
 //   V: NG column groups of GW columns (GW = 16 for IB in {8,16}, 32 for IB in
@@ -152,9 +153,16 @@ __device__ __forceinline__ void pack_panel(double* __restrict__ gpk, int p, VF v
 // ---- the update body ---------------------------------------------------------
 // Columns [col0, col0 + W*8*MB) of one task; spk = the smem packed tile whose
 // group barriers `bars` were armed by issue_packed_loads (parity `par`).
-template <int NB, int IB, int MB, bool LARFB, int W>
+struct NoHook {
+  __device__ void operator()(int) const {}
+};
+
+// hook(p) is called by every thread at the start of panel p (the DAG kernel
+// claims its next work item there, overlapping the claim with the tail).
+template <int NB, int IB, int MB, bool LARFB, int W, class Hook = NoHook>
 __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, uint64_t* bars, uint32_t par,
-                                               double* __restrict__ C1, double* __restrict__ C2, int col0) {
+                                               double* __restrict__ C1, double* __restrict__ C2, int col0,
+                                               Hook hook = Hook()) {
   using P = Pk<NB, IB>;
   constexpr int RB = NB / 8;
   constexpr int NBK = P::NBK;
@@ -162,7 +170,10 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, g = lane >> 2;
   const int wc0 = col0 + warp * 8 * MB;  // first column of this warp
-  if (wc0 >= NB) return;                 // idle warp (8*MB*W > NB): no CTA barrier follows
+  if (wc0 >= NB) {                       // idle warp (8*MB*W > NB): no CTA barrier follows
+    for (int p = 0; p < P::NP; ++p) hook(p);
+    return;
+  }
 
   // ---- C2 slab -> registers: acc[mb][rb][j] = C2(8rb+2t+j, wc0+8mb+g) --------
   double acc[MB][RB][2];
@@ -191,6 +202,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
 
 #pragma unroll 1
   for (int p = 0; p < P::NP; ++p) {
+    hook(p);
     const int c0 = p * IB;
     const int q = p / P::PPG, cb = (p % P::PPG) * P::PW;
     if (p % P::PPG == 0) mbar_wait(&bars[q], par);
@@ -208,17 +220,6 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
           w[mb][nb][j] = LARFB ? 0.0 : c1n[mb][nb][j];
           w2[mb][nb][j] = 0.0;
         }
-    if (!LARFB && p + 1 < P::NP) {  // prefetch the C1 rows of panel p+1
-#pragma unroll
-      for (int mb = 0; mb < MB; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < NBK; ++nb) {
-          const double2 v = *reinterpret_cast<const double2*>(C1 + c0 + IB + 8 * nb + 2 * t +
-                                                             (size_t)(wc0 + 8 * mb + g) * NB);
-          c1n[mb][nb][0] = v.x;
-          c1n[mb][nb][1] = v.y;
-        }
-    }
     // B fragment (row 8rb+2t+j, col cb+8nb+g): per-thread base per (j, nb), the
     // row block rb is a compile-time offset
     const int rb0 = LARFB ? (c0 >> 3) : 0;  // V_p is zero above row c0
@@ -273,16 +274,27 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
       }
     }
 
-    // ---- C1[p rows] -= W' (re-read C1: an L1/L2 hit) --------------------------
+    // ---- C1[p rows] -= W' (c1n still holds them), then prefetch panel p+1's --
     if (!LARFB) {
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
         for (int nb = 0; nb < NBK; ++nb) {
           double* dst = C1 + c0 + 8 * nb + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
-          const double2 v = *reinterpret_cast<const double2*>(dst);
-          *reinterpret_cast<double2*>(dst) = make_double2(v.x - w[mb][nb][0], v.y - w[mb][nb][1]);
+          *reinterpret_cast<double2*>(dst) =
+              make_double2(c1n[mb][nb][0] - w[mb][nb][0], c1n[mb][nb][1] - w[mb][nb][1]);
         }
+      if (p + 1 < P::NP) {  // in flight during step C
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NBK; ++nb) {
+            const double2 v = *reinterpret_cast<const double2*>(C1 + c0 + IB + 8 * nb + 2 * t +
+                                                               (size_t)(wc0 + 8 * mb + g) * NB);
+            c1n[mb][nb][0] = v.x;
+            c1n[mb][nb][1] = v.y;
+          }
+      }
     }
 
     // ---- step C: C2^T(:, r) -= sum_i W'^T(:, i) V_p(r, i) -----------------------

@@ -57,6 +57,7 @@ _SIGS = {
     "tileqr_dist_finalize": ([], None),
     "tileqr_rng_uniform": ([_i64, _i64, _p, _i64, _u64, _u64, _p], _i),
     "tileqr_ssrfb_impl": ([_i, _i], ctypes.c_char_p),
+    "tileqr_factor_schedule": ([_i, _i], ctypes.c_char_p),
     "tileqr_factor_plan": ([_i64, _i64, _i, _i, ctypes.POINTER(_i64)], _i),
     "tileqr_set_kernel_timing": ([_i], None),
     "tileqr_kernel_times": ([_i64, _i64, _i, _i, _i, _PD, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
@@ -254,6 +255,10 @@ def factor_plan(m: int, n: int, nb: int, ib: int) -> dict:
     _check(_lib.tileqr_factor_plan(m, n, nb, ib, out), "tileqr_factor_plan")
     keys = ["levels", "launches", "geqrt", "tsqrt", "larfb", "ssrfb", "MT", "NT"]
     return dict(zip(keys, list(out)))
+
+
+def factor_schedule(nb: int, ib: int) -> str:
+    return _lib.tileqr_factor_schedule(nb, ib).decode()
 
 
 KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3, "dag": 4}

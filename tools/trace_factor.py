@@ -41,7 +41,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
         print(json.dumps({"timing": timing, "ms": round(e0.elapsed_time(e1), 3)}), flush=True)
-    recs = tq.kernel_trace(n, n, nb, ib)
+    recs = tq.kernel_trace(n, n, nb, ib, max_recs=1 << 21)
     try:
         print(json.dumps({"dag_kernel_ms": round(tq.kernel_times(n, n, nb, ib, "dag")[0], 3)}))
     except tq.TileQRError:
