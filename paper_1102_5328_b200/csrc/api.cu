@@ -211,21 +211,38 @@ static bool dag_enabled(int NB, int IB) {
   return dag::dag_supported(NB, IB) && (NB > 128 || v2_supported(NB, IB));
 }
 
-// Tasks of the flat-tree tile QR with their dependencies:
-//   G(k) <- S(k-1,k,k);  L(k,n) <- G(k), S(k-1,k,n);
-//   T(k,m) <- (m == k+1 ? G(k) : T(k,m-1)), S(k-1,m,k);
-//   S(k,m,n) <- T(k,m), (m == k+1 ? L(k,n) : S(k,m-1,n)), S(k-1,m,n).
-// Claim order: bottom level (longest weighted path to the end of the DAG)
-// descending -- a topological order, since a task's bottom level exceeds
-// each successor's -- ties by ASAP level, then task id.
+// Columns of one GEQRT / TSQRT sub-task (a multiple of IB).
+static int panel_sub_cols(int NB, int IB) {
+  const char* e = getenv("TILEQR_PANEL_SUB");
+  int sc = e ? atoi(e) : 32;
+  if (sc <= 0 || sc >= NB) sc = NB;
+  sc = std::max(IB, sc / IB * IB);
+  while (NB % sc) sc += IB;
+  return sc;
+}
+
+// Tasks of the flat-tree tile QR with their dependencies.
+// GEQRT(k) and TSQRT(k,m) are split into NS sub-tasks s of consecutive inner
+// panels: inner panel c0 of a TSQRT reads and writes only the R rows
+// [c0, c0+IB) of tile (k,k) (and its own tile (m,k)), and GEQRT(k)'s inner
+// panel c0 is the last to touch those rows, so the flat TSQRT chain of step
+// k pipelines at sub-task granularity instead of running tile after tile:
+//   G(k,s) <- G(k,s-1) | S(k-1,k,k);         L(k,n) <- G(k,NS-1), S(k-1,k,n);
+//   T(k,m,s) <- T(k,m,s-1) | S(k-1,m,k),  (m == k+1 ? G(k,s) : T(k,m-1,s));
+//   S(k,m,n) <- T(k,m,NS-1), (m == k+1 ? L(k,n) : S(k,m-1,n)), S(k-1,m,n).
+// ("a | b": a for s > 0, b for s == 0.)  Claim order: bottom level (longest
+// weighted path to the end of the DAG) descending -- a topological order,
+// since a task's bottom level exceeds each successor's -- ties by ASAP level,
+// then task id.
 static int build_dag(FactorWS* ws) {
   const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT);
   const int NB = ws->NB, IB = ws->IB;
+  const int SC = panel_sub_cols(NB, IB), NS = NB / SC;
   std::vector<int64_t> offL(KT + 1), offT(KT + 1), offS(KT + 1);
-  int64_t nG = KT, nL = 0, nT = 0, nS = 0;
+  int64_t nG = KT * NS, nL = 0, nT = 0, nS = 0;
   for (int64_t k = 0; k < KT; ++k) {
     offL[k] = nL; nL += NT - k - 1;
-    offT[k] = nT; nT += MT - k - 1;
+    offT[k] = nT; nT += (MT - k - 1) * NS;
     offS[k] = nS; nS += (MT - k - 1) * (NT - k - 1);
   }
   const int64_t ntask = nG + nL + nT + nS;
@@ -233,32 +250,38 @@ static int build_dag(FactorWS* ws) {
     set_error("tileqr_factor: DAG too large for the dataflow kernel");
     return TILEQR_ERR_ALLOC;
   }
-  auto idG = [&](int64_t k) { return k; };
+  auto idG = [&](int64_t k, int s) { return k * NS + s; };
   auto idL = [&](int64_t k, int64_t n) { return nG + offL[k] + (n - k - 1); };
-  auto idT = [&](int64_t k, int64_t m) { return nG + nL + offT[k] + (m - k - 1); };
+  auto idT = [&](int64_t k, int64_t m, int s) { return nG + nL + offT[k] + (m - k - 1) * NS + s; };
   auto idS = [&](int64_t k, int64_t m, int64_t n) {
     return nG + nL + nT + offS[k] + (m - k - 1) * (NT - k - 1) + (n - k - 1);
   };
-  struct Task { int kind; int k, m, n; int level; int ndep; int dep[3]; };
+  struct Task { int kind; int k, m, n; int level; int ndep; int dep[3]; int s; };
   std::vector<Task> tk(ntask);
   for (int64_t k = 0; k < KT; ++k) {
-    Task g{dag::kGeqrt, (int)k, (int)k, (int)k, (int)(3 * k), 0, {0, 0, 0}};
-    if (k > 0) g.dep[g.ndep++] = (int)idS(k - 1, k, k);
-    tk[idG(k)] = g;
+    for (int sub = 0; sub < NS; ++sub) {
+      Task g{dag::kGeqrt, (int)k, (int)k, (int)k, (int)(3 * k), 0, {0, 0, 0}, sub};
+      if (sub > 0) g.dep[g.ndep++] = (int)idG(k, sub - 1);
+      else if (k > 0) g.dep[g.ndep++] = (int)idS(k - 1, k, k);
+      tk[idG(k, sub)] = g;
+    }
     for (int64_t n = k + 1; n < NT; ++n) {
-      Task l{dag::kLarfb, (int)k, (int)k, (int)n, (int)(3 * k + 1), 0, {0, 0, 0}};
-      l.dep[l.ndep++] = (int)idG(k);
+      Task l{dag::kLarfb, (int)k, (int)k, (int)n, (int)(3 * k + 1), 0, {0, 0, 0}, 0};
+      l.dep[l.ndep++] = (int)idG(k, NS - 1);
       if (k > 0) l.dep[l.ndep++] = (int)idS(k - 1, k, n);
       tk[idL(k, n)] = l;
     }
     for (int64_t m = k + 1; m < MT; ++m) {
-      Task t{dag::kTsqrt, (int)k, (int)m, (int)k, (int)(2 * k + m), 0, {0, 0, 0}};
-      t.dep[t.ndep++] = (int)(m == k + 1 ? idG(k) : idT(k, m - 1));
-      if (k > 0) t.dep[t.ndep++] = (int)idS(k - 1, m, k);
-      tk[idT(k, m)] = t;
+      for (int sub = 0; sub < NS; ++sub) {
+        Task t{dag::kTsqrt, (int)k, (int)m, (int)k, (int)(2 * k + m), 0, {0, 0, 0}, sub};
+        if (sub > 0) t.dep[t.ndep++] = (int)idT(k, m, sub - 1);
+        else if (k > 0) t.dep[t.ndep++] = (int)idS(k - 1, m, k);
+        t.dep[t.ndep++] = (int)(m == k + 1 ? idG(k, sub) : idT(k, m - 1, sub));
+        tk[idT(k, m, sub)] = t;
+      }
       for (int64_t n = k + 1; n < NT; ++n) {
-        Task u{dag::kSsrfb, (int)k, (int)m, (int)n, (int)(2 * k + m + 1), 0, {0, 0, 0}};
-        u.dep[u.ndep++] = (int)idT(k, m);
+        Task u{dag::kSsrfb, (int)k, (int)m, (int)n, (int)(2 * k + m + 1), 0, {0, 0, 0}, 0};
+        u.dep[u.ndep++] = (int)idT(k, m, NS - 1);
         u.dep[u.ndep++] = (int)(m == k + 1 ? idL(k, n) : idS(k, m - 1, n));
         if (k > 0) u.dep[u.ndep++] = (int)idS(k - 1, m, n);
         tk[idS(k, m, n)] = u;
@@ -267,7 +290,7 @@ static int build_dag(FactorWS* ws) {
   }
   // weights (ns, rough B200 per-SM durations): update work at ~150 GFLOP/s
   // per SM, panel latency ~1.2 us per column
-  const double wS = 4.0 * NB * NB * NB / 150.0, wL = wS / 2, wP = 1200.0 * NB;
+  const double wS = 4.0 * NB * NB * NB / 150.0, wL = wS / 2, wP = 1200.0 * NB / NS;
   auto weight = [&](int kind) { return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : wP; };
   std::vector<int> byLevel(ntask);
   {
@@ -289,6 +312,7 @@ static int build_dag(FactorWS* ws) {
   std::sort(order.begin(), order.end(), [&](int a, int b) {
     if (bl[a] != bl[b]) return bl[a] > bl[b];
     if (tk[a].level != tk[b].level) return tk[a].level < tk[b].level;
+    if (tk[a].s != tk[b].s) return tk[a].s < tk[b].s;
     return a < b;
   });
   const int cols = dag::dag_cols(NB);
@@ -307,6 +331,7 @@ static int build_dag(FactorWS* ws) {
     dag::Item it{};
     it.kind = t.kind;
     it.task = i;
+    if (t.kind == dag::kGeqrt || t.kind == dag::kTsqrt) it.col0 = (t.s * SC) | ((t.s + 1) * SC) << 16;
     it.ndep = t.ndep;
     for (int d = 0; d < t.ndep; ++d) {
       it.dep[d] = t.dep[d];
@@ -326,7 +351,7 @@ static int build_dag(FactorWS* ws) {
         break;
     }
     for (int sl = 0; sl < parts(t.kind); ++sl) {
-      it.col0 = sl * cols;
+      if (parts(t.kind) > 1 || t.kind == dag::kLarfb || t.kind == dag::kSsrfb) it.col0 = sl * cols;
       items.push_back(it);
       ws->item_kind.push_back((unsigned char)t.kind);
       ws->item_level.push_back(t.level);

@@ -139,13 +139,15 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       if (p == NPAN - 1 && nxt < nitems) fetch_desc(nxt, slot ^ 1);
     };
     switch (it.kind) {
-      case kGeqrt:
+      case kGeqrt:  // inner panels [col0 & 0xffff, col0 >> 16)
         pf::panel_fast_body<false, NB, kWarps>(IB, it.p[0], nullptr, it.p[2],
-                                               reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr);
+                                               reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
+                                               it.col0 & 0xffff, it.col0 >> 16);
         break;
       case kTsqrt:
         pf::panel_fast_body<true, NB, kWarps>(IB, it.p[0], it.p[1], it.p[2],
-                                              reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr);
+                                              reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
+                                              it.col0 & 0xffff, it.col0 >> 16);
         break;
       case kLarfb:
         if constexpr (V2)

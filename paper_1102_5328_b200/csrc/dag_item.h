@@ -13,7 +13,8 @@ enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3 };
 struct Item {
   int kind;
   int task;      // completion counter index
-  int col0;      // first column of the slab (LARFB / SSRFB)
+  int col0;      // LARFB / SSRFB: first column of the slab; GEQRT / TSQRT: the
+                 // sub-task's inner-panel columns [col0 & 0xffff, col0 >> 16)
   int ndep;
   int dep[3];    // tasks whose counters must reach need[] before the item runs
   int need[3];

@@ -58,8 +58,12 @@ struct FastSmem {
 };
 
 template <bool TS, int NB, int kWarps>
+// Inner panels c0 = cbeg, cbeg+IB, ... < cend (the whole tile by default; the
+// DAG kernel runs a TSQRT / GEQRT as several sub-tasks of consecutive inner
+// panels, every state between them lives in global memory).
 __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double* const Bx, double* const Tg,
-                                                unsigned char* smem_raw, double* const Vpk = nullptr) {
+                                                unsigned char* smem_raw, double* const Vpk = nullptr,
+                                                int cbeg = 0, int cend = NB) {
   constexpr int kThreads = kWarps * 32;
   constexpr int RW = NB / kWarps;  // rows per warp in the factorization
   constexpr int RB = NB / 8;       // 8-row blocks in the trailing update
@@ -76,7 +80,7 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
 #else
 #define TQ_PHASE(k) do { } while (0)
 #endif
-  for (int c0 = 0; c0 < NB; c0 += IB) {
+  for (int c0 = cbeg; c0 < cend; c0 += IB) {
     // ---- stage the panel (coalesced) and, for TSQRT, the R block -------------
     for (int idx = tid; idx < NB * IB; idx += kThreads) {
       const int c = idx / NB, r = idx - c * NB;
@@ -298,9 +302,13 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
     const int nbi = IB / 8;
     for (int cb = c0 + IB + 8 * warp; cb < NB; cb += 8 * kWarps) {
       const int col = cb + g;
+      // GEQRT: rows above c0 of the trailing columns are R rows of earlier
+      // inner panels -- never loaded or stored here (a concurrent TSQRT
+      // sub-task of the DAG kernel may own them)
       double acc[RB][2];
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
+        if (!TS && 8 * rb + 7 < c0) { acc[rb][0] = acc[rb][1] = 0.0; continue; }
         const double2 v = *reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)col * NB);
         acc[rb][0] = v.x;
         acc[rb][1] = v.y;
@@ -354,9 +362,11 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
         }
       }
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb)
+      for (int rb = 0; rb < RB; ++rb) {
+        if (!TS && 8 * rb + 7 < c0) continue;
         *reinterpret_cast<double2*>(B + 8 * rb + 2 * a + (size_t)col * NB) =
             make_double2(acc[rb][0], acc[rb][1]);
+      }
       __syncwarp();
     }
     __syncthreads();  // trailing writes visible before the next panel is staged

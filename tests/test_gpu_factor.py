@@ -194,10 +194,13 @@ def test_dataflow_kernel_equals_level_launcher(tq, monkeypatch, m, n, nb, ib, se
     tq.finalize()
     monkeypatch.setenv("TILEQR_SCHED", "levels")
     A0, T0, _ = gpu_factor(tq, a, nb, ib)
-    tq.finalize()
     monkeypatch.delenv("TILEQR_SCHED")
-    for _ in range(3):
-        A1, T1, info = gpu_factor(tq, a, nb, ib)
-        assert int(info.item()) == 0
-        assert torch.equal(A0, A1) and torch.equal(T0, T1)
+    # GEQRT / TSQRT split into sub-tasks of one inner panel, 32 columns, whole tile
+    for sub in (ib, 32, nb):
+        tq.finalize()
+        monkeypatch.setenv("TILEQR_PANEL_SUB", str(sub))
+        for _ in range(2):
+            A1, T1, info = gpu_factor(tq, a, nb, ib)
+            assert int(info.item()) == 0
+            assert torch.equal(A0, A1) and torch.equal(T0, T1)
     tq.finalize()
