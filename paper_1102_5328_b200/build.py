@@ -11,8 +11,13 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libtileqr.so")
+# TILEQR_BUILD_VARIANT=prof builds a diagnostic copy (-DTILEQR_PANEL_PROF) as
+# libtileqr_prof.so (loaded when TILEQR_LIB points at it); the default build is
+# the product library
+VARIANT = os.environ.get("TILEQR_BUILD_VARIANT", "")
+BUILD = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = os.path.join(HERE, "libtileqr" + (f"_{VARIANT}" if VARIANT else "") + ".so")
+EXTRA = (["-DTILEQR_PANEL_PROF"] if VARIANT == "prof" else []) + os.environ.get("TILEQR_EXTRA_FLAGS", "").split()
 SOURCES = ["kernels_layout.cu", "kernels_panel.cu", "kernels_panel_fast.cu", "kernels_update.cu",
            "api.cu", "tune.cu", "dist.cu"] + [f"update_nb{nb}.cu" for nb in (32, 64, 96, 128, 160, 192, 224, 256)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -42,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if force or not os.path.exists(o) or os.path.getmtime(o) < max(os.path.getmtime(s), hdr_mtime):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-I", inc, "-c", s, "-o", o])
+            jobs.append([NVCC, *ARCH, *FLAGS, *EXTRA, "-I", inc, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -168,6 +168,7 @@ struct FactorWS {
   cudaEvent_t dag_ev[2] = {nullptr, nullptr};
   bool use_dag = false, dag_timed = false;
   std::vector<unsigned char> item_kind;  // host copies for the diagnostics
+  std::vector<int> item_info;            // per item: kind, k, m, n, sub-task / slab column
   std::vector<int> item_level;
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
   struct Rec { int kind; int64_t tasks; int64_t level; cudaEvent_t a, b; };
@@ -354,6 +355,7 @@ static int build_dag(FactorWS* ws) {
       if (parts(t.kind) > 1 || t.kind == dag::kLarfb || t.kind == dag::kSsrfb) it.col0 = sl * cols;
       items.push_back(it);
       ws->item_kind.push_back((unsigned char)t.kind);
+      for (int v : {t.kind, t.k, t.m, t.n, (t.kind >= dag::kLarfb) ? it.col0 : t.s}) ws->item_info.push_back(v);
       ws->item_level.push_back(t.level);
     }
   }
@@ -381,8 +383,12 @@ static int run_dag(FactorWS* ws, cudaStream_t stream) {
     prof = ws->d_prof;
     TQ_CUDA(cudaEventRecord(ws->dag_ev[0], stream));
   }
-  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, ws->nitems, ws->d_ctr, ws->d_ctr + 1, ws->nsm, prof,
-                      stream);
+  int nitems = ws->nitems;
+  if (const char* e = getenv("TILEQR_DAG_NITEMS")) {  // diagnostics: run a prefix of the claim order
+    const long v = atol(e);
+    if (v >= 0 && v < nitems) nitems = (int)v;
+  }
+  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, nitems, ws->d_ctr, ws->d_ctr + 1, ws->nsm, prof, stream);
   if (rc) return rc;
   if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
   ws->dag_timed = g_timing != 0;
@@ -969,6 +975,20 @@ int tileqr_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t se
 }
 
 const char* tileqr_ssrfb_impl(int NB, int IB) { return ssrfb_impl_name(NB, IB); }
+
+// Diagnostic (not in the header): item idx of the dataflow work list of a cached
+// shape -> out[5] = {kind, k, m, n, sub-task or slab column}.
+int tileqr_debug_dag_item(int64_t M, int64_t N, int NB, int IB, int64_t idx, int* out) {
+  int dev;
+  TQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  if (it == g_ws.end() || !it->second->use_dag) return TILEQR_ERR_NOT_INIT;
+  FactorWS* ws = it->second.get();
+  if (idx < 0 || idx >= ws->nitems) return -5;
+  for (int q = 0; q < 5; ++q) out[q] = ws->item_info[5 * idx + q];
+  return 0;
+}
 
 // Diagnostic (not in the header): accumulated phase cycles of the fast panel kernel.
 int tileqr_debug_panel_prof(unsigned long long* out, int reset) { return tileqr::panel_prof_read(out, reset); }

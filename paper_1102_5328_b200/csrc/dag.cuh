@@ -19,6 +19,8 @@
 // identical to it.
 #pragma once
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "dag_item.h"
@@ -28,7 +30,6 @@
 namespace tileqr {
 namespace dag {
 
-constexpr int kThreads = kWarps * 32;
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -42,22 +43,52 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 template <int NB>
 constexpr bool dag_v2() { return NB <= 128; }
 
+// Ring stages of the packed reflector tile per CTA: as many as fit next to
+// the panel body's shared memory in ~110 KB (2 CTAs per SM), at least 2.
+template <int NB, int KW>
+constexpr int dag_stages() {
+  if constexpr (NB <= 128 && NB % KW == 0) {
+    using P = v2::Pk<NB, KW>;
+    constexpr size_t stage = (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double);
+    constexpr size_t budget = 110 * 1024;
+#ifdef TILEQR_FULL_RING
+    constexpr int s = P::NG;
+#else
+    constexpr int s = (int)(budget / stage);
+#endif
+    return s < 2 ? 2 : (s > P::NG ? P::NG : s);
+  } else {
+    return 1;
+  }
+}
+
 template <int NB, int KW>
 struct DagSmem {
+  static constexpr int W = dag_warps(NB);
   static constexpr int MB = dag_mb(NB);
-  using LS = upd::Layout<NB, MB, KW, false, false, kWarps>;
+  using LS = upd::Layout<NB, MB, KW, false, false, W>;
   static constexpr size_t old_bytes =
-      (2 * (size_t)LS::STAGE + (size_t)kWarps * 8 * MB * (KW + 4)) * sizeof(double);
-  static constexpr size_t v2_bytes = (NB % KW == 0) ? (size_t)v2::Pk<NB, (NB % KW == 0 ? KW : 8)>::TOTAL * sizeof(double) : 0;
+      (2 * (size_t)LS::STAGE + (size_t)W * 8 * MB * (KW + 4)) * sizeof(double);
+  static constexpr size_t v2_bytes =
+      (NB % KW == 0) ? v2::Ring<NB, (NB % KW == 0 ? KW : 8), dag_stages<NB, KW>()>::bytes : 0;
   static constexpr size_t upd_bytes = dag_v2<NB>() ? v2_bytes : old_bytes;
-  static constexpr size_t pan_bytes = sizeof(pf::FastSmem<NB, kWarps>);
+  static constexpr size_t pan_bytes = sizeof(pf::FastSmem<NB, W>);
+#ifdef TILEQR_ONE_CTA  // diagnostics: force one CTA per SM
+  static constexpr size_t bytes0 = upd_bytes > pan_bytes ? upd_bytes : pan_bytes;
+  static constexpr size_t bytes = bytes0 > 120 * 1024 ? bytes0 : 120 * 1024;
+#else
   static constexpr size_t bytes = upd_bytes > pan_bytes ? upd_bytes : pan_bytes;
+#endif
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // 16-byte async copy global -> shared (L2 only), for the item descriptors
@@ -70,23 +101,25 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 // prof (nullable, diagnostics): per item i, prof[3i .. 3i+2] = claim time,
 // start time (inputs ready), end time in globaltimer ns.
 //
-// Claims overlap the tail of the running item: during the second-to-last
-// inner panel of an update item thread 0 claims the next item (atomicAdd),
-// during the last one its descriptor is copied into the other smem slot, so
-// at the end only the dependency check remains.  A claimed item is held for
-// about two inner panels.  Items are claimed in list order and a CTA's held
+// Claims overlap the tail of the running item: three inner panels before the
+// end of an update item thread 0 claims the next item (atomicAdd), two before
+// its descriptor is copied into the other smem slot, one before its operand
+// tiles are prefetched into L2, so at the end only the dependency check
+// remains.  A claimed item is held for about three inner panels.  Items are claimed in list order and a CTA's held
 // item always follows its running one, so the smallest unfinished item is
 // always running or about to (no deadlock).
 template <int NB, int KW>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(dag_warps(NB) * 32, dag_ctas_per_sm(NB))
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
            unsigned long long* prof) {
+  constexpr int W = dag_warps(NB);
   constexpr int MB = dag_mb(NB);
+  constexpr int S = dag_stages<NB, KW>();
   static_assert(sizeof(Item) % 16 == 0, "Item is copied in 16-byte chunks");
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(16) Item s_desc[2];
   __shared__ int s_cur;
-  __shared__ __align__(8) uint64_t bars[8];
+  __shared__ __align__(8) uint64_t full[8], empty[8];
   constexpr bool V2 = dag_v2<NB>();
   int nxt = -1;   // thread 0: item claimed ahead (-1: none)
   int slot = 0;   // descriptor slot of the running item (all threads)
@@ -123,7 +156,8 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
           }
         if (prof) prof[3 * (size_t)cur + 1] = globaltimer();
         if constexpr (V2) {
-          if (it.kind == kLarfb || it.kind == kSsrfb) v2::issue_packed_loads<NB, KW>(it.pk, smem, bars);
+          if (it.kind == kLarfb || it.kind == kSsrfb)
+            v2::ring_start<NB, KW, S>(it.pk, smem, full, empty, v2::active_warps<NB, MB, W>(it.col0));
         }
       }
     }
@@ -131,37 +165,59 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     if (s_cur >= nitems) return;
     const int i = s_cur;
     const Item it = s_desc[slot];
-    // claim-ahead hook of the update bodies (thread 0)
+    // claim-ahead hook of the update bodies (thread 0), one step per inner
+    // panel near the end of the item: claim the next item, fetch its
+    // descriptor, prefetch its operand tiles into L2 (bulk prefetch; data a
+    // producer is still writing stays coherent in L2)
     constexpr int NPAN = NB / KW;
+    constexpr int PC = NPAN >= 3 ? NPAN - 3 : 0, PD = NPAN >= 2 ? NPAN - 2 : 0, PF = NPAN - 1;
     auto hook = [&](int p) {
       if (threadIdx.x != 0) return;
-      if (p == (NPAN >= 2 ? NPAN - 2 : 0)) nxt = atomicAdd(next, 1);
-      if (p == NPAN - 1 && nxt < nitems) fetch_desc(nxt, slot ^ 1);
+      if (p == PC) nxt = atomicAdd(next, 1);
+      if (nxt >= nitems) return;
+      if (p == PD) fetch_desc(nxt, slot ^ 1);
+#ifndef TILEQR_NO_HOOK_PREFETCH
+      if (p == PF) {
+        cp_async_wait<0>();
+        const Item& n = s_desc[slot ^ 1];
+        if (n.kind == kSsrfb || n.kind == kLarfb) {
+          constexpr uint32_t tb = NB * NB * sizeof(double);
+          prefetch_l2(n.p[n.kind == kSsrfb ? 3 : 2], tb);
+          if (n.kind == kSsrfb) prefetch_l2(n.p[2], tb);
+          if constexpr (V2) prefetch_l2(n.pk, (uint32_t)v2::Pk<NB, (NB % KW == 0 ? KW : 8)>::TOTAL * 8);
+        }
+      }
+#endif
     };
     switch (it.kind) {
       case kGeqrt:  // inner panels [col0 & 0xffff, col0 >> 16)
-        pf::panel_fast_body<false, NB, kWarps>(IB, it.p[0], nullptr, it.p[2],
+        pf::panel_fast_body<false, NB, W>(IB, it.p[0], nullptr, it.p[2],
                                                reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
                                                it.col0 & 0xffff, it.col0 >> 16);
         break;
       case kTsqrt:
-        pf::panel_fast_body<true, NB, kWarps>(IB, it.p[0], it.p[1], it.p[2],
+        pf::panel_fast_body<true, NB, W>(IB, it.p[0], it.p[1], it.p[2],
                                               reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
                                               it.col0 & 0xffff, it.col0 >> 16);
         break;
       case kLarfb:
         if constexpr (V2)
-          v2::update_v2_body<NB, KW, MB, true, kWarps>(smem, bars, 0, nullptr, it.p[2], it.col0, hook);
-        else upd::update_body<NB, MB, KW, true, true, false, kWarps>(IB, KW, NB, it.p[0], it.p[1], nullptr,
+          v2::update_v2_body<NB, KW, MB, true, W, S>(it.pk, smem, full, empty, nullptr, it.p[2], it.col0, hook);
+        else upd::update_body<NB, MB, KW, true, true, false, W>(IB, KW, NB, it.p[0], it.p[1], nullptr,
                                                                      it.p[2], 1, it.col0, smem);
         break;
       default:
         if constexpr (V2)
-          v2::update_v2_body<NB, KW, MB, false, kWarps>(smem, bars, 0, it.p[2], it.p[3], it.col0, hook);
-        else upd::update_body<NB, MB, KW, true, false, false, kWarps>(IB, KW, NB, it.p[0], it.p[1], it.p[2],
+          v2::update_v2_body<NB, KW, MB, false, W, S>(it.pk, smem, full, empty, it.p[2], it.p[3], it.col0,
+                                                      hook);
+        else upd::update_body<NB, MB, KW, true, false, false, W>(IB, KW, NB, it.p[0], it.p[1], it.p[2],
                                                                       it.p[3], 1, it.col0, smem);
         break;
     }
+    // every thread orders its generic-proxy shared-memory accesses of this
+    // item before the async-proxy (TMA) writes of the next item into the same
+    // shared memory (a CTA barrier alone does not order across proxies)
+    v2::fence_proxy_async_smem();
     __syncthreads();  // every write of the item issued; smem free for the next item
     if (threadIdx.x == 0) {
       __threadfence();
@@ -180,12 +236,18 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   int per_sm = 0;
+  constexpr int kThreads = dag_warps(NB) * 32;
   TQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, bytes));
   if (per_sm < 1) {
     set_error("DAG kernel does not fit on an SM");
     return TILEQR_ERR_CUDA;
   }
-  const int grid = std::min(nitems, nsm * per_sm);
+  if (nitems <= 0) return 0;
+  int grid = std::min(nitems, nsm * per_sm);
+  if (const char* e = getenv("TILEQR_DAG_GRID")) {  // diagnostics: fewer resident CTAs
+    const int g = atoi(e);
+    if (g > 0 && g < grid) grid = g;
+  }
   kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof);
   TQ_LAUNCH_CHECK();
   return 0;

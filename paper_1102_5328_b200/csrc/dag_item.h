@@ -5,7 +5,12 @@
 namespace tileqr {
 namespace dag {
 
-constexpr int kWarps = 8;  // warps per CTA of the DAG kernel
+// CTA geometry of the DAG kernel.  NB <= 128 (packed-reflector update with a
+// shared-memory ring): 2 CTAs of 4 warps per SM, so one CTA's item prologue,
+// epilogue and dependency waits overlap the other's DMMA work.  NB > 128:
+// 1 CTA of 8 warps per SM.
+__host__ __device__ constexpr int dag_warps(int NB) { return NB <= 128 ? 4 : 8; }
+__host__ __device__ constexpr int dag_ctas_per_sm(int NB) { return NB <= 128 ? 2 : 1; }
 
 enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3 };
 
@@ -22,9 +27,9 @@ struct Item {
   double* pk;    // packed reflector tile (NB <= 128): written by GEQRT/TSQRT, read by LARFB/SSRFB
 };
 
-// Update columns per item for tile order NB: 8 warps x 8*MB columns.
+// Update columns per item for tile order NB: warps x 8*MB columns.
 __host__ __device__ constexpr int dag_mb(int NB) { return (NB == 96 || NB == 128) ? 2 : 1; }
-__host__ __device__ constexpr int dag_cols(int NB) { return kWarps * 8 * dag_mb(NB); }
+__host__ __device__ constexpr int dag_cols(int NB) { return dag_warps(NB) * 8 * dag_mb(NB); }
 
 // DAG kernel supported for these (NB, IB): the fast panel set.
 inline bool dag_supported(int NB, int IB) {

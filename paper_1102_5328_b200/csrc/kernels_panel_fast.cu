@@ -2,6 +2,7 @@
 // (body in panel_fast.cuh): one CTA of 8 warps per task.
 #include <stdlib.h>
 
+#include "dag_item.h"
 #include "panel_fast.cuh"
 
 namespace tileqr {
@@ -32,21 +33,24 @@ int launch_fast_w(int IB, int batch, double* const* R, double* const* B, double*
   return 0;
 }
 
-int panel_warps() {
+// Warps per panel CTA: the DAG kernel's geometry for this NB (dag_item.h),
+// so the batched and the dataflow schedules compute bitwise the same
+// reductions; TILEQR_PANEL_WARPS=4|8 overrides (diagnostics).
+int panel_warps(int NB) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TILEQR_PANEL_WARPS");
-    v = e ? atoi(e) : 8;
-    if (v != 4 && v != 8) v = 8;
+    v = e ? atoi(e) : 0;
+    if (v != 4 && v != 8) v = 0;
   }
-  return v;
+  return v ? v : dag::dag_warps(NB);
 }
 
 template <bool TS, int NB>
 int launch_fast_t(int IB, int batch, double* const* R, double* const* B, double* const* T,
                   cudaStream_t s, double* const* Pk) {
-  return panel_warps() == 8 ? launch_fast_w<TS, NB, 8>(IB, batch, R, B, T, s, Pk)
-                            : launch_fast_w<TS, NB, 4>(IB, batch, R, B, T, s, Pk);
+  return panel_warps(NB) == 8 ? launch_fast_w<TS, NB, 8>(IB, batch, R, B, T, s, Pk)
+                              : launch_fast_w<TS, NB, 4>(IB, batch, R, B, T, s, Pk);
 }
 
 template <bool TS>

@@ -20,7 +20,9 @@
 //     W = [R_p; C]^T-part ... exactly the SSRFB/LARFB steps A/B/C of
 //     kernels_update.cu on DMMA, reading V_p (swizzled) and T_p from smem.
 // TSQRT never writes the strict lower part of R (read concurrently by the
-// LARFB of the same DAG level).
+// LARFB of the same DAG level).  Global loads bypass L1
+// (ld.global.cg): the persistent DAG kernel runs two CTAs per SM whose items
+// hand tiles to other SMs, and L2 is the coherence point.
 #pragma once
 
 #include <math.h>
@@ -32,7 +34,7 @@
 #include "update_v2.cuh"
 
 #ifdef TILEQR_PANEL_PROF  // phase-cycle diagnostics: only kernels_panel_fast.cu is built with it
-namespace tileqr { __device__ unsigned long long g_panel_prof[16]; }
+namespace tileqr { static __device__ unsigned long long g_panel_prof[16]; }  // per translation unit
 #endif
 
 namespace tileqr {
@@ -82,14 +84,35 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
 #endif
   for (int c0 = cbeg; c0 < cend; c0 += IB) {
     // ---- stage the panel (coalesced) and, for TSQRT, the R block -------------
-    for (int idx = tid; idx < NB * IB; idx += kThreads) {
-      const int c = idx / NB, r = idx - c * NB;
-      S.Vs[vsw(r, c, LDV)] = B[r + (size_t)(c0 + c) * NB];
+    // trailing columns of this inner panel -> L2 while the panel is factored
+#ifndef TILEQR_NO_PANEL_PREFETCH
+    if (tid == 0 && c0 + IB < NB)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(B + (size_t)(c0 + IB) * NB),
+                   "r"((uint32_t)((NB - c0 - IB) * NB * sizeof(double)))
+                   : "memory");
+#endif
+    // panel columns: 8 loads in flight per thread before the shared stores
+    for (int idx0 = tid; idx0 < NB * IB; idx0 += 8 * kThreads) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = idx0 + u * kThreads;
+        // GEQRT: rows above c0 are R rows of earlier inner panels that a
+        // concurrent TSQRT sub-task may be rewriting -- never read them (a
+        // stale line could even land in the L1 another CTA of this SM reads
+        // after its acquire); their operand entries are 0 anyway
+        v[u] = (idx < NB * IB && (TS || idx % NB >= c0)) ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = idx0 + u * kThreads;
+        if (idx < NB * IB) S.Vs[vsw(idx % NB, idx / NB, LDV)] = v[u];
+      }
     }
     if (TS) {
       for (int idx = tid; idx < IB * IB; idx += kThreads) {
         const int c = idx / IB, i = idx - c * IB;
-        S.Rin[i * LDR + c] = (i <= c) ? R[(c0 + i) + (size_t)(c0 + c) * NB] : 0.0;
+        S.Rin[i * LDR + c] = (i <= c) ? __ldcg(&R[(c0 + i) + (size_t)(c0 + c) * NB]) : 0.0;
       }
     }
     __syncthreads();
@@ -309,27 +332,34 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         if (!TS && 8 * rb + 7 < c0) { acc[rb][0] = acc[rb][1] = 0.0; continue; }
-        const double2 v = *reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)col * NB);
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)col * NB));
         acc[rb][0] = v.x;
         acc[rb][1] = v.y;
       }
-      // step A: W^T(col, i) = [TS: R(c0+i, col)] + sum_r C^T(col, r) V_p(r, i)
-      double wacc[4][2];
+      // step A: W^T(col, i) = [TS: R(c0+i, col)] + sum_r C^T(col, r) V_p(r, i);
+      // two partial sums (k rows 2a and 2a+1) per output block
+      double wacc[4][2], wacc2[4][2];
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          wacc[nb][j] = (TS && nb < nbi) ? R[(c0 + 8 * nb + 2 * a + j) + (size_t)col * NB] : 0.0;
+        for (int j = 0; j < 2; ++j) {
+          wacc[nb][j] = (TS && nb < nbi) ? __ldcg(&R[(c0 + 8 * nb + 2 * a + j) + (size_t)col * NB]) : 0.0;
+          wacc2[nb][j] = 0.0;
+        }
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
         if (!TS && 8 * rb + 7 < c0) continue;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int r = 8 * rb + 2 * a + j;
+        for (int nb = 0; nb < 4; ++nb)
+          if (nb < nbi) {
+            dmma(wacc[nb][0], wacc[nb][1], acc[rb][0], S.Vs[vsw(8 * rb + 2 * a, 8 * nb + g, LDV)]);
+            dmma(wacc2[nb][0], wacc2[nb][1], acc[rb][1], S.Vs[vsw(8 * rb + 2 * a + 1, 8 * nb + g, LDV)]);
+          }
+      }
 #pragma unroll
-          for (int nb = 0; nb < 4; ++nb)
-            if (nb < nbi) dmma(wacc[nb][0], wacc[nb][1], acc[rb][j], S.Vs[vsw(r, 8 * nb + g, LDV)]);
-        }
+      for (int nb = 0; nb < 4; ++nb) {
+        wacc[nb][0] += wacc2[nb][0];
+        wacc[nb][1] += wacc2[nb][1];
       }
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb)
@@ -347,8 +377,9 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
         Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
         Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
         if (TS) {
-          R[(c0 + 8 * nb + 2 * a) + (size_t)col * NB] -= o0;
-          R[(c0 + 8 * nb + 2 * a + 1) + (size_t)col * NB] -= o1;
+          double* r0 = &R[(c0 + 8 * nb + 2 * a) + (size_t)col * NB];
+          r0[0] = __ldcg(r0) - o0;
+          r0[1] = __ldcg(r0 + 1) - o1;
         }
         __syncwarp();
       }

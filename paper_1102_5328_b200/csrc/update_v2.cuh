@@ -93,31 +93,61 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 // generic-proxy accesses before / async-proxy (TMA) accesses after
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
-// One thread: (re)arm the NG group barriers and issue the bulk copies of a
-// packed tile (each group: its V block + the T_p of its panels).  The caller
-// orders this before the other threads' waits (CTA barrier).
-template <int NB, int IB>
-__device__ __forceinline__ void issue_packed_loads(const double* __restrict__ gpk, double* spk, uint64_t* bars) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Shared-memory ring of S stages for the column groups of a packed tile:
+// stage s = [V block of a group (GDBL) | T_p of its panels (PPG * TP)].
+// S >= NG stages hold the whole tile (no refill).
+template <int NB, int IB, int S>
+struct Ring {
   using P = Pk<NB, IB>;
+  static constexpr int SD = P::GDBL + P::PPG * P::TP;  // doubles per stage
+  static constexpr int NS = S < P::NG ? S : P::NG;     // stages in use
+  static constexpr size_t bytes = (size_t)NS * SD * sizeof(double);
+};
+
+// Thread 0: copy group q of the packed tile gpk into its stage (barrier full[q % S]).
+template <int NB, int IB, int S>
+__device__ __forceinline__ void ring_issue(const double* __restrict__ gpk, double* spk, uint64_t* full, int q) {
+  using P = Pk<NB, IB>;
+  using RG = Ring<NB, IB, S>;
+  const int st = q % RG::NS;
+  const int p0 = q * P::PPG;
+  const int np = (P::NP - p0) < P::PPG ? (P::NP - p0) : P::PPG;
+  const uint32_t vb = P::GDBL * 8, tb = np * P::TP * 8;
+  double* dst = spk + (size_t)st * RG::SD;
+  mbar_expect_tx(&full[st], vb + tb);
+  bulk_g2s(dst, gpk + q * P::GDBL, vb, &full[st]);
+  bulk_g2s(dst + P::GDBL, gpk + P::TOFF + p0 * P::TP, tb, &full[st]);
+}
+
+// Thread 0, before the CTA barrier that starts an update item: (re)arm the
+// ring barriers (full: 1 arrival + tx bytes; empty: one arrival per active
+// warp) and issue the first stages.
+template <int NB, int IB, int S>
+__device__ __forceinline__ void ring_start(const double* __restrict__ gpk, double* spk, uint64_t* full,
+                                           uint64_t* empty, int nact) {
+  using RG = Ring<NB, IB, S>;
   fence_proxy_async();
-  for (int q = 0; q < P::NG; ++q) mbar_init(&bars[q], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  for (int q = 0; q < P::NG; ++q) {
-    const int p0 = q * P::PPG;
-    const int np = (P::NP - p0) < P::PPG ? (P::NP - p0) : P::PPG;
-    const uint32_t vb = P::GDBL * 8, tb = np * P::TP * 8;
-    mbar_expect_tx(&bars[q], vb + tb);
-    bulk_g2s(spk + q * P::GDBL, gpk + q * P::GDBL, vb, &bars[q]);
-    bulk_g2s(spk + P::TOFF + p0 * P::TP, gpk + P::TOFF + p0 * P::TP, tb, &bars[q]);
+  for (int s = 0; s < RG::NS; ++s) {
+    mbar_init(&full[s], 1);
+    mbar_init(&empty[s], nact);
   }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (int q = 0; q < RG::NS; ++q) ring_issue<NB, IB, S>(gpk, spk, full, q);
 }
 
 // All threads of a CTA (kThreads): write panel p of the packed tile from
@@ -159,11 +189,14 @@ struct NoHook {
 
 // hook(p) is called by every thread at the start of panel p (the DAG kernel
 // claims its next work item there, overlapping the claim with the tail).
-template <int NB, int IB, int MB, bool LARFB, int W, class Hook = NoHook>
-__device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, uint64_t* bars, uint32_t par,
-                                               double* __restrict__ C1, double* __restrict__ C2, int col0,
-                                               Hook hook = Hook()) {
+// Ring of S stages (ring_start issued by thread 0 before the CTA barrier);
+// gpk = the packed tile in global memory (refills).
+template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook>
+__device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, double* spk, uint64_t* full,
+                                               uint64_t* empty, double* __restrict__ C1, double* __restrict__ C2,
+                                               int col0, Hook hook = Hook()) {
   using P = Pk<NB, IB>;
+  using RG = Ring<NB, IB, S>;
   constexpr int RB = NB / 8;
   constexpr int NBK = P::NBK;
   constexpr bool SPLIT = NBK * MB < 4;  // two partial sums per step-A block when chains are few
@@ -182,7 +215,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
     const double* src = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb) {
-      const double2 v = *reinterpret_cast<const double2*>(src + 8 * rb);
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(src + 8 * rb));  // streaming: L2 only
       acc[mb][rb][0] = v.x;
       acc[mb][rb][1] = v.y;
     }
@@ -194,7 +227,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
     for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
       for (int nb = 0; nb < NBK; ++nb) {
-        const double2 v = *reinterpret_cast<const double2*>(C1 + 8 * nb + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB);
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(C1 + 8 * nb + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB));
         c1n[mb][nb][0] = v.x;
         c1n[mb][nb][1] = v.y;
       }
@@ -205,9 +238,11 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
     hook(p);
     const int c0 = p * IB;
     const int q = p / P::PPG, cb = (p % P::PPG) * P::PW;
-    if (p % P::PPG == 0) mbar_wait(&bars[q], par);
-    const double* Vq = spk + q * P::GDBL;
-    const double* Tp = spk + P::TOFF + p * P::TP;
+    const int st = q % RG::NS;
+    if (p % P::PPG == 0) mbar_wait(&full[st], (q / RG::NS) & 1);
+    __syncwarp();  // reconverge (hook / refill / arrive are single-lane) before mma.sync.aligned
+    const double* Vq = spk + (size_t)st * RG::SD;
+    const double* Tp = Vq + P::GDBL + (p % P::PPG) * P::TP;
 
     // ---- step A: W^T = C1p^T + C2^T V_p ----------------------------------------
     double w[MB][NBK][2], w2[MB][NBK][2];
@@ -289,8 +324,8 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
         for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
           for (int nb = 0; nb < NBK; ++nb) {
-            const double2 v = *reinterpret_cast<const double2*>(C1 + c0 + IB + 8 * nb + 2 * t +
-                                                               (size_t)(wc0 + 8 * mb + g) * NB);
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(C1 + c0 + IB + 8 * nb + 2 * t +
+                                                                     (size_t)(wc0 + 8 * mb + g) * NB));
             c1n[mb][nb][0] = v.x;
             c1n[mb][nb][1] = v.y;
           }
@@ -319,6 +354,20 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ spk, u
           for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], w[mb][nb][s], bf);
         }
       }
+    if (RG::NS < P::NG && (p % P::PPG == P::PPG - 1 || p == P::NP - 1)) {
+      // group q done by this warp: release its stage; thread 0 refills it
+      // with group q + NS once every active warp has released it.  The proxy
+      // fence makes every lane's shared loads of the stage complete before the
+      // release: the refill is an async-proxy (TMA) write, which neither the
+      // arrive nor __syncwarp orders after generic loads still in flight
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (threadIdx.x == 0 && q + RG::NS < P::NG) {
+        mbar_wait(&empty[st], (q / RG::NS) & 1);
+        ring_issue<NB, IB, S>(gpk, spk, full, q + RG::NS);
+      }
+    }
   }
 
   // ---- registers -> C2 ----------------------------------------------------------
@@ -337,20 +386,29 @@ constexpr int kWarpsB = 8;  // warps per CTA of the batched v2 kernels (same geo
 __host__ __device__ constexpr int v2_mb(int NB) { return (NB == 96 || NB == 128) ? 2 : 1; }
 
 template <int NB, int IB>
-constexpr size_t v2_smem_bytes() { return (size_t)Pk<NB, IB>::TOTAL * sizeof(double); }
+constexpr size_t v2_smem_bytes() { return Ring<NB, IB, Pk<NB, IB>::NG>::bytes; }
+
+// warps of a CTA (W warps of 8*MB columns from col0) that own columns < NB
+template <int NB, int MB, int W>
+__device__ __forceinline__ int active_warps(int col0) {
+  const int a = (NB - col0 + 8 * MB - 1) / (8 * MB);
+  return a < 0 ? 0 : (a > W ? W : a);
+}
 
 // grid (slabs, batch): task b, columns [blockIdx.x * 64*MB, ...)
 template <int NB, int IB, bool LARFB>
 __global__ void __launch_bounds__(kWarpsB * 32, 1)
 update_v2_kernel(const double* const* Pkp, double* const* C1p, double* const* C2p) {
   constexpr int MB = v2_mb(NB);
+  constexpr int S = Pk<NB, IB>::NG;  // whole tile resident
   extern __shared__ __align__(128) double smem[];
-  __shared__ __align__(8) uint64_t bars[Pk<NB, IB>::NG];
+  __shared__ __align__(8) uint64_t full[S], empty[S];
   const int b = blockIdx.y;
-  if (threadIdx.x == 0) issue_packed_loads<NB, IB>(Pkp[b], smem, bars);
+  const int col0 = blockIdx.x * kWarpsB * 8 * MB;
+  if (threadIdx.x == 0) ring_start<NB, IB, S>(Pkp[b], smem, full, empty, active_warps<NB, MB, kWarpsB>(col0));
   __syncthreads();
-  update_v2_body<NB, IB, MB, LARFB, kWarpsB>(smem, bars, 0, LARFB ? nullptr : C1p[b], C2p[b],
-                                             blockIdx.x * kWarpsB * 8 * MB);
+  update_v2_body<NB, IB, MB, LARFB, kWarpsB, S>(Pkp[b], smem, full, empty, LARFB ? nullptr : C1p[b], C2p[b],
+                                                col0);
 }
 
 // grid (batch): standard V (NB x NB, GEQRT form if LARFB: unit lower

@@ -19,7 +19,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libtileqr.so")
+_LIB_PATH = os.environ.get("TILEQR_LIB") or os.path.join(_HERE, "libtileqr.so")
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"libtileqr.so not built ({_LIB_PATH}); run `python -m paper_1102_5328_b200.build`")

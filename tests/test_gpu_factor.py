@@ -204,3 +204,28 @@ def test_dataflow_kernel_equals_level_launcher(tq, monkeypatch, m, n, nb, ib, se
             assert int(info.item()) == 0
             assert torch.equal(A0, A1) and torch.equal(T0, T1)
     tq.finalize()
+
+
+@pytest.mark.parametrize("ib", [16, 32])
+def test_dataflow_kernel_stress_4096(tq, monkeypatch, ib):
+    """4096^2 at NB=128: ~24k work items, two CTAs per SM, ring refills of the
+    packed reflector tiles and pipelined panel sub-tasks all active.  The
+    dataflow result must equal the level-synchronous one bit for bit on every
+    run (this is the size at which a missing cross-proxy fence before the ring
+    refill showed up as sporadic corruption)."""
+    n, nb = 4096, 128
+    A0 = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    tq.rng_uniform(A0, n, n, seed=60)
+    tq.finalize()
+    monkeypatch.setenv("TILEQR_SCHED", "levels")
+    Ar = A0.clone()
+    Tr, _ = tq.factor(Ar, n, n, nb, ib)
+    tq.finalize()
+    monkeypatch.delenv("TILEQR_SCHED")
+    for _ in range(3):
+        A = A0.clone()
+        T, info = tq.factor(A, n, n, nb, ib)
+        torch.cuda.synchronize()
+        assert int(info.item()) == 0
+        assert torch.equal(A, Ar) and torch.equal(T, Tr)
+    tq.finalize()
