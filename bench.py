@@ -191,7 +191,7 @@ def measure_dag(tq, m, n, nb, ib, step, step_ms):
     step()
     import torch
     torch.cuda.synchronize()
-    dag_ms = tq.kernel_times(m, n, nb, ib, "dag")[0]
+    dag_ms, slots, _ = tq.kernel_times(m, n, nb, ib, "dag")   # slots = resident CTAs
     kinds = {"note": "dataflow kernel: per kind, items, busy ms summed over CTAs (inputs ready -> done), "
                      "one step after the timed region"}
     busy = {}
@@ -200,11 +200,12 @@ def measure_dag(tq, m, n, nb, ib, step, step_ms):
         busy[k] = tk
         kinds[k] = {"busy_ms_sum": round(tk, 3), "items": lk, "tasks": nk}
     tq.set_kernel_timing(False)
-    nsm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     s_tasks = kinds["ssrfb"]["tasks"]
+    # SSRFB rate while running: its flops over its CTA-time, scaled to all slots
     kinds["ssrfb"]["tflops_while_running"] = round(
-        s_tasks * 4.0 * nb ** 3 / (busy["ssrfb"] * 1e-3 / nsm) / 1e12, 3) if busy["ssrfb"] else None
-    kinds["sm_busy_frac"] = round(sum(busy.values()) / (nsm * dag_ms), 4) if dag_ms else None
+        s_tasks * 4.0 * nb ** 3 / (busy["ssrfb"] * 1e-3 / slots) / 1e12, 3) if busy["ssrfb"] else None
+    kinds["cta_slots"] = slots
+    kinds["slot_busy_frac"] = round(sum(busy.values()) / (slots * dag_ms), 4) if dag_ms else None
     flops = qr_flops(m, n)
     achieved = flops / (dag_ms * 1e-3) / 1e12 if dag_ms > 0 else 0.0
     roofline = {"kernel": "dag_kernel (persistent dataflow: GEQRT/TSQRT/LARFB/SSRFB items)",

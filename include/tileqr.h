@@ -250,7 +250,12 @@ int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out);
 void tileqr_set_kernel_timing(int mask);
 /* After the stream of a timed tileqr_factor(M, N, NB, IB) completed: sum of
  * the launch durations of kernel kind (0 GEQRT, 1 TSQRT, 2 LARFB, 3 SSRFB) in
- * the most recent run, the number of launches and of tasks. */
+ * the most recent run, the number of launches and of tasks.  Dataflow
+ * schedule ("dag", tileqr_factor_schedule): kinds 0-3 give the busy time of
+ * that kind's work items summed over CTAs (inputs ready -> completion), the
+ * number of items and of tasks; kind 4 gives the dataflow kernel's duration
+ * (CUDA events around its launch), h_launches = its resident CTAs and
+ * h_tasks = the DAG's task count. */
 int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
                         int64_t* h_launches, int64_t* h_tasks);
 

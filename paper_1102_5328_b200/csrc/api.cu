@@ -33,22 +33,22 @@ namespace tileqr {
 
 #define TQ_DECL_DAG(nb)                                                                        \
   int launch_dag_nb##nb(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm, \
-                        unsigned long long* prof, cudaStream_t s);
+                        unsigned long long* prof, cudaStream_t s, int* grid_out);
 TQ_DECL_DAG(32) TQ_DECL_DAG(64) TQ_DECL_DAG(96) TQ_DECL_DAG(128) TQ_DECL_DAG(160) TQ_DECL_DAG(192)
 TQ_DECL_DAG(224) TQ_DECL_DAG(256)
 #undef TQ_DECL_DAG
 
 static int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                      unsigned long long* prof, cudaStream_t s) {
+                      unsigned long long* prof, cudaStream_t s, int* grid_out) {
   switch (NB) {
-    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s);
-    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s);
-    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s);
-    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s);
-    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s);
-    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s);
-    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s);
-    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s);
+    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out);
     default: return TILEQR_ERR_CUDA;
   }
 }
@@ -167,6 +167,7 @@ struct FactorWS {
   unsigned long long* d_prof = nullptr;  // per-item claim/start/end (tileqr_set_kernel_timing)
   cudaEvent_t dag_ev[2] = {nullptr, nullptr};
   bool use_dag = false, dag_timed = false;
+  int dag_grid = 0;  // resident CTAs of the last DAG launch
   std::vector<unsigned char> item_kind;  // host copies for the diagnostics
   std::vector<int> item_info;            // per item: kind, k, m, n, sub-task / slab column
   std::vector<int> item_level;
@@ -291,7 +292,10 @@ static int build_dag(FactorWS* ws) {
   }
   // weights (ns, rough B200 per-SM durations): update work at ~150 GFLOP/s
   // per SM, panel latency ~1.2 us per column
-  const double wS = 4.0 * NB * NB * NB / 150.0, wL = wS / 2, wP = 1200.0 * NB / NS;
+  double wS = 4.0 * NB * NB * NB / 150.0, wP = 1200.0 * NB / NS;
+  if (const char* e = getenv("TILEQR_DAG_WS")) wS *= atof(e);  // diagnostics: priority weights
+  if (const char* e = getenv("TILEQR_DAG_WP")) wP *= atof(e);
+  const double wL = wS / 2;
   auto weight = [&](int kind) { return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : wP; };
   std::vector<int> byLevel(ntask);
   {
@@ -308,17 +312,108 @@ static int build_dag(FactorWS* ws) {
     bl[i] = weight(tk[i].kind) + succ[i];
     for (int d = 0; d < tk[i].ndep; ++d) succ[tk[i].dep[d]] = std::max(succ[tk[i].dep[d]], bl[i]);
   }
-  std::vector<int> order(ntask);
-  for (int64_t i = 0; i < ntask; ++i) order[i] = (int)i;
-  std::sort(order.begin(), order.end(), [&](int a, int b) {
-    if (bl[a] != bl[b]) return bl[a] > bl[b];
-    if (tk[a].level != tk[b].level) return tk[a].level < tk[b].level;
-    if (tk[a].s != tk[b].s) return tk[a].s < tk[b].s;
-    return a < b;
-  });
   const int cols = dag::dag_cols(NB);
   const int nslab = (NB + cols - 1) / cols;
   auto parts = [&](int kind) { return (kind == dag::kLarfb || kind == dag::kSsrfb) ? nslab : 1; };
+
+  // Claim order: a list schedule simulated on the host -- P workers (the
+  // resident CTAs), rough per-item durations, ready items started in bottom-
+  // level order -- and the items sorted by their simulated start time.  A
+  // CTA that claims an item blocks until its inputs are final, so claiming in
+  // an order the DAG can actually keep up with avoids head-of-line blocking
+  // (pure bottom-level order parks hundreds of CTAs on far-future items while
+  // the first panels run).  Start times respect dependencies strictly, so the
+  // order is topological (deadlock-free claiming).
+  int dev0 = 0, nsm0 = 0;
+  TQ_CUDA(cudaGetDevice(&dev0));
+  TQ_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0));
+  const int P = std::max(1, nsm0 * dag::dag_ctas_per_sm(NB));
+  const double cta_gflops = 220.0 / dag::dag_ctas_per_sm(NB);       // update rate per CTA
+  const double dS = 4.0 * NB * NB * cols / cta_gflops;               // ns per SSRFB slab
+  // measured in the dataflow kernel at NB = 128 (10000^2): TSQRT sub-task
+  // ~2 us per column, GEQRT sub-task ~3.4 us per column (both sharing their SM
+  // with an update CTA), LARFB slab ~0.77 of an SSRFB slab; plus ~3 us of
+  // hand-off (release -> acquire -> operand loads) per item
+  double sT = 3000.0, sG = 5000.0, hand = 5000.0;
+  if (dag::dag_ctas_per_sm(NB) == 1) sT = sG = 1500.0;  // a panel item has its SM alone
+  if (const char* e = getenv("TILEQR_DAG_SIM")) sscanf(e, "%lf,%lf,%lf", &sT, &sG, &hand);  // diagnostics
+  const double dL = 0.77 * dS + hand, dT = sT * SC + hand, dG = sG * SC + hand;
+  auto dur = [&](int kind) {
+    return kind == dag::kSsrfb ? dS + hand : kind == dag::kLarfb ? dL : kind == dag::kTsqrt ? dT : dG;
+  };
+  std::vector<int64_t> soff(ntask + 1, 0);  // successors (CSR)
+  for (int64_t i = 0; i < ntask; ++i)
+    for (int d = 0; d < tk[i].ndep; ++d) ++soff[tk[i].dep[d] + 1];
+  for (int64_t i = 0; i < ntask; ++i) soff[i + 1] += soff[i];
+  std::vector<int> succ_l(soff[ntask]);
+  {
+    std::vector<int64_t> fill(soff.begin(), soff.end() - 1);
+    for (int64_t i = 0; i < ntask; ++i)
+      for (int d = 0; d < tk[i].ndep; ++d) succ_l[fill[tk[i].dep[d]]++] = (int)i;
+  }
+  std::vector<int> indeg(ntask), left(ntask);
+  for (int64_t i = 0; i < ntask; ++i) {
+    indeg[i] = tk[i].ndep;
+    left[i] = parts(tk[i].kind);
+  }
+  struct Rd { double bl; int level, s, task, slab; };
+  auto rd_less = [](const Rd& a, const Rd& b) {  // max-heap on priority
+    if (a.bl != b.bl) return a.bl < b.bl;
+    if (a.level != b.level) return a.level > b.level;
+    if (a.s != b.s) return a.s > b.s;
+    if (a.task != b.task) return a.task > b.task;
+    return a.slab > b.slab;
+  };
+  std::vector<Rd> ready;
+  auto push_task = [&](int i) {
+    for (int sl = 0; sl < parts(tk[i].kind); ++sl) {
+      ready.push_back({bl[i], tk[i].level, tk[i].s, i, sl});
+      std::push_heap(ready.begin(), ready.end(), rd_less);
+    }
+  };
+  for (int64_t i = 0; i < ntask; ++i)
+    if (indeg[i] == 0) push_task((int)i);
+  struct Ev { double t; int task; };
+  auto ev_greater = [](const Ev& a, const Ev& b) { return a.t > b.t; };
+  std::vector<Ev> events;
+  struct Slot { double start; double bl; int task, slab; };
+  std::vector<Slot> sched;
+  sched.reserve((size_t)(nG + nT) + (size_t)(nL + nS) * nslab);
+  double now = 0.0;
+  int freew = P;
+  while (!ready.empty() || !events.empty()) {
+    while (freew > 0 && !ready.empty()) {
+      std::pop_heap(ready.begin(), ready.end(), rd_less);
+      const Rd r = ready.back();
+      ready.pop_back();
+      sched.push_back({now, r.bl, r.task, r.slab});
+      events.push_back({now + dur(tk[r.task].kind), r.task});
+      std::push_heap(events.begin(), events.end(), ev_greater);
+      --freew;
+    }
+    if (events.empty()) break;
+    std::pop_heap(events.begin(), events.end(), ev_greater);
+    const Ev e = events.back();
+    events.pop_back();
+    now = e.t;
+    ++freew;
+    if (--left[e.task] == 0)
+      for (int64_t q = soff[e.task]; q < soff[e.task + 1]; ++q)
+        if (--indeg[succ_l[q]] == 0) push_task(succ_l[q]);
+  }
+  if ((int64_t)sched.size() != nG + nT + (nL + nS) * (int64_t)nslab) {
+    set_error("tileqr_factor: internal error in the DAG schedule simulation");
+    return TILEQR_ERR_CUDA;
+  }
+  const char* ord = getenv("TILEQR_DAG_ORDER");  // diagnostics: "bl" = pure bottom-level order
+  if (ord && strcmp(ord, "bl") == 0)
+    std::stable_sort(sched.begin(), sched.end(), [&](const Slot& a, const Slot& b) {
+      if (a.bl != b.bl) return a.bl > b.bl;
+      if (a.task != b.task) return a.task < b.task;
+      return a.slab < b.slab;
+    });
+  else
+    std::stable_sort(sched.begin(), sched.end(), [](const Slot& a, const Slot& b) { return a.start < b.start; });
   const size_t tile = (size_t)NB * NB;
   double* A = ws->tiles;
   double* Tw = ws->Tws;
@@ -326,13 +421,15 @@ static int build_dag(FactorWS* ws) {
   auto tt = [&](int64_t m, int64_t k) { return Tw + (size_t)(m + k * MT) * IB * NB; };
   auto pkp = [&](int64_t m, int64_t k) { return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr; };
   std::vector<dag::Item> items;
-  items.reserve(nG + nT + (size_t)(nL + nS) * nslab);
-  for (int i : order) {
+  items.reserve(sched.size());
+  for (const Slot& sl : sched) {
+    const int i = sl.task;
     const Task& t = tk[i];
     dag::Item it{};
     it.kind = t.kind;
     it.task = i;
     if (t.kind == dag::kGeqrt || t.kind == dag::kTsqrt) it.col0 = (t.s * SC) | ((t.s + 1) * SC) << 16;
+    else it.col0 = sl.slab * cols;
     it.ndep = t.ndep;
     for (int d = 0; d < t.ndep; ++d) {
       it.dep[d] = t.dep[d];
@@ -351,13 +448,10 @@ static int build_dag(FactorWS* ws) {
         it.pk = pkp(t.m, t.k);
         break;
     }
-    for (int sl = 0; sl < parts(t.kind); ++sl) {
-      if (parts(t.kind) > 1 || t.kind == dag::kLarfb || t.kind == dag::kSsrfb) it.col0 = sl * cols;
-      items.push_back(it);
-      ws->item_kind.push_back((unsigned char)t.kind);
-      for (int v : {t.kind, t.k, t.m, t.n, (t.kind >= dag::kLarfb) ? it.col0 : t.s}) ws->item_info.push_back(v);
-      ws->item_level.push_back(t.level);
-    }
+    items.push_back(it);
+    ws->item_kind.push_back((unsigned char)t.kind);
+    ws->item_level.push_back(t.level);
+    for (int v : {t.kind, t.k, t.m, t.n, (t.kind >= dag::kLarfb) ? it.col0 : t.s}) ws->item_info.push_back(v);
   }
   ws->nitems = (int)items.size();
   ws->ntasks = (int)ntask;
@@ -388,7 +482,8 @@ static int run_dag(FactorWS* ws, cudaStream_t stream) {
     const long v = atol(e);
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
-  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, nitems, ws->d_ctr, ws->d_ctr + 1, ws->nsm, prof, stream);
+  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, nitems, ws->d_ctr, ws->d_ctr + 1, ws->nsm, prof, stream,
+                      &ws->dag_grid);
   if (rc) return rc;
   if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
   ws->dag_timed = g_timing != 0;
@@ -696,7 +791,10 @@ static int run_levels(FactorWS* ws, cudaStream_t stream) {
 
 }  // namespace tileqr
 
-namespace tileqr { int panel_prof_read(unsigned long long* out, int reset); }
+namespace tileqr {
+int panel_prof_read(unsigned long long* out, int reset);
+int panel_prof_read_dag128(unsigned long long* out, int reset);
+}
 using namespace tileqr;
 
 extern "C" {
@@ -992,6 +1090,10 @@ int tileqr_debug_dag_item(int64_t M, int64_t N, int NB, int IB, int64_t idx, int
 
 // Diagnostic (not in the header): accumulated phase cycles of the fast panel kernel.
 int tileqr_debug_panel_prof(unsigned long long* out, int reset) { return tileqr::panel_prof_read(out, reset); }
+// Diagnostic: the same counters of the panel bodies inside the NB=128 DAG kernel.
+int tileqr_debug_dag_panel_prof(unsigned long long* out, int reset) {
+  return tileqr::panel_prof_read_dag128(out, reset);
+}
 
 const char* tileqr_factor_schedule(int NB, int IB) {
   if (!valid_nb_ib(NB, IB)) return "invalid";
@@ -1058,11 +1160,11 @@ int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* 
       set_error("tileqr_kernel_times: the last run was not timed");
       return TILEQR_ERR_NOT_INIT;
     }
-    if (kind == 4) {
+    if (kind == 4) {  // the kernel: duration, launches = resident CTAs (work-item slots), tasks
       float ms = 0.f;
       TQ_CUDA(cudaEventElapsedTime(&ms, ws->dag_ev[0], ws->dag_ev[1]));
       *h_total_ms = ms;
-      *h_launches = 1;
+      *h_launches = ws->dag_grid;
       *h_tasks = ws->ntasks;
       return 0;
     }

@@ -191,12 +191,12 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     };
     switch (it.kind) {
       case kGeqrt:  // inner panels [col0 & 0xffff, col0 >> 16)
-        pf::panel_fast_body<false, NB, W>(IB, it.p[0], nullptr, it.p[2],
+        pf::panel_fast_body<false, NB, W, KW>(it.p[0], nullptr, it.p[2],
                                                reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
                                                it.col0 & 0xffff, it.col0 >> 16);
         break;
       case kTsqrt:
-        pf::panel_fast_body<true, NB, W>(IB, it.p[0], it.p[1], it.p[2],
+        pf::panel_fast_body<true, NB, W, KW>(it.p[0], it.p[1], it.p[2],
                                               reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
                                               it.col0 & 0xffff, it.col0 >> 16);
         break;
@@ -230,7 +230,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
 
 template <int NB, int KW>
 int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                 unsigned long long* prof, cudaStream_t s) {
+                 unsigned long long* prof, cudaStream_t s, int* grid_out) {
   auto kern = dag_kernel<NB, KW>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
@@ -248,6 +248,7 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
     const int g = atoi(e);
     if (g > 0 && g < grid) grid = g;
   }
+  if (grid_out) *grid_out = grid;
   kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof);
   TQ_LAUNCH_CHECK();
   return 0;
@@ -255,15 +256,15 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
 
 template <int NB>
 int launch_dag_nb(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                  unsigned long long* prof, cudaStream_t s) {
+                  unsigned long long* prof, cudaStream_t s, int* grid_out) {
   switch (IB) {
-    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s);
-    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s);
+    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
     case 24:
-      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s);
+      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
       set_error("DAG kernel: IB does not divide NB");
       return TILEQR_ERR_CUDA;
-    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s);
+    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
     default: set_error("DAG kernel: IB not in {8,16,24,32}"); return TILEQR_ERR_CUDA;
   }
 }

@@ -9,8 +9,13 @@ namespace dag {
 // shared-memory ring): 2 CTAs of 4 warps per SM, so one CTA's item prologue,
 // epilogue and dependency waits overlap the other's DMMA work.  NB > 128:
 // 1 CTA of 8 warps per SM.
+#ifdef TILEQR_DAG_ONE_CTA  // build variant: one 8-warp CTA per SM for every NB
+__host__ __device__ constexpr int dag_warps(int) { return 8; }
+__host__ __device__ constexpr int dag_ctas_per_sm(int) { return 1; }
+#else
 __host__ __device__ constexpr int dag_warps(int NB) { return NB <= 128 ? 4 : 8; }
 __host__ __device__ constexpr int dag_ctas_per_sm(int NB) { return NB <= 128 ? 2 : 1; }
+#endif
 
 enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3 };
 

@@ -14,23 +14,37 @@ __device__ unsigned long long g_panel_prof[16];  // phase cycles; filled only wi
 namespace {
 using pf::FastSmem;
 
-template <bool TS, int NB, int kWarps>
+template <bool TS, int NB, int kWarps, int IB>
 __global__ void __launch_bounds__(kWarps * 32, 1)
-panel_fast_kernel(int IB, double* const* Rp, double* const* Bp, double* const* Tp, double* const* Pk) {
+panel_fast_kernel(double* const* Rp, double* const* Bp, double* const* Tp, double* const* Pk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  pf::panel_fast_body<TS, NB, kWarps>(IB, Rp[blockIdx.x], TS ? Bp[blockIdx.x] : nullptr, Tp[blockIdx.x],
-                                      smem_raw, Pk ? Pk[blockIdx.x] : nullptr);
+  pf::panel_fast_body<TS, NB, kWarps, IB>(Rp[blockIdx.x], TS ? Bp[blockIdx.x] : nullptr, Tp[blockIdx.x],
+                                          smem_raw, Pk ? Pk[blockIdx.x] : nullptr);
+}
+
+template <bool TS, int NB, int NW, int IB>
+int launch_fast_i(int batch, double* const* R, double* const* B, double* const* T, cudaStream_t s,
+                  double* const* Pk) {
+  auto kern = panel_fast_kernel<TS, NB, NW, IB>;
+  const size_t bytes = sizeof(FastSmem<NB, NW>);
+  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  kern<<<batch, NW * 32, bytes, s>>>(R, B, T, Pk);
+  TQ_LAUNCH_CHECK();
+  return 0;
 }
 
 template <bool TS, int NB, int NW>
 int launch_fast_w(int IB, int batch, double* const* R, double* const* B, double* const* T,
                   cudaStream_t s, double* const* Pk) {
-  auto kern = panel_fast_kernel<TS, NB, NW>;
-  const size_t bytes = sizeof(FastSmem<NB, NW>);
-  TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  kern<<<batch, NW * 32, bytes, s>>>(IB, R, B, T, Pk);
-  TQ_LAUNCH_CHECK();
-  return 0;
+  switch (IB) {
+    case 8: return launch_fast_i<TS, NB, NW, 8>(batch, R, B, T, s, Pk);
+    case 16: return launch_fast_i<TS, NB, NW, 16>(batch, R, B, T, s, Pk);
+    case 24:
+      if constexpr (NB % 24 == 0) return launch_fast_i<TS, NB, NW, 24>(batch, R, B, T, s, Pk);
+      return -1;
+    case 32: return launch_fast_i<TS, NB, NW, 32>(batch, R, B, T, s, Pk);
+    default: return -1;
+  }
 }
 
 // Warps per panel CTA: the DAG kernel's geometry for this NB (dag_item.h),

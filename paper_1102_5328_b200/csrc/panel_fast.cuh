@@ -59,13 +59,15 @@ struct FastSmem {
   double Ws[kWarps][8 * LDW];
 };
 
-template <bool TS, int NB, int kWarps>
 // Inner panels c0 = cbeg, cbeg+IB, ... < cend (the whole tile by default; the
 // DAG kernel runs a TSQRT / GEQRT as several sub-tasks of consecutive inner
 // panels, every state between them lives in global memory).
-__device__ __forceinline__ void panel_fast_body(int IB, double* const R, double* const Bx, double* const Tg,
+template <bool TS, int NB, int kWarps, int IB>
+__device__ __forceinline__ void panel_fast_body(double* const R, double* const Bx, double* const Tg,
                                                 unsigned char* smem_raw, double* const Vpk = nullptr,
                                                 int cbeg = 0, int cend = NB) {
+  static_assert(IB % 8 == 0 && IB <= 32 && NB % IB == 0, "fast panel geometry");
+  constexpr int TR = IB / kWarps > 0 ? IB / kWarps : 1;  // GEQRT: top rows per warp
   constexpr int kThreads = kWarps * 32;
   constexpr int RW = NB / kWarps;  // rows per warp in the factorization
   constexpr int RB = NB / 8;       // 8-row blocks in the trailing update
@@ -116,37 +118,44 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
       }
     }
     __syncthreads();
+    // Registers: lane = column, warp w holds rows [w*RW, (w+1)*RW) in x[].
+    // GEQRT: the IB rows [c0, c0+IB) of the diagonal block -- the rows that
+    // leave the reflector one per step -- are held separately, row c0+i in
+    // top[i / W] of warp i % W, so that every step's row bookkeeping is a
+    // compile-time index (the step loop is unrolled); x[] holds only the rows
+    // below, which stay in every reflector of the panel.
     double x[RW];
 #pragma unroll
-    for (int q = 0; q < RW; ++q)  // GEQRT: rows above the panel (R of earlier panels) stay out
-      x[q] = (lane < IB && (TS || warp * RW + q >= c0)) ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
+    for (int q = 0; q < RW; ++q)
+      x[q] = (lane < IB && (TS || warp * RW + q >= c0 + IB)) ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
+    double top[TR];
+#pragma unroll
+    for (int t = 0; t < TR; ++t) {
+      const int i = t * kWarps + warp;
+      top[t] = (!TS && lane < IB && i < IB) ? S.Vs[vsw(c0 + i, lane, LDV)] : 0.0;
+    }
 
     TQ_PHASE(0);
     // ---- 1. factor the panel column by column --------------------------------
-    int buf = 0;
-    for (int jj = 0; jj < IB; ++jj) {
-      const int j = c0 + jj;
-      if (!TS && warp == j / RW) {
-        // GEQRT: row j leaves the reflector rows.  Its values go to smem (alpha
-        // and the R(j, c) inputs) and the registers of lanes >= jj are zeroed, so
-        // every R row sits as 0 in the registers: the dots and the rank-1 update
-        // below then run over all rows with no masks (rows < j hold 0 in the
-        // pivot column, lanes < jj keep their V entries of row j).
-        double rv = 0.0;
 #pragma unroll
-        for (int q = 0; q < RW; ++q)
-          if (warp * RW + q == j) {
-            rv = x[q];
-            if (lane >= jj) x[q] = 0.0;
-          }
-        S.rowj[buf][lane] = rv;
-      }
+    for (int jj = 0; jj < IB; ++jj) {
+      const int buf = jj & 1;
+      if (!TS && warp == jj % kWarps) S.rowj[buf][lane] = top[jj / kWarps];  // row j: alpha, R(j, c)
       double vj[RW];
       double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
 #pragma unroll
       for (int q = 0; q < RW; ++q) {
         vj[q] = __shfl_sync(0xffffffffu, x[q], jj);
         pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
+      }
+      double vt[TR];
+      if (!TS) {  // top rows below row j (warp-uniform predicate per slot)
+#pragma unroll
+        for (int t = 0; t < TR; ++t) {
+          vt[t] = __shfl_sync(0xffffffffu, top[t], jj);
+          if (t * kWarps + warp <= jj) vt[t] = 0.0;
+          pp[t & 3] = fma(vt[t], top[t], pp[t & 3]);
+        }
       }
       S.red[buf][warp][lane] = (pp[0] + pp[1]) + (pp[2] + pp[3]);
       __syncthreads();
@@ -199,17 +208,28 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
       const double coef = (lane == jj) ? scal - 1.0 : (lane > jj ? -tw * scal : 0.0);
 #pragma unroll
       for (int q = 0; q < RW; ++q) x[q] = fma(coef, vj[q], x[q]);
+      if (!TS) {
+#pragma unroll
+        for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t]);  // vt == 0 on rows <= j
+      }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
       if (warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
       if (tid == 0) S.tau[jj] = tau;
-      buf ^= 1;
     }
     __syncthreads();  // everyone done reading Vs (panel values) and red
     TQ_PHASE(1);
 
     // ---- write the factored panel: registers -> smem -> global (coalesced) ----
 #pragma unroll
-    for (int q = 0; q < RW; ++q) S.Vs[vsw(warp * RW + q, lane, LDV)] = lane < IB ? x[q] : 0.0;
+    for (int q = 0; q < RW; ++q)  // GEQRT: the top rows come from top[] below
+      if (TS || warp * RW + q >= c0 + IB) S.Vs[vsw(warp * RW + q, lane, LDV)] = lane < IB ? x[q] : 0.0;
+    if (!TS) {
+#pragma unroll
+      for (int t = 0; t < TR; ++t) {
+        const int i = t * kWarps + warp;
+        if (i < IB) S.Vs[vsw(c0 + i, lane, LDV)] = lane < IB ? top[t] : 0.0;
+      }
+    }
     __syncthreads();
     for (int idx = tid; idx < NB * IB; idx += kThreads) {
       const int c = idx / NB, r = idx - c * NB;
@@ -309,14 +329,7 @@ __device__ __forceinline__ void panel_fast_body(int IB, double* const R, double*
     if constexpr (NB <= 128) if (Vpk) {  // packed copy of V_p / T_p for the barrier-free update (update_v2.cuh)
       auto vf = [&](int r, int i) { return S.Vs[vsw(r, i, LDV)]; };
       auto tf = [&](int l, int i) { return S.Ts[l + i * LDT]; };
-      switch (IB) {
-        case 8: v2::pack_panel<NB, 8, kThreads>(Vpk, c0 / IB, vf, tf); break;
-        case 16: v2::pack_panel<NB, 16, kThreads>(Vpk, c0 / IB, vf, tf); break;
-        case 24:
-          if constexpr (NB % 24 == 0) v2::pack_panel<NB, 24, kThreads>(Vpk, c0 / IB, vf, tf);
-          break;
-        case 32: v2::pack_panel<NB, 32, kThreads>(Vpk, c0 / IB, vf, tf); break;
-      }
+      v2::pack_panel<NB, IB, kThreads>(Vpk, c0 / IB, vf, tf);
     }
     __syncthreads();
     TQ_PHASE(3);

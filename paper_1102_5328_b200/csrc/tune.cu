@@ -191,13 +191,16 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   double* buf = nullptr;
   double** ptrs = nullptr;
+  double* pkbuf = nullptr;  // packed reflector tiles of the step-1 batch
+  double** pkp = nullptr;
+  size_t pk_cap = 0;
   double* A0 = nullptr;
   double* A = nullptr;
   double* T = nullptr;
   int* dinfo = nullptr;
   auto cleanup = [&]() {
     if (s) cudaStreamSynchronize(s);
-    cudaFree(buf); cudaFree(ptrs); cudaFree(A0); cudaFree(A); cudaFree(T); cudaFree(dinfo);
+    cudaFree(buf); cudaFree(ptrs); cudaFree(pkbuf); cudaFree(pkp); cudaFree(A0); cudaFree(A); cudaFree(T); cudaFree(dinfo);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (s) cudaStreamDestroy(s);
@@ -209,7 +212,8 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   // ---- Step 1: SSRFB sweep ---------------------------------------------------
   const size_t tile_max = (size_t)nbmax * nbmax;
   if (cudaMalloc(&buf, (size_t)batch * (4 * tile_max + tile_max) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&ptrs, (size_t)batch * 5 * sizeof(double*)) != cudaSuccess) {
+      cudaMalloc(&ptrs, (size_t)batch * 5 * sizeof(double*)) != cudaSuccess ||
+      cudaMalloc(&pkp, (size_t)batch * sizeof(double*)) != cudaSuccess) {
     cudaGetLastError();
     set_error("tileqr_tune: step-1 allocation failed");
     cleanup();
@@ -234,12 +238,34 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
       // V2, T from a TSQRT of (top, bottom); fresh bottoms each time are not
       // needed for timing: the reflector values only scale the data.
       TQ_TRY(launch_tsqrt(nb, ib, batch, ptrs, ptrs + batch, ptrs + 4 * batch, s));
-      TQ_TRY(launch_ssrfb(true, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, ptrs + 2 * batch,
-                          ptrs + 3 * batch, nb, s));  // warm-up
+      // Time the kernel tileqr_factor runs for this (NB, IB): the packed-
+      // reflector update (operands packed once, outside the timing) where
+      // available, else the staged DMMA / SIMT update.
+      const bool pk = v2_supported(nb, ib);
+      if (pk) {
+        const size_t pd = v2_pk_doubles(nb, ib);
+        if (pd > pk_cap) {
+          cudaFree(pkbuf);
+          pkbuf = nullptr;
+          if (cudaMalloc(&pkbuf, pd * batch * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            set_error("tileqr_tune: step-1 packed buffer allocation failed");
+            cleanup();
+            return TILEQR_ERR_ALLOC;
+          }
+          pk_cap = pd;
+        }
+        TQ_TRY(launch_fill_ptrs(pkp, pkbuf, pd, batch, s));
+        TQ_TRY(launch_pack(false, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, pkp, s));
+      }
+      auto one = [&]() -> int {
+        if (pk) return launch_update_pk(false, nb, ib, batch, pkp, ptrs + 2 * batch, ptrs + 3 * batch, s);
+        return launch_ssrfb(true, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, ptrs + 2 * batch,
+                            ptrs + 3 * batch, nb, s);
+      };
+      TQ_TRY(one());  // warm-up
       TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
-      for (int r = 0; r < reps; ++r)
-        TQ_TRY(launch_ssrfb(true, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, ptrs + 2 * batch,
-                            ptrs + 3 * batch, nb, s));
+      for (int r = 0; r < reps; ++r) TQ_TRY(one());
       TQ_TRY(cudaEventRecord(e1, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
       TQ_TRY(cudaEventSynchronize(e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
       float ms = 0.f;
@@ -252,6 +278,10 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   }
   cudaFree(buf);
   buf = nullptr;
+  cudaFree(pkbuf);
+  pkbuf = nullptr;
+  cudaFree(pkp);
+  pkp = nullptr;
   std::vector<Pt> cand = preselect(samples, heuristic, 8);
 
   // ---- Step 2: factorizations on a ladder ascending to N --------------------

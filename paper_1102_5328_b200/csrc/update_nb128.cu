@@ -12,8 +12,8 @@ int launch_update_nb128(bool trans, bool larfb, int IB, int batch, const double*
   return upd::launch_update_dmma<128>(trans, larfb, IB, batch, V, T, C1, C2, ncols, s);
 }
 int launch_dag_nb128(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                     unsigned long long* prof, cudaStream_t s) {
-  return dag::launch_dag_nb<128>(IB, items, nitems, next, done, nsm, prof, s);
+                     unsigned long long* prof, cudaStream_t s, int* grid_out) {
+  return dag::launch_dag_nb<128>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
 }
 int launch_update_pk_nb128(bool larfb, int IB, int batch, const double* const* Pk, double* const* C1,
                           double* const* C2, cudaStream_t s) {
@@ -22,5 +22,20 @@ int launch_update_pk_nb128(bool larfb, int IB, int batch, const double* const* P
 int launch_pack_nb128(bool larfb, int IB, int batch, const double* const* V, const double* const* T,
                      double* const* Pk, cudaStream_t s) {
   return v2::launch_pack<128>(larfb, IB, batch, V, T, Pk, s);
+}
+int panel_prof_read_dag128(unsigned long long* out, int reset) {
+#ifdef TILEQR_PANEL_PROF
+  TQ_CUDA(cudaMemcpyFromSymbol(out, g_panel_prof, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {};
+    TQ_CUDA(cudaMemcpyToSymbol(g_panel_prof, z, sizeof z));
+  }
+  return 0;
+#else
+  (void)out;
+  (void)reset;
+  set_error("diagnostic counters need the TILEQR_BUILD_VARIANT=prof library");
+  return TILEQR_ERR_NOT_INIT;
+#endif
 }
 }  // namespace tileqr
