@@ -459,7 +459,7 @@ static int build_dag(FactorWS* ws) {
   TQ_CUDA(cudaGetDevice(&dev));
   TQ_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, dev));
   if (cudaMalloc(&ws->d_items, std::max<size_t>(items.size(), 1) * sizeof(dag::Item)) != cudaSuccess ||
-      cudaMalloc(&ws->d_ctr, (size_t)(ntask + 1) * sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&ws->d_ctr, (size_t)(ntask + 257) * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     set_error("tileqr_factor: device allocation of the DAG work list failed");
     return TILEQR_ERR_ALLOC;
@@ -470,7 +470,7 @@ static int build_dag(FactorWS* ws) {
 }
 
 static int run_dag(FactorWS* ws, cudaStream_t stream) {
-  TQ_CUDA(cudaMemsetAsync(ws->d_ctr, 0, (size_t)(ws->ntasks + 1) * sizeof(int), stream));
+  TQ_CUDA(cudaMemsetAsync(ws->d_ctr, 0, (size_t)(ws->ntasks + 257) * sizeof(int), stream));
   unsigned long long* prof = nullptr;
   if (g_timing) {
     if (!ws->d_prof) TQ_CUDA(cudaMalloc(&ws->d_prof, (size_t)ws->nitems * 3 * sizeof(unsigned long long)));
@@ -482,7 +482,8 @@ static int run_dag(FactorWS* ws, cudaStream_t stream) {
     const long v = atol(e);
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
-  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, nitems, ws->d_ctr, ws->d_ctr + 1, ws->nsm, prof, stream,
+  // counters: [claim cursor | 256 per-SM panel flags | one per task]
+  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, nitems, ws->d_ctr, ws->d_ctr + 257, ws->nsm, prof, stream,
                       &ws->dag_grid);
   if (rc) return rc;
   if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
