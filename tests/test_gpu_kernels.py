@@ -150,3 +150,63 @@ def test_rng_matches_synth_inputs(tq):
     tq.rng_uniform(buf, m, n, seed=4, offset=123, lda=310)
     got = buf.cpu().numpy().T[:m, :]
     assert np.array_equal(got, si.uniform(m, n, 4, offset=123))  # bit-exact
+
+
+PACKED = [(nb, ib) for nb in (32, 64, 96, 128) for ib in (8, 16, 24, 32) if nb % ib == 0]
+
+
+@pytest.mark.parametrize("nb,ib", PACKED)
+@pytest.mark.parametrize("larfb", [False, True])
+def test_packed_update_batched(tq, nb, ib, larfb):
+    """The factorization's update kernel (packed reflector tiles, TMA-staged,
+    barrier-free DMMA; update_v2.cuh) through tileqr_pack_batched +
+    tileqr_update_packed_batched, against the oracle's SSRFB / LARFB (Q^T)."""
+    assert tq.packed_size(nb, ib) > 0
+    vs, ts = [], []
+    for x, y in zip(seeds(nb, ib, 11), seeds(nb, ib, 12)):
+        if larfb:
+            v, t = oracle.geqrt(x, ib)
+        else:
+            _, v, t = oracle.tsqrt(np.triu(x), y, ib)
+        vs.append(v)
+        ts.append(t)
+    c1, c2 = seeds(nb, ib, 13), seeds(nb, ib, 14)
+    vb, vp = dev_tiles(vs)
+    tb, tp = dev_tiles(ts)
+    c1b, c1p = dev_tiles(c1)
+    c2b, c2p = dev_tiles(c2)
+    pk = torch.zeros(BATCH * tq.packed_size(nb, ib), dtype=torch.float64, device="cuda")
+    pp = torch.arange(BATCH, dtype=torch.int64, device="cuda") * tq.packed_size(nb, ib) * 8 + pk.data_ptr()
+    tq.pack_batched(larfb, nb, ib, vp, tp, pp)
+    tq.update_packed_batched(larfb, nb, ib, pp, None if larfb else c1p, c2p)
+    torch.cuda.synchronize()
+    for i in range(BATCH):
+        if larfb:
+            o2 = oracle.larfb(vs[i], ts[i], c2[i], "T")
+            assert nrel(host(c2b[i]), o2) < tol(nb), i
+            assert np.array_equal(host(c1b[i]), c1[i])  # C1 untouched by the LARFB form
+        else:
+            o1, o2 = oracle.ssrfb(vs[i], ts[i], c1[i], c2[i], "T")
+            assert nrel(host(c1b[i]), o1) < tol(nb), i
+            assert nrel(host(c2b[i]), o2) < tol(nb), i
+
+
+def test_packed_layout_is_a_permutation_of_v_and_t(tq):
+    """The packed tile holds exactly the entries of V (unit lower trapezoid for
+    the GEQRT form) and the upper triangles of the T_p blocks, nothing else."""
+    nb, ib = 64, 16
+    x = seeds(nb, ib, 15)[0]
+    v, t = oracle.geqrt(x, ib)
+    vb, vp = dev_tiles([v])
+    tb, tp = dev_tiles([t])
+    n = tq.packed_size(nb, ib)
+    pk = torch.full((n,), 12345.0, dtype=torch.float64, device="cuda")
+    pp = torch.tensor([pk.data_ptr()], dtype=torch.int64, device="cuda")
+    tq.pack_batched(True, nb, ib, vp, tp, pp)
+    torch.cuda.synchronize()
+    got = np.sort(pk.cpu().numpy())
+    vu = np.tril(v, -1) + np.eye(nb)                       # GEQRT reflectors, unit diagonal
+    tt = [np.triu(t[:, p * ib:(p + 1) * ib]) for p in range(nb // ib)]
+    want_nonzero = np.sort(np.concatenate([vu[vu != 0]] + [b[b != 0] for b in tt]))
+    assert not np.any(got == 12345.0)                       # every slot written
+    assert np.array_equal(got[got != 0], want_nonzero)
