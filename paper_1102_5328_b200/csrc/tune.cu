@@ -185,6 +185,11 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   const char* e_reps = getenv("TILEQR_TUNE_REPS");
   const int reps = e_reps ? atoi(e_reps) : 50;
   const int nb_grid[] = {64, 96, 128, 160, 192, 224, 256};
+  // TILEQR_TUNE_FLUSH=1: Step 1 with an L2 flush before every timed call
+  const char* e_flush = getenv("TILEQR_TUNE_FLUSH");
+  const bool flush = e_flush && e_flush[0] == '1';
+  const size_t flush_bytes = (size_t)512 << 20;  // 4x the 126 MB L2
+  void* flushbuf = nullptr;
   const int nbmax = 256;
 
   cudaStream_t s = nullptr;
@@ -200,12 +205,13 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   int* dinfo = nullptr;
   auto cleanup = [&]() {
     if (s) cudaStreamSynchronize(s);
-    cudaFree(buf); cudaFree(ptrs); cudaFree(pkbuf); cudaFree(pkp); cudaFree(A0); cudaFree(A); cudaFree(T); cudaFree(dinfo);
+    cudaFree(buf); cudaFree(ptrs); cudaFree(pkbuf); cudaFree(pkp); cudaFree(flushbuf); cudaFree(A0); cudaFree(A); cudaFree(T); cudaFree(dinfo);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (s) cudaStreamDestroy(s);
   };
   TQ_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+  if (flush) TQ_TRY(cudaMalloc(&flushbuf, flush_bytes) == cudaSuccess ? 0 : TILEQR_ERR_ALLOC);
   TQ_TRY(cudaEventCreate(&e0) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
   TQ_TRY(cudaEventCreate(&e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
 
@@ -264,12 +270,26 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
                             ptrs + 3 * batch, nb, s);
       };
       TQ_TRY(one());  // warm-up
-      TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
-      for (int r = 0; r < reps; ++r) TQ_TRY(one());
-      TQ_TRY(cudaEventRecord(e1, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
-      TQ_TRY(cudaEventSynchronize(e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, e0, e1);
+      if (!flush) {  // No Flush: reps back-to-back calls timed at once
+        TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        for (int r = 0; r < reps; ++r) TQ_TRY(one());
+        TQ_TRY(cudaEventRecord(e1, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        TQ_TRY(cudaEventSynchronize(e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+        cudaEventElapsedTime(&ms, e0, e1);
+      } else {  // flushed (the MultCallFlushLRU idea): every call
+                // timed alone after overwriting a buffer larger than L2
+        for (int r = 0; r < reps; ++r) {
+          TQ_TRY(cudaMemsetAsync(flushbuf, r & 0xff, flush_bytes, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+          TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+          TQ_TRY(one());
+          TQ_TRY(cudaEventRecord(e1, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+          TQ_TRY(cudaEventSynchronize(e1) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
+          float m1 = 0.f;
+          cudaEventElapsedTime(&m1, e0, e1);
+          ms += m1;
+        }
+      }
       const double g = (double)reps * batch * 4.0 * nb * nb * (double)nb / (ms * 1e-3) / 1e9;
       samples.push_back({nb, ib, g});
       // keep magnitudes bounded across the repeated in-place updates
@@ -363,8 +383,8 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   if (report_json_path) {
     FILE* f = fopen(report_json_path, "w");
     if (f) {
-      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d,\n",
-              (long long)M, (long long)N, heuristic, payg, batch, reps);
+      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d, \"step1_timing\": \"%s\",\n",
+              (long long)M, (long long)N, heuristic, payg, batch, reps, flush ? "flush" : "no_flush");
       fprintf(f, " \"step1\": %s,\n \"candidates\": %s,\n \"step2\": %s,\n \"best\": {\"nb\": %d, \"ib\": %d, \"gflops\": %.3f}}\n",
               pts_json(samples).c_str(), pts_json(cand).c_str(), step2.c_str(), best.nb, best.ib, best.g);
       fclose(f);
