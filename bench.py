@@ -311,22 +311,20 @@ def run_tileqr(args, rank, world, local_rank):
     else:
         roofline, kinds = measure_levels(tq, m, n, nb, ib, step, ms)
 
-    # e2e: same metric through the public API with host buffers (pinned), H2D of
-    # the input and D2H of the result (R/V and T) inside the timed region
+    # e2e: same metric through the public host-buffer API (tileqr_factor_host):
+    # pinned host A in, R/V and T back to pinned host buffers, the copies
+    # overlapped with the factorization inside the call; every step moves the
+    # whole input in and the whole result out inside the timed region
     e2e = None
     if not args.no_e2e:
         hA = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         hA.copy_(A0)
         hR = torch.empty_like(hA, pin_memory=True)
         hT = torch.empty(T.numel(), dtype=torch.float64, pin_memory=True)
-        dA = torch.empty_like(A0)
         e2e_steps = max(1, min(args.steps, 3))
 
         def step_e2e():
-            dA.copy_(hA, non_blocking=True)
-            tq.factor(dA, m, n, nb, ib, T=T, info=info)
-            hR.copy_(dA, non_blocking=True)
-            hT.copy_(T, non_blocking=True)
+            tq.factor_host(hA, m, n, nb, ib, hR=hR, hT=hT, info=info)
 
         step_e2e()
         torch.cuda.synchronize()
@@ -338,7 +336,8 @@ def run_tileqr(args, rank, world, local_rank):
         ms_e2e = e0.elapsed_time(e1) / e2e_steps
         e2e = {"value": flops / (ms_e2e * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": hA.numel() * 8, "d2h_bytes_per_step": (hR.numel() + hT.numel()) * 8,
-               "ms_per_step": ms_e2e, "steps": e2e_steps}
+               "ms_per_step": ms_e2e, "steps": e2e_steps,
+               "api": "tileqr_factor_host (copies overlapped with the dataflow kernel)"}
 
     cpu = None
     if not args.no_cpu_baseline:

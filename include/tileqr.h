@@ -83,6 +83,29 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
                   int* d_info, tileqr_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * tileqr_factor_host -- tileqr_factor for a matrix in HOST memory, with the
+ * host<->device transfers overlapped with the factorization (the user-facing
+ * end-to-end call).
+ *
+ *   h_A [in]  host, M x N, lda >= max(1, M); read column tile by column tile
+ *             by the copy engine while the factorization runs (the dataflow
+ *             kernel's LOAD items convert each column tile as it lands).
+ *   h_R [out] host, M x N, ldr >= max(1, M): the tileqr_factor output (R and
+ *             V as there); may alias h_A (each column is read before it is
+ *             written).  Column tiles are copied back as soon as the
+ *             factorization has finished them (STORE items + stream waits).
+ *   h_T [out] host, tileqr_t_size() doubles, the T factors.
+ *   d_info [out] device int (may be NULL), as tileqr_factor.
+ *   Stream-ordered: the host buffers must stay valid until `stream` completes;
+ *   page-locked buffers give the full overlap (pageable ones serialise the
+ *   copies with the host thread).  (NB, IB) outside the dataflow set: copy
+ *   in, tileqr_factor, copy out, without overlap.
+ *   Errors: -1 M, -2 N, -3 h_A, -4 lda, -5 NB, -6 IB, -7 h_R, -8 ldr, -9 h_T.
+ * ------------------------------------------------------------------------ */
+int tileqr_factor_host(int64_t M, int64_t N, const double* h_A, int64_t lda, int NB, int IB, double* h_R,
+                       int64_t ldr, double* h_T, int* d_info, tileqr_stream_t stream);
+
+/* ------------------------------------------------------------------------
  * tileqr_apply_qt -- B <- Q^T B (trans = 'T') or B <- Q B (trans = 'N') with
  * the Q of a tileqr_factor output:
  *   'T': k ascending: LARFB(k) on B's row-tile k, then SSRFB(k,m) on row-tiles

@@ -13,6 +13,7 @@
 // streams.  The whole level sequence is captured once per shape into a CUDA
 // graph and replayed (the GPU counterpart of PLASMA's static schedule,
 // PAPER.md:163-164).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -33,22 +34,24 @@ namespace tileqr {
 
 #define TQ_DECL_DAG(nb)                                                                        \
   int launch_dag_nb##nb(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm, \
-                        unsigned long long* prof, cudaStream_t s, int* grid_out);
+                        unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO& io,  \
+                        long long MT, double* tiles);
 TQ_DECL_DAG(32) TQ_DECL_DAG(64) TQ_DECL_DAG(96) TQ_DECL_DAG(128) TQ_DECL_DAG(160) TQ_DECL_DAG(192)
 TQ_DECL_DAG(224) TQ_DECL_DAG(256)
 #undef TQ_DECL_DAG
 
 static int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                      unsigned long long* prof, cudaStream_t s, int* grid_out) {
+                      unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO& io,
+                      long long MT, double* tiles) {
   switch (NB) {
-    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
     default: return TILEQR_ERR_CUDA;
   }
 }
@@ -136,6 +139,21 @@ static void build_tasks(int64_t MT, int64_t NT, HostTasks& h, int64_t nlev) {
   for (int64_t t = 0; t < nlev; ++t) h.S[t].insert(h.S[t].end(), Sb[t].begin(), Sb[t].end());
 }
 
+// One work list of the dataflow kernel (items in claim order + counters).
+struct DagList {
+  dag::Item* d_items = nullptr;
+  int nitems = 0, ntasks = 0, nio = 0;
+  int64_t id_ld = 0, id_st = 0, id_ar = 0;  // first LOAD / STORE / ARRIVE task (host pipeline)
+  int* d_ctr = nullptr;                     // [claim cursor | 256 per-SM flags | one per task]
+  std::vector<unsigned char> item_kind;     // host copies for the diagnostics
+  std::vector<int> item_info;               // per item: kind, k, m, n, sub-task / slab column
+  std::vector<int> item_level;
+  ~DagList() {
+    cudaFree(d_items);
+    cudaFree(d_ctr);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Workspace of one factorization shape
 // ---------------------------------------------------------------------------
@@ -160,17 +178,21 @@ struct FactorWS {
   std::vector<cudaEvent_t> ev;
   cudaGraphExec_t graph = nullptr;
   int graph_timed = 0;
-  // dataflow DAG kernel (dag.cuh): items in claim order, counters [next | done per task]
-  dag::Item* d_items = nullptr;
-  int nitems = 0, ntasks = 0, nsm = 0;
-  int* d_ctr = nullptr;
+  // dataflow DAG kernel (dag.cuh): two work lists -- device input
+  // (tileqr_factor) and host input with LOAD/STORE items (tileqr_factor_host)
+  DagList dag_plain, dag_io;
+  DagList* dag_last = nullptr;           // list of the most recent run (diagnostics)
+  int nsm = 0;
   unsigned long long* d_prof = nullptr;  // per-item claim/start/end (tileqr_set_kernel_timing)
+  size_t prof_cap = 0;
   cudaEvent_t dag_ev[2] = {nullptr, nullptr};
   bool use_dag = false, dag_timed = false;
   int dag_grid = 0;  // resident CTAs of the last DAG launch
-  std::vector<unsigned char> item_kind;  // host copies for the diagnostics
-  std::vector<int> item_info;            // per item: kind, k, m, n, sub-task / slab column
-  std::vector<int> item_level;
+  // host pipeline (tileqr_factor_host): column-major staging, copy streams
+  double* st_in = nullptr;
+  double* st_out = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t io_ev[3] = {nullptr, nullptr, nullptr};
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
   struct Rec { int kind; int64_t tasks; int64_t level; cudaEvent_t a, b; };
   int64_t cur_level = 0;
@@ -185,11 +207,14 @@ struct FactorWS {
     cudaFree(tiles);
     cudaFree(Tws);
     cudaFree(dptr);
-    cudaFree(d_items);
     cudaFree(Vpk);
-    cudaFree(d_ctr);
     cudaFree(d_prof);
+    cudaFree(st_in);
+    cudaFree(st_out);
     for (auto e : dag_ev) if (e) cudaEventDestroy(e);
+    for (auto e : io_ev) if (e) cudaEventDestroy(e);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
   }
 };
 
@@ -236,7 +261,7 @@ static int panel_sub_cols(int NB, int IB) {
 // weighted path to the end of the DAG) descending -- a topological order,
 // since a task's bottom level exceeds each successor's -- ties by ASAP level,
 // then task id.
-static int build_dag(FactorWS* ws) {
+static int build_dag(FactorWS* ws, bool io) {
   const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT);
   const int NB = ws->NB, IB = ws->IB;
   const int SC = panel_sub_cols(NB, IB), NS = NB / SC;
@@ -247,7 +272,12 @@ static int build_dag(FactorWS* ws) {
     offT[k] = nT; nT += (MT - k - 1) * NS;
     offS[k] = nS; nS += (MT - k - 1) * (NT - k - 1);
   }
-  const int64_t ntask = nG + nL + nT + nS;
+  const int64_t ntask0 = nG + nL + nT + nS;        // the factorization's tasks
+  // host pipeline: LOAD(n), STORE(n), ARRIVE(n) per tile column n (the copy
+  // engine lands the input column block by column block: contiguous copies
+  // run at the link's rate, strided row blocks of NB doubles measured ~30 %
+  // slower in total)
+  const int64_t ntask = ntask0 + (io ? 3 * NT : 0);
   if (ntask > (int64_t)1 << 30) {
     set_error("tileqr_factor: DAG too large for the dataflow kernel");
     return TILEQR_ERR_ALLOC;
@@ -258,6 +288,10 @@ static int build_dag(FactorWS* ws) {
   auto idS = [&](int64_t k, int64_t m, int64_t n) {
     return nG + nL + nT + offS[k] + (m - k - 1) * (NT - k - 1) + (n - k - 1);
   };
+  auto idLD = [&](int64_t n) { return ntask0 + n; };
+  auto idST = [&](int64_t n) { return ntask0 + NT + n; };
+  auto idAR = [&](int64_t n) { return ntask0 + 2 * NT + n; };
+  constexpr int kArrive = 6;  // host-only pseudo kind: set by the copy stream
   struct Task { int kind; int k, m, n; int level; int ndep; int dep[3]; int s; };
   std::vector<Task> tk(ntask);
   for (int64_t k = 0; k < KT; ++k) {
@@ -265,12 +299,14 @@ static int build_dag(FactorWS* ws) {
       Task g{dag::kGeqrt, (int)k, (int)k, (int)k, (int)(3 * k), 0, {0, 0, 0}, sub};
       if (sub > 0) g.dep[g.ndep++] = (int)idG(k, sub - 1);
       else if (k > 0) g.dep[g.ndep++] = (int)idS(k - 1, k, k);
+      else if (io) g.dep[g.ndep++] = (int)idLD(0);
       tk[idG(k, sub)] = g;
     }
     for (int64_t n = k + 1; n < NT; ++n) {
       Task l{dag::kLarfb, (int)k, (int)k, (int)n, (int)(3 * k + 1), 0, {0, 0, 0}, 0};
       l.dep[l.ndep++] = (int)idG(k, NS - 1);
       if (k > 0) l.dep[l.ndep++] = (int)idS(k - 1, k, n);
+      else if (io) l.dep[l.ndep++] = (int)idLD(n);
       tk[idL(k, n)] = l;
     }
     for (int64_t m = k + 1; m < MT; ++m) {
@@ -290,31 +326,79 @@ static int build_dag(FactorWS* ws) {
       }
     }
   }
-  // weights (ns, rough B200 per-SM durations): update work at ~150 GFLOP/s
-  // per SM, panel latency ~1.2 us per column
-  double wS = 4.0 * NB * NB * NB / 150.0, wP = 1200.0 * NB / NS;
-  if (const char* e = getenv("TILEQR_DAG_WS")) wS *= atof(e);  // diagnostics: priority weights
-  if (const char* e = getenv("TILEQR_DAG_WP")) wP *= atof(e);
-  const double wL = wS / 2;
-  auto weight = [&](int kind) { return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : wP; };
-  std::vector<int> byLevel(ntask);
-  {
-    int maxl = 0;
-    for (const Task& t : tk) maxl = std::max(maxl, t.level);
-    std::vector<int64_t> cnt(maxl + 2, 0);
-    for (const Task& t : tk) ++cnt[t.level + 1];
-    for (int l = 0; l <= maxl; ++l) cnt[l + 1] += cnt[l];
-    for (int64_t i = 0; i < ntask; ++i) byLevel[cnt[tk[i].level]++] = (int)i;
-  }
-  std::vector<double> bl(ntask, 0.0), succ(ntask, 0.0);
-  for (int64_t q = ntask - 1; q >= 0; --q) {  // reverse topological (successors sit at higher levels)
-    const int i = byLevel[q];
-    bl[i] = weight(tk[i].kind) + succ[i];
-    for (int d = 0; d < tk[i].ndep; ++d) succ[tk[i].dep[d]] = std::max(succ[tk[i].dep[d]], bl[i]);
+  if (io) {
+    const int last_level = (int)num_levels(MT, NT);
+    for (int64_t n = 0; n < NT; ++n) {
+      tk[idAR(n)] = Task{kArrive, 0, 0, (int)n, 0, 0, {0, 0, 0}, 0};
+      Task ld{dag::kLoad, 0, 0, (int)n, 0, 0, {0, 0, 0}, 0};
+      ld.dep[ld.ndep++] = (int)idAR(n);
+      tk[idLD(n)] = ld;
+      // the last task writing tile column n (its chain implies every earlier writer)
+      int64_t last;
+      if (n < KT) last = (MT > n + 1) ? idT(n, MT - 1, NS - 1) : idG(n, NS - 1);
+      else last = (MT > KT) ? idS(KT - 1, MT - 1, n) : idL(KT - 1, n);
+      Task st{dag::kStore, 0, 0, (int)n, last_level, 0, {0, 0, 0}, 0};
+      st.dep[st.ndep++] = (int)last;
+      tk[idST(n)] = st;
+    }
   }
   const int cols = dag::dag_cols(NB);
   const int nslab = (NB + cols - 1) / cols;
-  auto parts = [&](int kind) { return (kind == dag::kLarfb || kind == dag::kSsrfb) ? nslab : 1; };
+  constexpr int kIoTiles = 8;  // tiles per LOAD / STORE item
+  const int nld = (int)((MT + kIoTiles - 1) / kIoTiles), nst = nld;
+  auto parts = [&](int kind) {
+    if (kind == dag::kLarfb || kind == dag::kSsrfb) return nslab;
+    if (kind == dag::kLoad) return nld;
+    if (kind == dag::kStore) return nst;
+    return 1;
+  };
+  // successors (CSR) and a topological order (Kahn)
+  std::vector<int64_t> soff(ntask + 1, 0);
+  for (int64_t i = 0; i < ntask; ++i)
+    for (int d = 0; d < tk[i].ndep; ++d) ++soff[tk[i].dep[d] + 1];
+  for (int64_t i = 0; i < ntask; ++i) soff[i + 1] += soff[i];
+  std::vector<int> succ_l(soff[ntask]);
+  {
+    std::vector<int64_t> fill(soff.begin(), soff.end() - 1);
+    for (int64_t i = 0; i < ntask; ++i)
+      for (int d = 0; d < tk[i].ndep; ++d) succ_l[fill[tk[i].dep[d]]++] = (int)i;
+  }
+  std::vector<int> topo;
+  topo.reserve(ntask);
+  {
+    std::vector<int> indeg(ntask);
+    for (int64_t i = 0; i < ntask; ++i) {
+      indeg[i] = tk[i].ndep;
+      if (indeg[i] == 0) topo.push_back((int)i);
+    }
+    for (size_t q = 0; q < topo.size(); ++q)
+      for (int64_t e = soff[topo[q]]; e < soff[topo[q] + 1]; ++e)
+        if (--indeg[succ_l[e]] == 0) topo.push_back(succ_l[e]);
+    if ((int64_t)topo.size() != ntask) {
+      set_error("tileqr_factor: internal error: the task graph has a cycle");
+      return TILEQR_ERR_CUDA;
+    }
+  }
+  // bottom levels (priority of ready items in the simulation below)
+  double wS = 4.0 * NB * NB * NB / 150.0, wP = 1200.0 * NB / NS;
+  if (const char* e = getenv("TILEQR_DAG_WS")) wS *= atof(e);  // diagnostics: priority weights
+  if (const char* e = getenv("TILEQR_DAG_WP")) wP *= atof(e);
+  const double wL = wS / 2, wIO = 10000.0;
+  auto weight = [&](int kind) {
+    return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : kind == kArrive ? 0.0
+         : (kind == dag::kLoad || kind == dag::kStore) ? wIO : wP;
+  };
+  std::vector<double> bl(ntask, 0.0);
+  for (int64_t q = ntask - 1; q >= 0; --q) {
+    const int i = topo[q];
+    double mx = 0.0;
+    for (int64_t e = soff[i]; e < soff[i + 1]; ++e) mx = std::max(mx, bl[succ_l[e]]);
+    bl[i] = weight(tk[i].kind) + mx;
+  }
+  // LOAD / STORE items start as soon as they are ready: they gate everything
+  // downstream (LOAD) or the device-to-host copy (STORE) and are cheap
+  for (int64_t i = ntask0; i < ntask; ++i)
+    if (tk[i].kind == dag::kLoad || tk[i].kind == dag::kStore) bl[i] = 1e30;
 
   // Claim order: a list schedule simulated on the host -- P workers (the
   // resident CTAs), rough per-item durations, ready items started in bottom-
@@ -323,7 +407,8 @@ static int build_dag(FactorWS* ws) {
   // an order the DAG can actually keep up with avoids head-of-line blocking
   // (pure bottom-level order parks hundreds of CTAs on far-future items while
   // the first panels run).  Start times respect dependencies strictly, so the
-  // order is topological (deadlock-free claiming).
+  // order is topological (deadlock-free claiming).  ARRIVE pseudo-tasks (host
+  // pipeline) complete at the time their column's copy is expected to land.
   int dev0 = 0, nsm0 = 0;
   TQ_CUDA(cudaGetDevice(&dev0));
   TQ_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0));
@@ -338,19 +423,17 @@ static int build_dag(FactorWS* ws) {
   if (dag::dag_ctas_per_sm(NB) == 1) sT = sG = 1500.0;  // a panel item has its SM alone
   if (const char* e = getenv("TILEQR_DAG_SIM")) sscanf(e, "%lf,%lf,%lf", &sT, &sG, &hand);  // diagnostics
   const double dL = 0.77 * dS + hand, dT = sT * SC + hand, dG = sG * SC + hand;
+  const double dIO = 1.0e3 + (double)kIoTiles * NB * NB * 16 / 50.0;  // ~50 GB/s per CTA
+  const double tcol = (double)MT * NB * NB * 8 / 45.0;                  // ~45 GB/s host link
   auto dur = [&](int kind) {
-    return kind == dag::kSsrfb ? dS + hand : kind == dag::kLarfb ? dL : kind == dag::kTsqrt ? dT : dG;
+    switch (kind) {
+      case dag::kSsrfb: return dS + hand;
+      case dag::kLarfb: return dL;
+      case dag::kTsqrt: return dT;
+      case dag::kGeqrt: return dG;
+      default: return dIO;
+    }
   };
-  std::vector<int64_t> soff(ntask + 1, 0);  // successors (CSR)
-  for (int64_t i = 0; i < ntask; ++i)
-    for (int d = 0; d < tk[i].ndep; ++d) ++soff[tk[i].dep[d] + 1];
-  for (int64_t i = 0; i < ntask; ++i) soff[i + 1] += soff[i];
-  std::vector<int> succ_l(soff[ntask]);
-  {
-    std::vector<int64_t> fill(soff.begin(), soff.end() - 1);
-    for (int64_t i = 0; i < ntask; ++i)
-      for (int d = 0; d < tk[i].ndep; ++d) succ_l[fill[tk[i].dep[d]]++] = (int)i;
-  }
   std::vector<int> indeg(ntask), left(ntask);
   for (int64_t i = 0; i < ntask; ++i) {
     indeg[i] = tk[i].ndep;
@@ -371,14 +454,20 @@ static int build_dag(FactorWS* ws) {
       std::push_heap(ready.begin(), ready.end(), rd_less);
     }
   };
-  for (int64_t i = 0; i < ntask; ++i)
-    if (indeg[i] == 0) push_task((int)i);
-  struct Ev { double t; int task; };
+  struct Ev { double t; int task; bool worker; };
   auto ev_greater = [](const Ev& a, const Ev& b) { return a.t > b.t; };
   std::vector<Ev> events;
+  for (int64_t i = 0; i < ntask; ++i) {
+    if (indeg[i] != 0) continue;
+    if (tk[i].kind == kArrive) {  // completes without a worker when its copy lands
+      events.push_back({tcol * (tk[i].n + 1), (int)i, false});
+      std::push_heap(events.begin(), events.end(), ev_greater);
+    } else {
+      push_task((int)i);
+    }
+  }
   struct Slot { double start; double bl; int task, slab; };
   std::vector<Slot> sched;
-  sched.reserve((size_t)(nG + nT) + (size_t)(nL + nS) * nslab);
   double now = 0.0;
   int freew = P;
   while (!ready.empty() || !events.empty()) {
@@ -387,7 +476,7 @@ static int build_dag(FactorWS* ws) {
       const Rd r = ready.back();
       ready.pop_back();
       sched.push_back({now, r.bl, r.task, r.slab});
-      events.push_back({now + dur(tk[r.task].kind), r.task});
+      events.push_back({now + dur(tk[r.task].kind), r.task, true});
       std::push_heap(events.begin(), events.end(), ev_greater);
       --freew;
     }
@@ -396,12 +485,15 @@ static int build_dag(FactorWS* ws) {
     const Ev e = events.back();
     events.pop_back();
     now = e.t;
-    ++freew;
-    if (--left[e.task] == 0)
+    if (e.worker) ++freew;
+    if (--left[e.task] <= 0)
       for (int64_t q = soff[e.task]; q < soff[e.task + 1]; ++q)
         if (--indeg[succ_l[q]] == 0) push_task(succ_l[q]);
   }
-  if ((int64_t)sched.size() != nG + nT + (nL + nS) * (int64_t)nslab) {
+  int64_t nitems_expect = 0;
+  for (int64_t i = 0; i < ntask; ++i)
+    if (tk[i].kind != kArrive) nitems_expect += parts(tk[i].kind);
+  if ((int64_t)sched.size() != nitems_expect) {
     set_error("tileqr_factor: internal error in the DAG schedule simulation");
     return TILEQR_ERR_CUDA;
   }
@@ -420,8 +512,12 @@ static int build_dag(FactorWS* ws) {
   auto tp = [&](int64_t m, int64_t n) { return A + (size_t)(m + n * MT) * tile; };
   auto tt = [&](int64_t m, int64_t k) { return Tw + (size_t)(m + k * MT) * IB * NB; };
   auto pkp = [&](int64_t m, int64_t k) { return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr; };
+  DagList& L = io ? ws->dag_io : ws->dag_plain;
   std::vector<dag::Item> items;
   items.reserve(sched.size());
+  L.item_kind.clear();
+  L.item_level.clear();
+  L.item_info.clear();
   for (const Slot& sl : sched) {
     const int i = sl.task;
     const Task& t = tk[i];
@@ -443,52 +539,76 @@ static int build_dag(FactorWS* ws) {
       case dag::kLarfb:
         it.p[0] = tp(t.k, t.k); it.p[1] = tt(t.k, t.k); it.p[2] = tp(t.k, t.n); it.pk = pkp(t.k, t.k);
         break;
+      case dag::kLoad:   // tiles (m, n), m in the item's row range
+      case dag::kStore:
+        it.aux[0] = t.n;
+        it.aux[1] = t.n + 1;
+        it.aux[2] = sl.slab * kIoTiles;
+        it.aux[3] = (int)std::min<int64_t>(MT, (int64_t)(sl.slab + 1) * kIoTiles);
+        break;
       default:
         it.p[0] = tp(t.m, t.k); it.p[1] = tt(t.m, t.k); it.p[2] = tp(t.k, t.n); it.p[3] = tp(t.m, t.n);
         it.pk = pkp(t.m, t.k);
         break;
     }
     items.push_back(it);
-    ws->item_kind.push_back((unsigned char)t.kind);
-    ws->item_level.push_back(t.level);
-    for (int v : {t.kind, t.k, t.m, t.n, (t.kind >= dag::kLarfb) ? it.col0 : t.s}) ws->item_info.push_back(v);
+    L.item_kind.push_back((unsigned char)t.kind);
+    L.item_level.push_back(t.level);
+    for (int v : {t.kind, t.k, t.m, t.n, (t.kind >= dag::kLarfb) ? it.col0 : t.s}) L.item_info.push_back(v);
   }
-  ws->nitems = (int)items.size();
-  ws->ntasks = (int)ntask;
+  L.nitems = (int)items.size();
+  L.ntasks = (int)ntask;
+  L.nio = nst;
+  L.id_ld = ntask0;
+  L.id_st = ntask0 + NT;
+  L.id_ar = ntask0 + 2 * NT;
   int dev = 0;
   TQ_CUDA(cudaGetDevice(&dev));
   TQ_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, dev));
-  if (cudaMalloc(&ws->d_items, std::max<size_t>(items.size(), 1) * sizeof(dag::Item)) != cudaSuccess ||
-      cudaMalloc(&ws->d_ctr, (size_t)(ntask + 257) * sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&L.d_items, std::max<size_t>(items.size(), 1) * sizeof(dag::Item)) != cudaSuccess ||
+      cudaMalloc(&L.d_ctr, (size_t)(ntask + 257) * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     set_error("tileqr_factor: device allocation of the DAG work list failed");
     return TILEQR_ERR_ALLOC;
   }
-  TQ_CUDA(cudaMemcpy(ws->d_items, items.data(), items.size() * sizeof(dag::Item), cudaMemcpyHostToDevice));
-  for (auto& e : ws->dag_ev) TQ_CUDA(cudaEventCreate(&e));
+  TQ_CUDA(cudaMemcpy(L.d_items, items.data(), items.size() * sizeof(dag::Item), cudaMemcpyHostToDevice));
+  if (!ws->dag_ev[0])
+    for (auto& e : ws->dag_ev) TQ_CUDA(cudaEventCreate(&e));
   return 0;
 }
 
-static int run_dag(FactorWS* ws, cudaStream_t stream) {
-  TQ_CUDA(cudaMemsetAsync(ws->d_ctr, 0, (size_t)(ws->ntasks + 257) * sizeof(int), stream));
+static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO& io, cudaStream_t stream) {
   unsigned long long* prof = nullptr;
   if (g_timing) {
-    if (!ws->d_prof) TQ_CUDA(cudaMalloc(&ws->d_prof, (size_t)ws->nitems * 3 * sizeof(unsigned long long)));
+    if (ws->prof_cap < (size_t)L.nitems) {
+      cudaFree(ws->d_prof);
+      ws->d_prof = nullptr;
+      TQ_CUDA(cudaMalloc(&ws->d_prof, (size_t)L.nitems * 3 * sizeof(unsigned long long)));
+      ws->prof_cap = L.nitems;
+    }
     prof = ws->d_prof;
     TQ_CUDA(cudaEventRecord(ws->dag_ev[0], stream));
   }
-  int nitems = ws->nitems;
+  int nitems = L.nitems;
   if (const char* e = getenv("TILEQR_DAG_NITEMS")) {  // diagnostics: run a prefix of the claim order
     const long v = atol(e);
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
-  // counters: [claim cursor | 256 per-SM panel flags | one per task]
-  int rc = launch_dag(ws->NB, ws->IB, ws->d_items, nitems, ws->d_ctr, ws->d_ctr + 257, ws->nsm, prof, stream,
-                      &ws->dag_grid);
+  int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, ws->nsm, prof, stream,
+                      &ws->dag_grid, io, ws->MT, ws->tiles);
   if (rc) return rc;
   if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
   ws->dag_timed = g_timing != 0;
+  ws->dag_last = &L;
   return 0;
+}
+
+static int run_dag(FactorWS* ws, cudaStream_t stream) {
+  DagList& L = ws->dag_plain;
+  // counters: [claim cursor | 256 per-SM panel flags | one per task]
+  TQ_CUDA(cudaMemsetAsync(L.d_ctr, 0, (size_t)(L.ntasks + 257) * sizeof(int), stream));
+  dag::DagIO io{ws->M, ws->N, ws->M, nullptr, nullptr, nullptr};
+  return run_dag_list(ws, L, io, stream);
 }
 
 static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** out) {
@@ -613,7 +733,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
   for (auto& e : ws->ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   ws->use_dag = dag_enabled(NB, IB);
   if (ws->use_dag) {
-    int rc = build_dag(ws.get());
+    int rc = build_dag(ws.get(), false);
     if (rc) return rc;
   }
   *out = ws.get();
@@ -790,6 +910,104 @@ static int run_levels(FactorWS* ws, cudaStream_t stream) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline (tileqr_factor_host)
+// ---------------------------------------------------------------------------
+using PFN_streamValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_streamValue32 g_wait_value = nullptr, g_write_value = nullptr;
+
+// cuStreamWaitValue32 / cuStreamWriteValue32 through the runtime's driver
+// entry points (no link dependency on libcuda).
+static int stream_value_ops() {
+  if (g_wait_value && g_write_value) return 0;
+  void* f1 = nullptr;
+  void* f2 = nullptr;
+  cudaDriverEntryPointQueryResult q1 = cudaDriverEntryPointSymbolNotFound, q2 = q1;
+  TQ_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", &f1, cudaEnableDefault, &q1));
+  TQ_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &f2, cudaEnableDefault, &q2));
+  if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !f1 || !f2) {
+    set_error("tileqr_factor_host: stream memory operations unavailable");
+    return TILEQR_ERR_CUDA;
+  }
+  g_wait_value = reinterpret_cast<PFN_streamValue32>(f1);
+  g_write_value = reinterpret_cast<PFN_streamValue32>(f2);
+  return 0;
+}
+
+#define TQ_CU(call)                                                         \
+  do {                                                                      \
+    CUresult r_ = (call);                                                   \
+    if (r_ != CUDA_SUCCESS) {                                               \
+      set_error("tileqr_factor_host: stream memory operation failed");      \
+      return TILEQR_ERR_CUDA;                                               \
+    }                                                                       \
+  } while (0)
+
+static int factor_host_dag(FactorWS* ws, const double* hA, int64_t lda, double* hR, int64_t ldr, double* hT,
+                           int* d_info, cudaStream_t s) {
+  const int64_t M = ws->M, N = ws->N, MT = ws->MT, NT = ws->NT;
+  const int NB = ws->NB, IB = ws->IB;
+  DagList& L = ws->dag_io;
+  if (!L.d_items) {
+    int rc = build_dag(ws, true);
+    if (rc) return rc;
+  }
+  if (int rc = stream_value_ops()) return rc;
+  if (!ws->st_in) {
+    if (cudaMalloc(&ws->st_in, (size_t)M * N * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&ws->st_out, (size_t)M * N * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("tileqr_factor_host: device allocation of the staging buffers failed");
+      return TILEQR_ERR_ALLOC;
+    }
+    TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_h2d, cudaStreamNonBlocking));
+    TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_d2h, cudaStreamNonBlocking));
+    for (auto& e : ws->io_ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  int* ctr = L.d_ctr;
+  TQ_CUDA(cudaMemsetAsync(ctr, 0, (size_t)(L.ntasks + 257) * sizeof(int), s));
+  TQ_CUDA(cudaEventRecord(ws->io_ev[0], s));
+  TQ_CUDA(cudaStreamWaitEvent(ws->s_h2d, ws->io_ev[0], 0));
+  TQ_CUDA(cudaStreamWaitEvent(ws->s_d2h, ws->io_ev[0], 0));
+  auto counter = [&](int64_t task) { return (CUdeviceptr)(uintptr_t)(ctr + 257 + task); };
+  // copy engine, host -> device: one tile column at a time (contiguous when
+  // lda == M), each followed by its ARRIVE counter (the LOAD items of that
+  // column wait on it)
+  for (int64_t n = 0; n < NT; ++n) {
+    const int64_t c0 = n * NB, nc = std::min<int64_t>(NB, N - c0);
+    if (lda == M)
+      TQ_CUDA(cudaMemcpyAsync(ws->st_in + c0 * M, hA + c0 * lda, (size_t)M * nc * sizeof(double),
+                              cudaMemcpyHostToDevice, ws->s_h2d));
+    else
+      TQ_CUDA(cudaMemcpy2DAsync(ws->st_in + c0 * M, M * sizeof(double), hA + c0 * lda, lda * sizeof(double),
+                                M * sizeof(double), nc, cudaMemcpyHostToDevice, ws->s_h2d));
+    TQ_CU(g_write_value((CUstream)ws->s_h2d, counter(L.id_ar + n), 1, CU_STREAM_WRITE_VALUE_DEFAULT));
+  }
+  // the factorization, with LOAD / STORE items
+  dag::DagIO io{M, N, M, ws->st_in, ws->st_out, d_info};
+  if (int rc = run_dag_list(ws, L, io, s)) return rc;
+  // copy engine, device -> host: each tile column as soon as its STORE items
+  // are done (and with it that column of T)
+  for (int64_t n = 0; n < NT; ++n) {
+    const int64_t c0 = n * NB, nc = std::min<int64_t>(NB, N - c0);
+    TQ_CU(g_wait_value((CUstream)ws->s_d2h, counter(L.id_st + n), (cuuint32_t)L.nio, CU_STREAM_WAIT_VALUE_GEQ));
+    if (ldr == M)
+      TQ_CUDA(cudaMemcpyAsync(hR + c0 * ldr, ws->st_out + c0 * M, (size_t)M * nc * sizeof(double),
+                              cudaMemcpyDeviceToHost, ws->s_d2h));
+    else
+      TQ_CUDA(cudaMemcpy2DAsync(hR + c0 * ldr, ldr * sizeof(double), ws->st_out + c0 * M, M * sizeof(double),
+                                M * sizeof(double), nc, cudaMemcpyDeviceToHost, ws->s_d2h));
+    const size_t tcol = (size_t)MT * IB * NB;
+    TQ_CUDA(cudaMemcpyAsync(hT + n * tcol, ws->Tws + n * tcol, tcol * sizeof(double), cudaMemcpyDeviceToHost,
+                            ws->s_d2h));
+  }
+  TQ_CUDA(cudaEventRecord(ws->io_ev[1], ws->s_h2d));
+  TQ_CUDA(cudaEventRecord(ws->io_ev[2], ws->s_d2h));
+  TQ_CUDA(cudaStreamWaitEvent(s, ws->io_ev[1], 0));
+  TQ_CUDA(cudaStreamWaitEvent(s, ws->io_ev[2], 0));
+  return 0;
+}
+
 }  // namespace tileqr
 
 namespace tileqr {
@@ -856,6 +1074,57 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
   if ((rc = launch_tiles_to_layout(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, s))) return rc;
   TQ_CUDA(cudaMemcpyAsync(T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
                           cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int tileqr_factor_host(int64_t M, int64_t N, const double* h_A, int64_t lda, int NB, int IB, double* h_R,
+                       int64_t ldr, double* h_T, int* d_info, tileqr_stream_t stream) {
+  static const char* fn = "tileqr_factor_host";
+  if (M < 0) return arg_error(1, fn, "M < 0");
+  if (N < 0) return arg_error(2, fn, "N < 0");
+  if (!h_A && M > 0 && N > 0) return arg_error(3, fn, "h_A is NULL");
+  if (lda < std::max<int64_t>(1, M)) return arg_error(4, fn, "lda < max(1,M)");
+  if (NB < 1 || NB > 512) return arg_error(5, fn, "NB not in [1, 512]");
+  if (IB < 1 || IB > NB || NB % IB) return arg_error(6, fn, "IB must divide NB");
+  if (!h_R && M > 0 && N > 0) return arg_error(7, fn, "h_R is NULL");
+  if (ldr < std::max<int64_t>(1, M)) return arg_error(8, fn, "ldr < max(1,M)");
+  if (!h_T && M > 0 && N > 0) return arg_error(9, fn, "h_T is NULL");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (d_info) {
+    int rc = launch_zero_int(d_info, s);
+    if (rc) return rc;
+  }
+  if (M == 0 || N == 0) return 0;
+  int dev;
+  TQ_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(g_mu);
+  FactorWS* ws = nullptr;
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  if (it != g_ws.end()) {
+    ws = it->second.get();
+  } else {
+    int rc = create_ws(dev, M, N, NB, IB, &ws);
+    if (rc) return rc;
+  }
+  if (ws->use_dag) return factor_host_dag(ws, h_A, lda, h_R, ldr, h_T, d_info, s);
+  // level-synchronous schedule: copy in, factor, copy out (no overlap)
+  if (!ws->st_in) {
+    if (cudaMalloc(&ws->st_in, (size_t)M * N * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("tileqr_factor_host: device allocation of the staging buffer failed");
+      return TILEQR_ERR_ALLOC;
+    }
+  }
+  TQ_CUDA(cudaMemcpy2DAsync(ws->st_in, M * sizeof(double), h_A, lda * sizeof(double), M * sizeof(double), N,
+                            cudaMemcpyHostToDevice, s));
+  int rc = launch_layout_to_tiles(M, N, ws->st_in, M, NB, ws->MT, ws->NT, ws->tiles, d_info, s);
+  if (rc) return rc;
+  if ((rc = run_levels(ws, s))) return rc;
+  if ((rc = launch_tiles_to_layout(M, N, ws->st_in, M, NB, ws->MT, ws->NT, ws->tiles, s))) return rc;
+  TQ_CUDA(cudaMemcpy2DAsync(h_R, ldr * sizeof(double), ws->st_in, M * sizeof(double), M * sizeof(double), N,
+                            cudaMemcpyDeviceToHost, s));
+  TQ_CUDA(cudaMemcpyAsync(h_T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
   return 0;
 }
 
@@ -1084,8 +1353,9 @@ int tileqr_debug_dag_item(int64_t M, int64_t N, int NB, int IB, int64_t idx, int
   auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
   if (it == g_ws.end() || !it->second->use_dag) return TILEQR_ERR_NOT_INIT;
   FactorWS* ws = it->second.get();
-  if (idx < 0 || idx >= ws->nitems) return -5;
-  for (int q = 0; q < 5; ++q) out[q] = ws->item_info[5 * idx + q];
+  const DagList& L = ws->dag_last ? *ws->dag_last : ws->dag_plain;
+  if (idx < 0 || idx >= L.nitems) return -5;
+  for (int q = 0; q < 5; ++q) out[q] = L.item_info[5 * idx + q];
   return 0;
 }
 
@@ -1166,15 +1436,16 @@ int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* 
       TQ_CUDA(cudaEventElapsedTime(&ms, ws->dag_ev[0], ws->dag_ev[1]));
       *h_total_ms = ms;
       *h_launches = ws->dag_grid;
-      *h_tasks = ws->ntasks;
+      *h_tasks = ws->dag_last ? ws->dag_last->ntasks : 0;
       return 0;
     }
-    std::vector<unsigned long long> pr((size_t)ws->nitems * 3);
+    const DagList& L = *ws->dag_last;
+    std::vector<unsigned long long> pr((size_t)L.nitems * 3);
     TQ_CUDA(cudaMemcpy(pr.data(), ws->d_prof, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     const int cols = dag::dag_cols(ws->NB);
     const int nslab = (ws->NB + cols - 1) / cols;
-    for (int i = 0; i < ws->nitems; ++i) {
-      if (ws->item_kind[i] != kind) continue;
+    for (int i = 0; i < L.nitems; ++i) {
+      if (L.item_kind[i] != kind) continue;
       tot += (double)(pr[3 * i + 2] - pr[3 * i + 1]) * 1e-6;
       ++nl;
     }
@@ -1221,16 +1492,17 @@ int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, 
       set_error("tileqr_kernel_trace: the last run was not timed");
       return TILEQR_ERR_NOT_INIT;
     }
-    std::vector<unsigned long long> pr((size_t)ws->nitems * 3);
+    const DagList& L = *ws->dag_last;
+    std::vector<unsigned long long> pr((size_t)L.nitems * 3);
     TQ_CUDA(cudaMemcpy(pr.data(), ws->d_prof, pr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ull;
-    for (int i = 0; i < ws->nitems; ++i) t0 = std::min(t0, pr[3 * i]);
-    *h_count = ws->nitems;
-    for (int64_t i = 0; i < ws->nitems && i < max_recs; ++i) {
+    for (int i = 0; i < L.nitems; ++i) t0 = std::min(t0, pr[3 * i]);
+    *h_count = L.nitems;
+    for (int64_t i = 0; i < L.nitems && i < max_recs; ++i) {
       if (h_t0_ms) h_t0_ms[i] = (double)(pr[3 * i + 1] - t0) * 1e-6;
       if (h_t1_ms) h_t1_ms[i] = (double)(pr[3 * i + 2] - t0) * 1e-6;
-      if (h_kind) h_kind[i] = ws->item_kind[i];
-      if (h_level) h_level[i] = ws->item_level[i];
+      if (h_kind) h_kind[i] = L.item_kind[i];
+      if (h_level) h_level[i] = L.item_level[i];
       if (h_tasks) h_tasks[i] = (int64_t)(pr[3 * i] - t0);  // DAG: claim time (ns from origin)
     }
     return 0;

@@ -19,6 +19,7 @@
 // identical to it.
 #pragma once
 
+#include <math.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -91,6 +92,84 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// LOAD item: tiles (m, n), n in [n0, n1), m in [m0, m1), from the
+// column-major staging buffer (padding of DESIGN.md R5: rows >= M are 0, a
+// padded column j >= N is e_j when M <= j < MT*NB), flagging non-finite
+// input.  Element pairs of a column (16-byte accesses on the tile side), 8
+// pairs in flight per thread.
+template <int NB>
+__device__ __forceinline__ void load_body(const DagIO& io, long long MT, double* tiles, int n0, int n1, int m0,
+                                          int m1) {
+  constexpr int HP = NB / 2;  // row pairs per tile column segment
+  int bad = 0;
+  const int tm = m1 - m0;
+  const long long per = (long long)(n1 - n0) * tm * NB * HP;  // pairs
+  auto value = [&](long long i, long long j) {
+    if (i < io.M && j < io.N) {
+      const double v = __ldcg(io.in + i + j * io.ld);
+      if (!isfinite(v)) bad = 1;
+      return v;
+    }
+    return (j >= io.N && i == j && j >= io.M) ? 1.0 : 0.0;
+  };
+  for (long long e0 = threadIdx.x; e0 < per; e0 += 8LL * blockDim.x) {
+    double2 v[8];
+    long long dst[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long e = e0 + (long long)u * blockDim.x;
+      dst[u] = -1;
+      if (e < per) {
+        const long long t = e / ((long long)NB * HP), r = e - t * NB * HP;   // t: tile, r: pair in tile
+        const long long n = n0 + t / tm, m = m0 + t % tm;
+        const int jl = (int)(r / HP), il = 2 * (int)(r - (long long)jl * HP);
+        const long long i = m * NB + il, j = n * NB + jl;
+        v[u] = make_double2(value(i, j), value(i + 1, j));
+        dst[u] = (m + n * MT) * NB * NB + il + (long long)jl * NB;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (dst[u] >= 0) *reinterpret_cast<double2*>(tiles + dst[u]) = v[u];
+  }
+  if (bad && io.info) *io.info = 1;  // benign race: every writer stores 1
+}
+
+// STORE item: tiles (m, n), m in [m0, m1) -> column-major output staging
+// (16-byte loads from the tiles, 8 in flight per thread).
+template <int NB>
+__device__ __forceinline__ void store_body(const DagIO& io, long long MT, const double* tiles, int n, int m0,
+                                           int m1) {
+  constexpr int HP = NB / 2;
+  const long long j0 = (long long)n * NB;
+  const long long per = (long long)(m1 - m0) * NB * HP;
+  for (long long e0 = threadIdx.x; e0 < per; e0 += 8LL * blockDim.x) {
+    double2 v[8];
+    long long i0[8], jj[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long e = e0 + (long long)u * blockDim.x;
+      i0[u] = -1;
+      if (e < per) {
+        const long long t = e / ((long long)NB * HP), r = e - t * NB * HP;
+        const int jl = (int)(r / HP), il = 2 * (int)(r - (long long)jl * HP);
+        const long long m = m0 + t;
+        v[u] = __ldcg(reinterpret_cast<const double2*>(tiles + (m + (long long)n * MT) * NB * NB + il +
+                                                       (long long)jl * NB));
+        i0[u] = m * NB + il;
+        jj[u] = j0 + jl;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (i0[u] < 0 || jj[u] >= io.N) continue;
+      double* d = io.out + i0[u] + jj[u] * io.ld;
+      if (i0[u] < io.M) d[0] = v[u].x;
+      if (i0[u] + 1 < io.M) d[1] = v[u].y;
+    }
+  }
+}
+
 // 16-byte async copy global -> shared (L2 only), for the item descriptors
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
@@ -111,7 +190,7 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 template <int NB, int KW>
 __global__ void __launch_bounds__(dag_warps(NB) * 32, dag_ctas_per_sm(NB))
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
-           unsigned long long* prof, int throttle) {
+           unsigned long long* prof, int throttle, DagIO io, long long MT, double* tiles) {
   constexpr int W = dag_warps(NB);
   // per-SM count of running panel items (next[1 .. 256]): with `throttle`,
   // update warps sharing an SM with a panel item pause at their inner-panel
@@ -219,6 +298,12 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         else upd::update_body<NB, MB, KW, true, true, false, W>(IB, KW, NB, it.p[0], it.p[1], nullptr,
                                                                      it.p[2], 1, it.col0, smem);
         break;
+      case kLoad:
+        load_body<NB>(io, MT, tiles, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
+        break;
+      case kStore:
+        store_body<NB>(io, MT, tiles, it.aux[0], it.aux[2], it.aux[3]);
+        break;
       default:
         if constexpr (V2)
           v2::update_v2_body<NB, KW, MB, false, W, S>(it.pk, smem, full, empty, it.p[2], it.p[3], it.col0,
@@ -244,7 +329,8 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
 
 template <int NB, int KW>
 int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                 unsigned long long* prof, cudaStream_t s, int* grid_out) {
+                 unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO& io, long long MT,
+                 double* tiles) {
   auto kern = dag_kernel<NB, KW>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
@@ -265,22 +351,23 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
   if (grid_out) *grid_out = grid;
   const char* th = getenv("TILEQR_DAG_THROTTLE");
   const int throttle = th ? atoi(th) : 0;
-  kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof, throttle);
+  kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof, throttle, io, MT, tiles);
   TQ_LAUNCH_CHECK();
   return 0;
 }
 
 template <int NB>
 int launch_dag_nb(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                  unsigned long long* prof, cudaStream_t s, int* grid_out) {
+                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO& io, long long MT,
+                  double* tiles) {
   switch (IB) {
-    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
-    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
     case 24:
-      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
       set_error("DAG kernel: IB does not divide NB");
       return TILEQR_ERR_CUDA;
-    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out);
+    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
     default: set_error("DAG kernel: IB not in {8,16,24,32}"); return TILEQR_ERR_CUDA;
   }
 }

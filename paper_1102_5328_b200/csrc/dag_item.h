@@ -17,7 +17,7 @@ __host__ __device__ constexpr int dag_warps(int NB) { return NB <= 128 ? 4 : 8; 
 __host__ __device__ constexpr int dag_ctas_per_sm(int NB) { return NB <= 128 ? 2 : 1; }
 #endif
 
-enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3 };
+enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3, kLoad = 4, kStore = 5 };
 
 // One work item: a whole panel task, or a column slab of an update task.
 struct Item {
@@ -30,6 +30,18 @@ struct Item {
   int need[3];
   double* p[4];  // GEQRT: A, -, T; TSQRT: R, A2, T; LARFB: V, T, C; SSRFB: V2, T, C1, C2
   double* pk;    // packed reflector tile (NB <= 128): written by GEQRT/TSQRT, read by LARFB/SSRFB
+  int aux[4];    // LOAD / STORE (host-buffer pipeline): tile column n, tile rows [aux[1], aux[2])
+};
+
+// Host-buffer pipeline of tileqr_factor_host: LOAD items convert a tile
+// column that the copy engine has landed in a column-major staging buffer
+// into tiles; STORE items convert a finished tile column back for the
+// device-to-host copy.
+struct DagIO {
+  long long M, N, ld;   // matrix and staging leading dimension
+  const double* in;     // column-major input staging (device)
+  double* out;          // column-major output staging (device)
+  int* info;            // non-finite flag
 };
 
 // Update columns per item for tile order NB: warps x 8*MB columns.

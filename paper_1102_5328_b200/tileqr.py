@@ -36,6 +36,7 @@ _SIGS = {
     "tileqr_last_error": ([], ctypes.c_char_p),
     "tileqr_t_size": ([_i64, _i64, _i, _i, ctypes.POINTER(_sz)], _i),
     "tileqr_factor": ([_i64, _i64, _p, _i64, _i, _i, _p, _p, _p], _i),
+    "tileqr_factor_host": ([_i64, _i64, _p, _i64, _i, _i, _p, _i64, _p, _p, _p], _i),
     "tileqr_apply_qt": ([_c, _i64, _i64, _i64, _p, _i64, _p, _i, _i, _p, _i64, _p], _i),
     "tileqr_geqrt_batched": ([_i, _i, _i, _p, _p, _p], _i),
     "tileqr_tsqrt_batched": ([_i, _i, _i, _p, _p, _p, _p], _i),
@@ -153,6 +154,26 @@ def factor(A: torch.Tensor, m: int, n: int, nb: int, ib: int, T: torch.Tensor | 
                             T.data_ptr(), info.data_ptr(), _stream(stream))
     _check(rc, "tileqr_factor")
     return T, info
+
+
+def factor_host(hA: torch.Tensor, m: int, n: int, nb: int, ib: int, hR: torch.Tensor | None = None,
+                hT: torch.Tensor | None = None, info: torch.Tensor | None = None, lda: int | None = None,
+                ldr: int | None = None, stream=None):
+    """tileqr_factor_host: the column-major m x n matrix in HOST tensor hA
+    (pin it for overlap) -> R/V in host tensor hR (default: in place in hA) and
+    T in host tensor hT.  Stream-ordered; returns (hR, hT, info)."""
+    assert hA.dtype == torch.float64 and not hA.is_cuda and hA.is_contiguous()
+    if hR is None:
+        hR = hA
+    if hT is None:
+        hT = torch.empty(max(1, t_size(m, n, nb, ib)), dtype=torch.float64, pin_memory=hA.is_pinned())
+    if info is None:
+        info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rc = _lib.tileqr_factor_host(m, n, hA.data_ptr(), lda if lda is not None else max(1, m), nb, ib,
+                                 hR.data_ptr(), ldr if ldr is not None else max(1, m), hT.data_ptr(),
+                                 info.data_ptr(), _stream(stream))
+    _check(rc, "tileqr_factor_host")
+    return hR, hT, info
 
 
 def apply_qt(trans: str, A: torch.Tensor, m: int, k: int, T: torch.Tensor, nb: int, ib: int,
@@ -288,7 +309,7 @@ def kernel_trace(m: int, n: int, nb: int, ib: int, max_recs: int = 1 << 16):
     cnt = _i64()
     _check(_lib.tileqr_kernel_trace(m, n, nb, ib, max_recs, t0, t1, kd, lv, nt, ctypes.byref(cnt)),
            "tileqr_kernel_trace")
-    names = {v: k for k, v in KINDS.items()}
+    names = {0: "geqrt", 1: "tsqrt", 2: "larfb", 3: "ssrfb", 4: "load", 5: "store"}
     return [(t0[i], t1[i], names[kd[i]], lv[i], nt[i]) for i in range(min(cnt.value, max_recs))]
 
 

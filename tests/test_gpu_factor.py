@@ -229,3 +229,38 @@ def test_dataflow_kernel_stress_4096(tq, monkeypatch, ib):
         assert int(info.item()) == 0
         assert torch.equal(A, Ar) and torch.equal(T, Tr)
     tq.finalize()
+
+
+@pytest.mark.parametrize("m,n,nb,ib,seed", [
+    (1000, 1000, 128, 16, 70),   # ragged, dataflow path with LOAD/STORE items
+    (900, 400, 64, 16, 71),      # tall
+    (400, 900, 96, 32, 72),      # wide
+    (2048, 2048, 64, 8, 73),
+    (300, 300, 48, 6, 74),       # level-synchronous fallback (no overlap)
+])
+def test_factor_host_equals_device_factor(tq, m, n, nb, ib, seed):
+    """tileqr_factor_host (host buffers, copies overlapped with the dataflow
+    kernel through LOAD / STORE items and stream waits) returns bitwise the
+    device path's factors, in place and to a separate output."""
+    a = si.uniform(m, n, seed)
+    A, T, _ = gpu_factor(tq, a, nb, ib)
+    hA = torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory()  # column-major storage
+    hR = torch.empty_like(hA).pin_memory()
+    hT = torch.empty(T.numel(), dtype=torch.float64).pin_memory()
+    _, _, info = tq.factor_host(hA, m, n, nb, ib, hR=hR, hT=hT)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    assert torch.equal(hR, A.cpu()) and torch.equal(hT, T.cpu())
+    assert torch.equal(hA, torch.from_numpy(np.ascontiguousarray(a.T)))  # input untouched
+    hR2, hT2, _ = tq.factor_host(hA, m, n, nb, ib)  # in place
+    torch.cuda.synchronize()
+    assert torch.equal(hR2, A.cpu()) and torch.equal(hT2, T.cpu())
+
+
+def test_factor_host_flags_nonfinite(tq):
+    a = si.uniform(512, 512, 75)
+    a[300, 200] = np.inf
+    hA = torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory()
+    _, _, info = tq.factor_host(hA, 512, 512, 128, 16)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 1
