@@ -34,24 +34,22 @@ namespace tileqr {
 
 #define TQ_DECL_DAG(nb)                                                                        \
   int launch_dag_nb##nb(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm, \
-                        unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO& io,  \
-                        long long MT, double* tiles);
+                        unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io);
 TQ_DECL_DAG(32) TQ_DECL_DAG(64) TQ_DECL_DAG(96) TQ_DECL_DAG(128) TQ_DECL_DAG(160) TQ_DECL_DAG(192)
 TQ_DECL_DAG(224) TQ_DECL_DAG(256)
 #undef TQ_DECL_DAG
 
 static int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                      unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO& io,
-                      long long MT, double* tiles) {
+                      unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io) {
   switch (NB) {
-    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
     default: return TILEQR_ERR_CUDA;
   }
 }
@@ -191,6 +189,7 @@ struct FactorWS {
   // host pipeline (tileqr_factor_host): column-major staging, copy streams
   double* st_in = nullptr;
   double* st_out = nullptr;
+  dag::DagIO* d_io = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t io_ev[3] = {nullptr, nullptr, nullptr};
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
@@ -211,6 +210,7 @@ struct FactorWS {
     cudaFree(d_prof);
     cudaFree(st_in);
     cudaFree(st_out);
+    cudaFree(d_io);
     for (auto e : dag_ev) if (e) cudaEventDestroy(e);
     for (auto e : io_ev) if (e) cudaEventDestroy(e);
     if (s_h2d) cudaStreamDestroy(s_h2d);
@@ -577,7 +577,7 @@ static int build_dag(FactorWS* ws, bool io) {
   return 0;
 }
 
-static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO& io, cudaStream_t stream) {
+static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStream_t stream) {
   unsigned long long* prof = nullptr;
   if (g_timing) {
     if (ws->prof_cap < (size_t)L.nitems) {
@@ -595,7 +595,7 @@ static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO& io, cudaStre
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
   int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, ws->nsm, prof, stream,
-                      &ws->dag_grid, io, ws->MT, ws->tiles);
+                      &ws->dag_grid, io);
   if (rc) return rc;
   if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
   ws->dag_timed = g_timing != 0;
@@ -607,8 +607,7 @@ static int run_dag(FactorWS* ws, cudaStream_t stream) {
   DagList& L = ws->dag_plain;
   // counters: [claim cursor | 256 per-SM panel flags | one per task]
   TQ_CUDA(cudaMemsetAsync(L.d_ctr, 0, (size_t)(L.ntasks + 257) * sizeof(int), stream));
-  dag::DagIO io{ws->M, ws->N, ws->M, nullptr, nullptr, nullptr};
-  return run_dag_list(ws, L, io, stream);
+  return run_dag_list(ws, L, nullptr, stream);
 }
 
 static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** out) {
@@ -984,8 +983,12 @@ static int factor_host_dag(FactorWS* ws, const double* hA, int64_t lda, double* 
     TQ_CU(g_write_value((CUstream)ws->s_h2d, counter(L.id_ar + n), 1, CU_STREAM_WRITE_VALUE_DEFAULT));
   }
   // the factorization, with LOAD / STORE items
-  dag::DagIO io{M, N, M, ws->st_in, ws->st_out, d_info};
-  if (int rc = run_dag_list(ws, L, io, s)) return rc;
+  // the LOAD / STORE items read their parameters from device memory (a
+  // by-value kernel argument would cost every item registers)
+  const dag::DagIO io{M, N, M, ws->st_in, ws->st_out, d_info, MT, ws->tiles};
+  if (!ws->d_io) TQ_CUDA(cudaMalloc(&ws->d_io, sizeof(dag::DagIO)));
+  TQ_CUDA(cudaMemcpyAsync(ws->d_io, &io, sizeof io, cudaMemcpyHostToDevice, s));
+  if (int rc = run_dag_list(ws, L, ws->d_io, s)) return rc;
   // copy engine, device -> host: each tile column as soon as its STORE items
   // are done (and with it that column of T)
   for (int64_t n = 0; n < NT; ++n) {

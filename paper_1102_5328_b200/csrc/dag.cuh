@@ -98,8 +98,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // input.  Element pairs of a column (16-byte accesses on the tile side), 8
 // pairs in flight per thread.
 template <int NB>
-__device__ __forceinline__ void load_body(const DagIO& io, long long MT, double* tiles, int n0, int n1, int m0,
-                                          int m1) {
+__device__ __noinline__ void load_body(const DagIO* __restrict__ iop, int n0, int n1, int m0, int m1) {
+  const DagIO io = *iop;
+  const long long MT = io.MT;
+  double* const tiles = io.tiles;
   constexpr int HP = NB / 2;  // row pairs per tile column segment
   int bad = 0;
   const int tm = m1 - m0;
@@ -138,8 +140,10 @@ __device__ __forceinline__ void load_body(const DagIO& io, long long MT, double*
 // STORE item: tiles (m, n), m in [m0, m1) -> column-major output staging
 // (16-byte loads from the tiles, 8 in flight per thread).
 template <int NB>
-__device__ __forceinline__ void store_body(const DagIO& io, long long MT, const double* tiles, int n, int m0,
-                                           int m1) {
+__device__ __noinline__ void store_body(const DagIO* __restrict__ iop, int n, int m0, int m1) {
+  const DagIO io = *iop;
+  const long long MT = io.MT;
+  const double* const tiles = io.tiles;
   constexpr int HP = NB / 2;
   const long long j0 = (long long)n * NB;
   const long long per = (long long)(m1 - m0) * NB * HP;
@@ -190,7 +194,7 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 template <int NB, int KW>
 __global__ void __launch_bounds__(dag_warps(NB) * 32, dag_ctas_per_sm(NB))
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
-           unsigned long long* prof, int throttle, DagIO io, long long MT, double* tiles) {
+           unsigned long long* prof, int throttle, const DagIO* io) {
   constexpr int W = dag_warps(NB);
   // per-SM count of running panel items (next[1 .. 256]): with `throttle`,
   // update warps sharing an SM with a panel item pause at their inner-panel
@@ -299,10 +303,10 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
                                                                      it.p[2], 1, it.col0, smem);
         break;
       case kLoad:
-        load_body<NB>(io, MT, tiles, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
+        load_body<NB>(io, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
         break;
       case kStore:
-        store_body<NB>(io, MT, tiles, it.aux[0], it.aux[2], it.aux[3]);
+        store_body<NB>(io, it.aux[0], it.aux[2], it.aux[3]);
         break;
       default:
         if constexpr (V2)
@@ -329,8 +333,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
 
 template <int NB, int KW>
 int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                 unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO& io, long long MT,
-                 double* tiles) {
+                 unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io) {
   auto kern = dag_kernel<NB, KW>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
@@ -351,23 +354,22 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
   if (grid_out) *grid_out = grid;
   const char* th = getenv("TILEQR_DAG_THROTTLE");
   const int throttle = th ? atoi(th) : 0;
-  kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof, throttle, io, MT, tiles);
+  kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof, throttle, io);
   TQ_LAUNCH_CHECK();
   return 0;
 }
 
 template <int NB>
 int launch_dag_nb(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO& io, long long MT,
-                  double* tiles) {
+                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io) {
   switch (IB) {
-    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
-    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
     case 24:
-      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
       set_error("DAG kernel: IB does not divide NB");
       return TILEQR_ERR_CUDA;
-    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
     default: set_error("DAG kernel: IB not in {8,16,24,32}"); return TILEQR_ERR_CUDA;
   }
 }

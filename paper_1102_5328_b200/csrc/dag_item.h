@@ -42,6 +42,8 @@ struct DagIO {
   const double* in;     // column-major input staging (device)
   double* out;          // column-major output staging (device)
   int* info;            // non-finite flag
+  long long MT;         // tile rows of the workspace
+  double* tiles;        // tile workspace
 };
 
 // Update columns per item for tile order NB: warps x 8*MB columns.

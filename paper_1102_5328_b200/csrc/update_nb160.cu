@@ -11,8 +11,7 @@ int launch_update_nb160(bool trans, bool larfb, int IB, int batch, const double*
   return upd::launch_update_dmma<160>(trans, larfb, IB, batch, V, T, C1, C2, ncols, s);
 }
 int launch_dag_nb160(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                     unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO& io,
-                     long long MT, double* tiles) {
-  return dag::launch_dag_nb<160>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, MT, tiles);
+                     unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io) {
+  return dag::launch_dag_nb<160>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
 }
 }  // namespace tileqr
