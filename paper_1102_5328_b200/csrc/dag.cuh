@@ -197,9 +197,9 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
            unsigned long long* prof, int throttle, const DagIO* io) {
   constexpr int W = dag_warps(NB);
   // per-SM count of running panel items (next[1 .. 256]): with `throttle`,
-  // update warps sharing an SM with a panel item pause at their inner-panel
-  // boundaries so the latency-bound panel (the DAG's critical path) gets the
-  // SM's issue slots
+  // update warps sharing an SM with a panel item (1: GEQRT or TSQRT, 2: GEQRT
+  // only) pause at their inner-panel boundaries so the latency-bound panel
+  // (the DAG's critical path) gets the SM's issue slots
   int* const smflag = next + 1;
   unsigned smid;
   asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -245,7 +245,8 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
             got[d] = ld_acquire(done + it.dep[d]);
           }
         if (prof) prof[3 * (size_t)cur + 1] = globaltimer();
-        if (throttle && (it.kind == kGeqrt || it.kind == kTsqrt)) atomicAdd(&smflag[smid & 255], 1);
+        if (throttle && (it.kind == kGeqrt || (throttle == 1 && it.kind == kTsqrt)))
+          atomicAdd(&smflag[smid & 255], 1);
         if constexpr (V2) {
           if (it.kind == kLarfb || it.kind == kSsrfb)
             v2::ring_start<NB, KW, S>(it.pk, smem, full, empty, v2::active_warps<NB, MB, W>(it.col0));
@@ -324,7 +325,8 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(done + it.task, 1);
-      if (throttle && (it.kind == kGeqrt || it.kind == kTsqrt)) atomicSub(&smflag[smid & 255], 1);
+      if (throttle && (it.kind == kGeqrt || (throttle == 1 && it.kind == kTsqrt)))
+        atomicSub(&smflag[smid & 255], 1);
       if (prof) prof[3 * (size_t)i + 2] = globaltimer();
     }
     slot ^= 1;

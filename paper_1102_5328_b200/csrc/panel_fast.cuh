@@ -80,7 +80,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
   for (int e = tid; e < 32 * LDG; e += kThreads) S.Gs[e] = 0.0;
 #ifdef TILEQR_PANEL_PROF
   long long tp0 = clock64(), tp1;
-#define TQ_PHASE(k) do { if (tid == 0) { tp1 = clock64(); atomicAdd(&g_panel_prof[k], (unsigned long long)(tp1 - tp0)); tp0 = tp1; } } while (0)
+#define TQ_PHASE(k) do { if (tid == 0) { tp1 = clock64(); atomicAdd(&g_panel_prof[(k) + (TS ? 0 : 8)], (unsigned long long)(tp1 - tp0)); tp0 = tp1; } } while (0)
 #else
 #define TQ_PHASE(k) do { } while (0)
 #endif
@@ -121,9 +121,9 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
     // Registers: lane = column, warp w holds rows [w*RW, (w+1)*RW) in x[].
     // GEQRT: the IB rows [c0, c0+IB) of the diagonal block -- the rows that
     // leave the reflector one per step -- are held separately, row c0+i in
-    // top[i / W] of warp i % W, so that every step's row bookkeeping is a
-    // compile-time index (the step loop is unrolled); x[] holds only the rows
-    // below, which stay in every reflector of the panel.
+    // top[i / W] of warp i % W (a warp's rows leave in order: slot 0 is always
+    // the next one, see the step); x[] holds only the rows below, which stay in
+    // every reflector of the panel.
     double x[RW];
 #pragma unroll
     for (int q = 0; q < RW; ++q)
@@ -137,10 +137,19 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 
     TQ_PHASE(0);
     // ---- 1. factor the panel column by column --------------------------------
-#pragma unroll
-    for (int jj = 0; jj < IB; ++jj) {
+    auto step = [&](const int jj) {
       const int buf = jj & 1;
-      if (!TS && warp == jj % kWarps) S.rowj[buf][lane] = top[jj / kWarps];  // row j: alpha, R(j, c)
+      if (!TS && warp == jj % kWarps) {
+        // row j leaves the reflector: its owner publishes it (alpha, R(j, c))
+        // and stores its final V entries (lanes < j; the rest is R, written
+        // from Rout), then shifts its remaining top rows down one slot, so
+        // every slot always holds a row below j (no dynamic register index)
+        S.rowj[buf][lane] = top[0];
+        S.Vs[vsw(c0 + jj, lane, LDV)] = lane < IB ? top[0] : 0.0;
+#pragma unroll
+        for (int t = 0; t + 1 < TR; ++t) top[t] = top[t + 1];
+        top[TR - 1] = 0.0;
+      }
       double vj[RW];
       double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
 #pragma unroll
@@ -153,7 +162,6 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
         for (int t = 0; t < TR; ++t) {
           vt[t] = __shfl_sync(0xffffffffu, top[t], jj);
-          if (t * kWarps + warp <= jj) vt[t] = 0.0;
           pp[t & 3] = fma(vt[t], top[t], pp[t & 3]);
         }
       }
@@ -210,27 +218,37 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       for (int q = 0; q < RW; ++q) x[q] = fma(coef, vj[q], x[q]);
       if (!TS) {
 #pragma unroll
-        for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t]);  // vt == 0 on rows <= j
+        for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t]);
       }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
       if (warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
       if (tid == 0) S.tau[jj] = tau;
+    };
+#ifdef TILEQR_TSQRT_ROLLED  // diagnostic variant: TSQRT's step loop rolled too
+    constexpr bool kUnrolled = false;
+#else
+    constexpr bool kUnrolled = TS;
+#endif
+    if constexpr (kUnrolled) {
+#pragma unroll
+      for (int jj = 0; jj < IB; ++jj) step(jj);
+    } else {
+      // GEQRT runs on one SM at a time while every other SM runs update code:
+      // its instructions are cold in the SM's instruction caches, and a fully
+      // unrolled step loop (~55 KB of SASS) stalled it on instruction fetch
+      // about half of the time (ncu source view, stall_no_instruction) -- keep
+      // the loop rolled so it is fetched once per inner panel
+#pragma unroll 1
+      for (int jj = 0; jj < IB; ++jj) step(jj);
     }
     __syncthreads();  // everyone done reading Vs (panel values) and red
     TQ_PHASE(1);
 
     // ---- write the factored panel: registers -> smem -> global (coalesced) ----
 #pragma unroll
-    for (int q = 0; q < RW; ++q)  // GEQRT: the top rows come from top[] below
+    for (int q = 0; q < RW; ++q)  // GEQRT: the top rows were stored by the step loop
       if (TS || warp * RW + q >= c0 + IB) S.Vs[vsw(warp * RW + q, lane, LDV)] = lane < IB ? x[q] : 0.0;
-    if (!TS) {
-#pragma unroll
-      for (int t = 0; t < TR; ++t) {
-        const int i = t * kWarps + warp;
-        if (i < IB) S.Vs[vsw(c0 + i, lane, LDV)] = lane < IB ? top[t] : 0.0;
-      }
-    }
-    __syncthreads();
+    __syncthreads();  // GEQRT: the top rows were stored as they left the reflector
     for (int idx = tid; idx < NB * IB; idx += kThreads) {
       const int c = idx / NB, r = idx - c * NB;
       double* p = &S.Vs[vsw(r, c, LDV)];

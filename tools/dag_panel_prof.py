@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1102_5328_b200 import tileqr as tq  # noqa: E402
 
 ib = int(sys.argv[1]) if len(sys.argv) > 1 else 16
-n, nb = 10000, 128
+n, nb = int(sys.argv[2]) if len(sys.argv) > 2 else 10000, 128
 f = tq._lib.tileqr_debug_dag_panel_prof
 f.argtypes = [ctypes.c_void_p, ctypes.c_int]
 out = (ctypes.c_ulonglong * 16)()
@@ -26,8 +26,8 @@ tq.factor(A, n, n, nb, ib)
 torch.cuda.synchronize()
 f(out, 1)
 names = {0: "stage", 1: "factor", 2: "writeV", 5: "gram", 6: "Tdiag", 7: "Tmerge", 3: "Twrite+pack", 4: "trailing"}
-ph = {v: out[k] for k, v in names.items()}
-tot = sum(ph.values())
-npan = (n // nb + 1) * (n // nb + 2) // 2 * (nb // ib)  # inner panels of all GEQRT/TSQRT (approx)
-print({k: f"{100 * v / tot:.1f}%" for k, v in ph.items()}, "total Gcycles %.2f" % (tot / 1e9),
-      "per inner panel %.0f cycles" % (tot / npan))
+nt = -(-n // nb)
+for label, off, npan in (("TSQRT", 0, nt * (nt - 1) // 2 * (nb // ib)), ("GEQRT", 8, nt * (nb // ib))):
+    ph = {v: out[k + off] for k, v in names.items()}
+    tot = sum(ph.values())
+    print(label, {k: round(v / npan) for k, v in ph.items()}, "cycles per inner panel, total %.0f" % (tot / npan))
