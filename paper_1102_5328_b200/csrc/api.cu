@@ -262,7 +262,7 @@ static int panel_sub_cols(int NB, int IB) {
 // since a task's bottom level exceeds each successor's -- ties by ASAP level,
 // then task id.
 static int build_dag(FactorWS* ws, bool io) {
-  const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT);
+  const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT), N = ws->N;
   const int NB = ws->NB, IB = ws->IB;
   const int SC = panel_sub_cols(NB, IB), NS = NB / SC;
   std::vector<int64_t> offL(KT + 1), offT(KT + 1), offS(KT + 1);
@@ -551,6 +551,8 @@ static int build_dag(FactorWS* ws, bool io) {
         it.pk = pkp(t.m, t.k);
         break;
     }
+    if (t.kind == dag::kLarfb || t.kind == dag::kSsrfb)  // padded columns (e_j or 0) are invariant
+      it.aux[0] = (int)std::min<int64_t>(NB, std::max<int64_t>(0, N - (int64_t)t.n * NB));
     items.push_back(it);
     L.item_kind.push_back((unsigned char)t.kind);
     L.item_level.push_back(t.level);

@@ -248,8 +248,10 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         if (throttle && (it.kind == kGeqrt || (throttle == 1 && it.kind == kTsqrt)))
           atomicAdd(&smflag[smid & 255], 1);
         if constexpr (V2) {
-          if (it.kind == kLarfb || it.kind == kSsrfb)
-            v2::ring_start<NB, KW, S>(it.pk, smem, full, empty, v2::active_warps<NB, MB, W>(it.col0));
+          if (it.kind == kLarfb || it.kind == kSsrfb) {
+            const int na = v2::active_warps<NB, MB, W>(it.col0, it.aux[0]);
+            if (na > 0) v2::ring_start<NB, KW, S>(it.pk, smem, full, empty, na);
+          }
         }
       }
     }
@@ -297,10 +299,12 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
                                               reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
                                               it.col0 & 0xffff, it.col0 >> 16);
         break;
-      case kLarfb:
+      case kLarfb:  // columns [col0, min(col0 + slab, aux[0])): the rest of the tile is padding
+        if (it.aux[0] <= it.col0) break;
         if constexpr (V2)
-          v2::update_v2_body<NB, KW, MB, true, W, S>(it.pk, smem, full, empty, nullptr, it.p[2], it.col0, hook);
-        else upd::update_body<NB, MB, KW, true, true, false, W>(IB, KW, NB, it.p[0], it.p[1], nullptr,
+          v2::update_v2_body<NB, KW, MB, true, W, S>(it.pk, smem, full, empty, nullptr, it.p[2], it.col0, hook,
+                                                     it.aux[0]);
+        else upd::update_body<NB, MB, KW, true, true, false, W>(IB, KW, it.aux[0], it.p[0], it.p[1], nullptr,
                                                                      it.p[2], 1, it.col0, smem);
         break;
       case kLoad:
@@ -309,11 +313,12 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       case kStore:
         store_body<NB>(io, it.aux[0], it.aux[2], it.aux[3]);
         break;
-      default:
+      default:  // SSRFB: columns as LARFB
+        if (it.aux[0] <= it.col0) break;
         if constexpr (V2)
           v2::update_v2_body<NB, KW, MB, false, W, S>(it.pk, smem, full, empty, it.p[2], it.p[3], it.col0,
-                                                      hook);
-        else upd::update_body<NB, MB, KW, true, false, false, W>(IB, KW, NB, it.p[0], it.p[1], it.p[2],
+                                                      hook, it.aux[0]);
+        else upd::update_body<NB, MB, KW, true, false, false, W>(IB, KW, it.aux[0], it.p[0], it.p[1], it.p[2],
                                                                       it.p[3], 1, it.col0, smem);
         break;
     }

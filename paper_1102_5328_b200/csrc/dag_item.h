@@ -30,7 +30,9 @@ struct Item {
   int need[3];
   double* p[4];  // GEQRT: A, -, T; TSQRT: R, A2, T; LARFB: V, T, C; SSRFB: V2, T, C1, C2
   double* pk;    // packed reflector tile (NB <= 128): written by GEQRT/TSQRT, read by LARFB/SSRFB
-  int aux[4];    // LOAD / STORE (host-buffer pipeline): tile column n, tile rows [aux[1], aux[2])
+  int aux[4];    // LOAD / STORE (host-buffer pipeline): tile column n, tile rows [aux[1], aux[2]);
+                 // LARFB / SSRFB: aux[0] = column limit in the tile (N - n*NB, at most NB):
+                 // the columns past it are padding, which every update leaves exactly as is
 };
 
 // Host-buffer pipeline of tileqr_factor_host: LOAD items convert a tile

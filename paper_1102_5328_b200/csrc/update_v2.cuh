@@ -194,7 +194,7 @@ struct NoHook {
 template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook>
 __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, double* spk, uint64_t* full,
                                                uint64_t* empty, double* __restrict__ C1, double* __restrict__ C2,
-                                               int col0, Hook hook = Hook()) {
+                                               int col0, Hook hook = Hook(), int cend = NB) {
   using P = Pk<NB, IB>;
   using RG = Ring<NB, IB, S>;
   constexpr int RB = NB / 8;
@@ -203,7 +203,9 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, g = lane >> 2;
   const int wc0 = col0 + warp * 8 * MB;  // first column of this warp
-  if (wc0 >= NB) {                       // idle warp (8*MB*W > NB): no CTA barrier follows
+  // idle warp (8*MB*W > NB, or every column from wc0 on is padding: cend,
+  // the item's column limit): no CTA barrier follows
+  if (wc0 >= cend) {
     for (int p = 0; p < P::NP; ++p) hook(p);
     return;
   }
@@ -390,8 +392,8 @@ constexpr size_t v2_smem_bytes() { return Ring<NB, IB, Pk<NB, IB>::NG>::bytes; }
 
 // warps of a CTA (W warps of 8*MB columns from col0) that own columns < NB
 template <int NB, int MB, int W>
-__device__ __forceinline__ int active_warps(int col0) {
-  const int a = (NB - col0 + 8 * MB - 1) / (8 * MB);
+__device__ __forceinline__ int active_warps(int col0, int cend = NB) {
+  const int a = (cend - col0 + 8 * MB - 1) / (8 * MB);
   return a < 0 ? 0 : (a > W ? W : a);
 }
 

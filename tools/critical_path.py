@@ -36,13 +36,14 @@ f = tq._lib.tileqr_debug_dag_item
 f.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]
 out = (ctypes.c_int * 5)()
 names = ["G", "T", "L", "S"]
-task_start, task_end = {}, {}
+task_start, task_end, task_claim = {}, {}, {}
 for i, r in enumerate(recs):
     f(n, n, nb, ib, i, out)
     kind, k, m, nn, s = list(out)
     key = (names[kind], k, m, nn, s if kind < 2 else 0)
     task_start[key] = min(task_start.get(key, 1e30), r[0])
     task_end[key] = max(task_end.get(key, 0.0), r[1])
+    task_claim[key] = max(task_claim.get(key, 0.0), r[4] * 1e-6)
 NS = max(key[4] for key in task_end if key[0] == "G") + 1
 
 
@@ -66,6 +67,8 @@ t = max(task_end, key=task_end.get)
 span = task_end[t]
 run = collections.Counter()
 gap = collections.Counter()
+late_claim = collections.Counter()  # part of the gap: the item was claimed after its input was final
+tail = collections.Counter()        # run / gap of path tasks starting in the last 10 % of the span
 path = []
 while True:
     ds = deps(t)
@@ -76,8 +79,14 @@ while True:
         break
     d = max(ds, key=task_end.get)
     gap[t[0]] += max(0.0, task_start[t] - task_end[d])
+    late_claim[t[0]] += max(0.0, task_claim[t] - task_end[d])
+    if task_start[t] > 0.9 * span:
+        tail["run_" + t[0]] += task_end[t] - task_start[t]
+        tail["gap_" + t[0]] += max(0.0, task_start[t] - task_end[d])
     t = d
 print(json.dumps({"span_ms": round(span, 3), "path_tasks": len(path),
                   "run_ms": {k: round(v, 3) for k, v in run.items()},
                   "gap_ms_before": {k: round(v, 3) for k, v in gap.items()},
+                  "late_claim_ms": {k: round(v, 3) for k, v in late_claim.items()},
+                  "last_10pct": {k: round(v, 3) for k, v in sorted(tail.items())},
                   "kinds_on_path": dict(collections.Counter(x[0] for x in path))}))
