@@ -191,7 +191,11 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 // remains.  A claimed item is held for about three inner panels.  Items are claimed in list order and a CTA's held
 // item always follows its running one, so the smallest unfinished item is
 // always running or about to (no deadlock).
-template <int NB, int KW>
+//
+// IO: the instantiation for tileqr_factor_host, with the LOAD / STORE items
+// (their code in the kernel costs the device-only factorization ~1.8 %, same
+// box A/B, so tileqr_factor runs an instantiation without them).
+template <int NB, int KW, bool IO>
 __global__ void __launch_bounds__(dag_warps(NB) * 32, dag_ctas_per_sm(NB))
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
            unsigned long long* prof, int throttle, const DagIO* io) {
@@ -308,10 +312,10 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
                                                                      it.p[2], 1, it.col0, smem);
         break;
       case kLoad:
-        load_body<NB>(io, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
+        if constexpr (IO) load_body<NB>(io, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
         break;
       case kStore:
-        store_body<NB>(io, it.aux[0], it.aux[2], it.aux[3]);
+        if constexpr (IO) store_body<NB>(io, it.aux[0], it.aux[2], it.aux[3]);
         break;
       default:  // SSRFB: columns as LARFB
         if (it.aux[0] <= it.col0) break;
@@ -341,7 +345,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
 template <int NB, int KW>
 int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io) {
-  auto kern = dag_kernel<NB, KW>;
+  auto kern = io ? dag_kernel<NB, KW, true> : dag_kernel<NB, KW, false>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
