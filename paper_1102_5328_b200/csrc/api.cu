@@ -142,7 +142,7 @@ struct DagList {
   dag::Item* d_items = nullptr;
   int nitems = 0, ntasks = 0, nio = 0;
   int64_t id_ld = 0, id_st = 0, id_ar = 0;  // first LOAD / STORE / ARRIVE task (host pipeline)
-  int* d_ctr = nullptr;                     // [claim cursor | 256 per-SM flags | one per task]
+  int* d_ctr = nullptr;                     // [claim cursor | 256 reserved | one per task]
   std::vector<unsigned char> item_kind;     // host copies for the diagnostics
   std::vector<int> item_info;               // per item: kind, k, m, n, sub-task / slab column
   std::vector<int> item_level;
@@ -607,7 +607,7 @@ static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStre
 
 static int run_dag(FactorWS* ws, cudaStream_t stream) {
   DagList& L = ws->dag_plain;
-  // counters: [claim cursor | 256 per-SM panel flags | one per task]
+  // counters: [claim cursor | 256 reserved | one per task]
   TQ_CUDA(cudaMemsetAsync(L.d_ctr, 0, (size_t)(L.ntasks + 257) * sizeof(int), stream));
   return run_dag_list(ws, L, nullptr, stream);
 }

@@ -198,15 +198,8 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 template <int NB, int KW, bool IO>
 __global__ void __launch_bounds__(dag_warps(NB) * 32, dag_ctas_per_sm(NB))
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
-           unsigned long long* prof, int throttle, const DagIO* io) {
+           unsigned long long* prof, const DagIO* io) {
   constexpr int W = dag_warps(NB);
-  // per-SM count of running panel items (next[1 .. 256]): with `throttle`,
-  // update warps sharing an SM with a panel item (1: GEQRT or TSQRT, 2: GEQRT
-  // only) pause at their inner-panel boundaries so the latency-bound panel
-  // (the DAG's critical path) gets the SM's issue slots
-  int* const smflag = next + 1;
-  unsigned smid;
-  asm("mov.u32 %0, %%smid;" : "=r"(smid));
   constexpr int MB = dag_mb(NB);
   constexpr int S = dag_stages<NB, KW>();
   static_assert(sizeof(Item) % 16 == 0, "Item is copied in 16-byte chunks");
@@ -249,8 +242,6 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
             got[d] = ld_acquire(done + it.dep[d]);
           }
         if (prof) prof[3 * (size_t)cur + 1] = globaltimer();
-        if (throttle && (it.kind == kGeqrt || (throttle == 1 && it.kind == kTsqrt)))
-          atomicAdd(&smflag[smid & 255], 1);
         if constexpr (V2) {
           if (it.kind == kLarfb || it.kind == kSsrfb) {
             const int na = v2::active_warps<NB, MB, W>(it.col0, it.aux[0]);
@@ -270,11 +261,6 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     constexpr int NPAN = NB / KW;
     constexpr int PC = NPAN >= 3 ? NPAN - 3 : 0, PD = NPAN >= 2 ? NPAN - 2 : 0, PF = NPAN - 1;
     auto hook = [&](int p) {
-      if (throttle) {
-        if ((threadIdx.x & 31) == 0)
-          while (*reinterpret_cast<volatile int*>(&smflag[smid & 255]) > 0) __nanosleep(256);
-        __syncwarp();
-      }
       if (threadIdx.x != 0) return;
       if (p == PC) nxt = atomicAdd(next, 1);
       if (nxt >= nitems) return;
@@ -334,8 +320,6 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(done + it.task, 1);
-      if (throttle && (it.kind == kGeqrt || (throttle == 1 && it.kind == kTsqrt)))
-        atomicSub(&smflag[smid & 255], 1);
       if (prof) prof[3 * (size_t)i + 2] = globaltimer();
     }
     slot ^= 1;
@@ -363,9 +347,7 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
     if (g > 0 && g < grid) grid = g;
   }
   if (grid_out) *grid_out = grid;
-  const char* th = getenv("TILEQR_DAG_THROTTLE");
-  const int throttle = th ? atoi(th) : 0;
-  kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof, throttle, io);
+  kern<<<grid, kThreads, bytes, s>>>(items, nitems, next, done, IB, prof, io);
   TQ_LAUNCH_CHECK();
   return 0;
 }

@@ -224,10 +224,14 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       if (warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
       if (tid == 0) S.tau[jj] = tau;
     };
-#ifdef TILEQR_TSQRT_ROLLED  // diagnostic variant: TSQRT's step loop rolled too
+    // TSQRT: unrolled for IB <= 16; for IB >= 24 the unrolled loop's code
+    // size costs more than the loop (same-box A/B of the whole 10000^2
+    // factorization: IB=32 rolled 51.3 ms, unrolled 52.8; IB=16 rolled 52.9,
+    // unrolled 52.7)
+#ifdef TILEQR_TSQRT_ROLLED  // diagnostic variant: TSQRT's step loop rolled for every IB
     constexpr bool kUnrolled = false;
 #else
-    constexpr bool kUnrolled = TS;
+    constexpr bool kUnrolled = TS && IB <= 16;
 #endif
     if constexpr (kUnrolled) {
 #pragma unroll
