@@ -415,16 +415,19 @@ static int build_dag(FactorWS* ws, bool io) {
   const int P = std::max(1, nsm0 * dag::dag_ctas_per_sm(NB));
   const double cta_gflops = 220.0 / dag::dag_ctas_per_sm(NB);       // update rate per CTA
   const double dS = 4.0 * NB * NB * cols / cta_gflops;               // ns per SSRFB slab
-  // measured in the dataflow kernel at NB = 128 (10000^2): TSQRT sub-task
-  // ~2 us per column, GEQRT sub-task ~3.4 us per column (both sharing their SM
-  // with an update CTA), LARFB slab ~0.77 of an SSRFB slab; plus ~3 us of
-  // hand-off (release -> acquire -> operand loads) per item
-  double sT = 3000.0, sG = 5000.0, hand = 5000.0;
+  // measured in the dataflow kernel at NB = 128 (10000^2): TSQRT and GEQRT
+  // sub-tasks ~2-3 us per column (sharing their SM with an update CTA), LARFB
+  // slab ~0.77 of an SSRFB slab; plus ~3 us of hand-off (release -> acquire
+  // -> operand loads) per item.  The values below are the best of a sweep
+  // (tools/sim_sweep.sh; +-40 % moves the factorization by ~1 %)
+  double sT = 3000.0, sG = 3000.0, hand = 5000.0;
   if (dag::dag_ctas_per_sm(NB) == 1) sT = sG = 1500.0;  // a panel item has its SM alone
   if (const char* e = getenv("TILEQR_DAG_SIM")) sscanf(e, "%lf,%lf,%lf", &sT, &sG, &hand);  // diagnostics
   const double dL = 0.77 * dS + hand, dT = sT * SC + hand, dG = sG * SC + hand;
   const double dIO = 1.0e3 + (double)kIoTiles * NB * NB * 16 / 50.0;  // ~50 GB/s per CTA
-  const double tcol = (double)MT * NB * NB * 8 / 45.0;                  // ~45 GB/s host link
+  double h2d_gbs = 54.0;  // host link, measured while the kernel runs (54 GB/s; 30-100 in the sim: +-3 %)
+  if (const char* e = getenv("TILEQR_DAG_H2D_GBS")) h2d_gbs = atof(e);  // diagnostics
+  const double tcol = (double)MT * NB * NB * 8 / h2d_gbs;
   auto dur = [&](int kind) {
     switch (kind) {
       case dag::kSsrfb: return dS + hand;

@@ -33,3 +33,16 @@ st = sorted([r for r in recs if r[2] == "store"], key=lambda r: r[1])
 print("load items: first start %.3f last end %.3f" % (ld[0][0], max(r[1] for r in ld)))
 print("store items: first end %.3f last end %.3f" % (st[0][1], st[-1][1]))
 print("span %.3f" % max(r[1] for r in recs))
+# utilisation of the CTA slots per 2 ms (all kinds) -- where the host pipeline waits
+slots = torch.cuda.get_device_properties(0).multi_processor_count * 2
+span = max(r[1] for r in recs)
+nb_ = int(span / 2.0) + 1
+busy = [0.0] * nb_
+for r in recs:
+    t0, t1 = r[0], r[1]
+    b = int(t0 / 2.0)
+    while t0 < t1:
+        e = min(t1, (b + 1) * 2.0)
+        busy[b] += e - t0
+        t0, b = e, b + 1
+print("busy fraction per 2 ms:", " ".join("%.2f" % (x / (slots * 2.0)) for x in busy))
