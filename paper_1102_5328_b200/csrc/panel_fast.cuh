@@ -71,9 +71,19 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
   constexpr int kThreads = kWarps * 32;
   constexpr int RW = NB / kWarps;  // rows per warp in the factorization
   constexpr int RB = NB / 8;       // 8-row blocks in the trailing update
+  // TSQRT with IB <= 16: HL lane groups of IB lanes share a column (group h
+  // holds rows [w*RW + h*RL, w*RW + (h+1)*RL)), so no lane idles and the step
+  // issues RW/HL instead of RW shuffles and FMAs per warp; their partial dots
+  // are combined with shfl_xor (symmetric: every lane of a column gets the
+  // same bits).  GEQRT keeps one column per lane (its top-row slots).
+  constexpr int HL = (TS && IB <= 16 && 32 % IB == 0) ? 32 / IB : 1;
+  constexpr int RL = RW / HL;      // rows per lane
   FastSmem<NB, kWarps>& S = *reinterpret_cast<FastSmem<NB, kWarps>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int a = lane & 3, g = lane >> 2;
+  const int col = HL > 1 ? (lane % IB) : lane;  // the lane's panel column (>= IB: none)
+  const int hg = HL > 1 ? (lane / IB) : 0;      // its lane group
+  const int rbase = warp * RW + hg * RL;        // first row it holds
   double* const B = TS ? Bx : R;  // TSQRT: R tile + square tile B; GEQRT: the tile
 
   for (int e = tid; e < 32 * LDT; e += kThreads) S.Ts[e] = 0.0;  // zero padding for the T merges
@@ -124,10 +134,10 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
     // top[i / W] of warp i % W (a warp's rows leave in order: slot 0 is always
     // the next one, see the step); x[] holds only the rows below, which stay in
     // every reflector of the panel.
-    double x[RW];
+    double x[RL];
 #pragma unroll
-    for (int q = 0; q < RW; ++q)
-      x[q] = (lane < IB && (TS || warp * RW + q >= c0 + IB)) ? S.Vs[vsw(warp * RW + q, lane, LDV)] : 0.0;
+    for (int q = 0; q < RL; ++q)
+      x[q] = (col < IB && (TS || rbase + q >= c0 + IB)) ? S.Vs[vsw(rbase + q, col, LDV)] : 0.0;
     double top[TR];
 #pragma unroll
     for (int t = 0; t < TR; ++t) {
@@ -150,11 +160,11 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         for (int t = 0; t + 1 < TR; ++t) top[t] = top[t + 1];
         top[TR - 1] = 0.0;
       }
-      double vj[RW];
+      double vj[RL];
       double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
 #pragma unroll
-      for (int q = 0; q < RW; ++q) {
-        vj[q] = __shfl_sync(0xffffffffu, x[q], jj);
+      for (int q = 0; q < RL; ++q) {
+        vj[q] = __shfl_sync(0xffffffffu, x[q], jj + hg * IB);
         pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
       }
       double vt[TR];
@@ -165,13 +175,16 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
           pp[t & 3] = fma(vt[t], top[t], pp[t & 3]);
         }
       }
-      S.red[buf][warp][lane] = (pp[0] + pp[1]) + (pp[2] + pp[3]);
+      double part = (pp[0] + pp[1]) + (pp[2] + pp[3]);
+#pragma unroll
+      for (int o = IB; o < 32 && HL > 1; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (hg == 0) S.red[buf][warp][lane] = part;
       __syncthreads();
       double ps[kWarps], pd[kWarps];
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
         ps[w] = S.red[buf][w][jj];
-        pd[w] = S.red[buf][w][lane];
+        pd[w] = S.red[buf][w][col];
       }
 #pragma unroll
       for (int h = kWarps / 2; h > 0; h >>= 1)  // pairwise tree (fixed order: deterministic)
@@ -182,7 +195,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         }
       const double sigma = ps[0], d = pd[0];
       const double alpha = TS ? S.Rin[jj * LDR + jj] : S.rowj[buf][jj];
-      const double rjl = TS ? S.Rin[jj * LDR + lane] : S.rowj[buf][lane];
+      const double rjl = TS ? S.Rin[jj * LDR + col] : S.rowj[buf][col];
       double tau = 0.0, scal = 0.0, beta = alpha;
       if (sigma != 0.0) {
         // Reflector rule (R1) from one reciprocal square root and one
@@ -209,19 +222,19 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         scal = sg * rc;
       }
       const double w = fma(scal, d, rjl);
-      const double tw = lane < IB ? tau * w : 0.0;
+      const double tw = col < IB ? tau * w : 0.0;
       // select-free rank-1 update of the reflector rows, x += coef * vj:
       //   lane == jj: coef = scal - 1 (vj == x there: x becomes v2 = x2 * scal);
       //   lane >  jj: coef = -tw * scal;   lane < jj: coef = 0.
-      const double coef = (lane == jj) ? scal - 1.0 : (lane > jj ? -tw * scal : 0.0);
+      const double coef = (col == jj) ? scal - 1.0 : (col > jj ? -tw * scal : 0.0);
 #pragma unroll
-      for (int q = 0; q < RW; ++q) x[q] = fma(coef, vj[q], x[q]);
+      for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q]);
       if (!TS) {
 #pragma unroll
         for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t]);
       }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
-      if (warp == 0 && lane >= jj && lane < IB) S.Rout[jj * LDR + lane] = (lane == jj) ? beta : rjl - tw;
+      if (warp == 0 && hg == 0 && col >= jj && col < IB) S.Rout[jj * LDR + col] = (col == jj) ? beta : rjl - tw;
       if (tid == 0) S.tau[jj] = tau;
     };
     // TSQRT: unrolled for IB <= 16; for IB >= 24 the unrolled loop's code
@@ -250,8 +263,8 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 
     // ---- write the factored panel: registers -> smem -> global (coalesced) ----
 #pragma unroll
-    for (int q = 0; q < RW; ++q)  // GEQRT: the top rows were stored by the step loop
-      if (TS || warp * RW + q >= c0 + IB) S.Vs[vsw(warp * RW + q, lane, LDV)] = lane < IB ? x[q] : 0.0;
+    for (int q = 0; q < RL; ++q)  // GEQRT: the top rows were stored by the step loop
+      if (TS || rbase + q >= c0 + IB) S.Vs[vsw(rbase + q, col, LDV)] = col < IB ? x[q] : 0.0;
     __syncthreads();  // GEQRT: the top rows were stored as they left the reflector
     for (int idx = tid; idx < NB * IB; idx += kThreads) {
       const int c = idx / NB, r = idx - c * NB;
