@@ -57,6 +57,7 @@ struct FastSmem {
   double rowj[2][32];
   double tau[32];
   double Ws[kWarps][8 * LDW];
+  double Tsv[32 * LDT];  // T_p of the sub-task's earlier inner panels (step 3)
 };
 
 // Inner panels c0 = cbeg, cbeg+IB, ... < cend (the whole tile by default; the
@@ -94,6 +95,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #else
 #define TQ_PHASE(k) do { } while (0)
 #endif
+  const bool fuse = cend - cbeg > IB && cend - cbeg <= 32 && 32 % IB == 0;  // see step 3
   for (int c0 = cbeg; c0 < cend; c0 += IB) {
     // ---- stage the panel (coalesced) and, for TSQRT, the R block -------------
     // trailing columns of this inner panel -> L2 while the panel is factored
@@ -155,7 +157,9 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         // from Rout), then shifts its remaining top rows down one slot, so
         // every slot always holds a row below j (no dynamic register index)
         S.rowj[buf][lane] = top[0];
-        S.Vs[vsw(c0 + jj, lane, LDV)] = lane < IB ? top[0] : 0.0;
+        // columns >= IB: kept panels (step 3), or for IB = 24 the zero padding
+        // the packed copy takes
+        if (lane < IB || 32 % IB != 0) S.Vs[vsw(c0 + jj, lane, LDV)] = lane < IB ? top[0] : 0.0;
 #pragma unroll
         for (int t = 0; t + 1 < TR; ++t) top[t] = top[t + 1];
         top[TR - 1] = 0.0;
@@ -264,7 +268,8 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
     // ---- write the factored panel: registers -> smem -> global (coalesced) ----
 #pragma unroll
     for (int q = 0; q < RL; ++q)  // GEQRT: the top rows were stored by the step loop
-      if (TS || rbase + q >= c0 + IB) S.Vs[vsw(rbase + q, col, LDV)] = col < IB ? x[q] : 0.0;
+      if ((col < IB || 32 % IB != 0) && (TS || rbase + q >= c0 + IB))
+        S.Vs[vsw(rbase + q, col, LDV)] = col < IB ? x[q] : 0.0;
     __syncthreads();  // GEQRT: the top rows were stored as they left the reflector
     for (int idx = tid; idx < NB * IB; idx += kThreads) {
       const int c = idx / NB, r = idx - c * NB;
@@ -368,86 +373,118 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
     }
     __syncthreads();
     TQ_PHASE(3);
-    // ---- 3. trailing columns [c0+IB, NB): 8-column blocks per warp ------------
-    double* Wsw = S.Ws[warp];
-    const int nbi = IB / 8;
-    for (int cb = c0 + IB + 8 * warp; cb < NB; cb += 8 * kWarps) {
-      const int col = cb + g;
-      // GEQRT: rows above c0 of the trailing columns are R rows of earlier
-      // inner panels -- never loaded or stored here (a concurrent TSQRT
-      // sub-task of the DAG kernel may own them)
-      double acc[RB][2];
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        if (!TS && 8 * rb + 7 < c0) { acc[rb][0] = acc[rb][1] = 0.0; continue; }
-        const double2 v = __ldcg(reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)col * NB));
-        acc[rb][0] = v.x;
-        acc[rb][1] = v.y;
+    // ---- 3. trailing columns: 8-column blocks per warp ------------------------
+    // A sub-task of NPS <= 32/IB inner panels (the DAG kernel) updates, after
+    // panel j, only its own later columns [c0+IB, cend) ("near"); the columns
+    // [cend, NB) get all NPS panels in one pass after the last one ("far"):
+    // each column block crosses L2 once instead of NPS times, with the same
+    // operations in the same order (bitwise the per-panel result).  The
+    // earlier panels' V_p and T_p are kept for it in Vs columns
+    // [32 - IB(j+1), 32 - IB j) and Tsv rows [j IB, (j+1) IB).
+    const int jc = (c0 - cbeg) / IB;  // this panel's index in the sub-task
+    const bool last = c0 + IB >= cend;
+    if (fuse && !last) {  // read after later barriers only
+      const int off = 32 - IB * (jc + 1);
+      for (int e = tid; e < NB * IB; e += kThreads) {
+        const int r = e / IB, i = e - r * IB;
+        S.Vs[vsw(r, off + i, LDV)] = S.Vs[vsw(r, i, LDV)];
       }
-      // step A: W^T(col, i) = [TS: R(c0+i, col)] + sum_r C^T(col, r) V_p(r, i);
-      // two partial sums (k rows 2a and 2a+1) per output block
-      double wacc[4][2], wacc2[4][2];
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          wacc[nb][j] = (TS && nb < nbi) ? __ldcg(&R[(c0 + 8 * nb + 2 * a + j) + (size_t)col * NB]) : 0.0;
-          wacc2[nb][j] = 0.0;
-        }
-#pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        if (!TS && 8 * rb + 7 < c0) continue;
-#pragma unroll
-        for (int nb = 0; nb < 4; ++nb)
-          if (nb < nbi) {
-            dmma(wacc[nb][0], wacc[nb][1], acc[rb][0], S.Vs[vsw(8 * rb + 2 * a, 8 * nb + g, LDV)]);
-            dmma(wacc2[nb][0], wacc2[nb][1], acc[rb][1], S.Vs[vsw(8 * rb + 2 * a + 1, 8 * nb + g, LDV)]);
-          }
+      for (int e = tid; e < IB * IB; e += kThreads) {
+        const int r = e % IB, i = e / IB;
+        S.Tsv[jc * IB + r + i * LDT] = S.Ts[r + i * LDT];
       }
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb) {
-        wacc[nb][0] += wacc2[nb][0];
-        wacc[nb][1] += wacc2[nb][1];
-      }
-#pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
-        if (nb < nbi) {
-          Wsw[g * LDW + 8 * nb + 2 * a] = wacc[nb][0];
-          Wsw[g * LDW + 8 * nb + 2 * a + 1] = wacc[nb][1];
-        }
-      __syncwarp();
-      // step B: W'^T = W^T T_p (descending blocks, in place); TS: R(c0+i, col) -= W'
-      for (int nb = nbi - 1; nb >= 0; --nb) {
-        double o0 = 0.0, o1 = 0.0;
-        for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
-          dmma(o0, o1, Wsw[g * LDW + k4 + a], S.Ts[(k4 + a) + (8 * nb + g) * LDT]);
-        __syncwarp();
-        Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
-        Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
-        if (TS) {
-          double* r0 = &R[(c0 + 8 * nb + 2 * a) + (size_t)col * NB];
-          r0[0] = __ldcg(r0) - o0;
-          r0[1] = __ldcg(r0 + 1) - o1;
-        }
-        __syncwarp();
-      }
-      // step C: C^T(col, r) += (-W'^T)(col, i) V_p(r, i)
-      for (int k4 = 0; k4 < IB; k4 += 4) {
-        const double af = Wsw[g * LDW + k4 + a];
+    }
+    // apply panels j0..j1 of the sub-task, in order, to columns [lo, hi)
+    auto trailing = [&](const int lo, const int hi, const int j0, const int j1) {
+      double* Wsw = S.Ws[warp];
+      const int nbi = IB / 8;
+      const int rlo = cbeg + j0 * IB;
+      for (int cb = lo + 8 * warp; cb < hi; cb += 8 * kWarps) {
+        const int cc = cb + g;
+        // GEQRT: rows above the first applied panel of the trailing columns
+        // are R rows of earlier inner panels -- never loaded or stored here
+        // (a concurrent TSQRT sub-task of the DAG kernel may own them)
+        double acc[RB][2];
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
-          if (!TS && 8 * rb + 7 < c0) continue;
-          dmma(acc[rb][0], acc[rb][1], af, S.Vs[vsw(8 * rb + g, k4 + a, LDV)]);
+          if (!TS && 8 * rb + 7 < rlo) { acc[rb][0] = acc[rb][1] = 0.0; continue; }
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)cc * NB));
+          acc[rb][0] = v.x;
+          acc[rb][1] = v.y;
         }
-      }
+#pragma unroll 1
+        for (int j = j0; j <= j1; ++j) {
+          const int pc0 = cbeg + j * IB;
+          const int voff = (j == jc) ? 0 : 32 - IB * (j + 1);
+          const double* Tj = (j == jc) ? S.Ts : S.Tsv + j * IB;
+          // step A: W^T(col, i) = [TS: R(pc0+i, col)] + sum_r C^T(col, r) V_p(r, i);
+          // two partial sums (k rows 2a and 2a+1) per output block
+          double wacc[4][2], wacc2[4][2];
 #pragma unroll
-      for (int rb = 0; rb < RB; ++rb) {
-        if (!TS && 8 * rb + 7 < c0) continue;
-        *reinterpret_cast<double2*>(B + 8 * rb + 2 * a + (size_t)col * NB) =
-            make_double2(acc[rb][0], acc[rb][1]);
+          for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              wacc[nb][jj] = (TS && nb < nbi) ? __ldcg(&R[(pc0 + 8 * nb + 2 * a + jj) + (size_t)cc * NB]) : 0.0;
+              wacc2[nb][jj] = 0.0;
+            }
+#pragma unroll
+          for (int rb = 0; rb < RB; ++rb) {
+            if (!TS && 8 * rb + 7 < pc0) continue;
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+              if (nb < nbi) {
+                dmma(wacc[nb][0], wacc[nb][1], acc[rb][0], S.Vs[vsw(8 * rb + 2 * a, voff + 8 * nb + g, LDV)]);
+                dmma(wacc2[nb][0], wacc2[nb][1], acc[rb][1], S.Vs[vsw(8 * rb + 2 * a + 1, voff + 8 * nb + g, LDV)]);
+              }
+          }
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            wacc[nb][0] += wacc2[nb][0];
+            wacc[nb][1] += wacc2[nb][1];
+          }
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb)
+            if (nb < nbi) {
+              Wsw[g * LDW + 8 * nb + 2 * a] = wacc[nb][0];
+              Wsw[g * LDW + 8 * nb + 2 * a + 1] = wacc[nb][1];
+            }
+          __syncwarp();
+          // step B: W'^T = W^T T_p (descending blocks, in place); TS: R(pc0+i, col) -= W'
+          for (int nb = nbi - 1; nb >= 0; --nb) {
+            double o0 = 0.0, o1 = 0.0;
+            for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
+              dmma(o0, o1, Wsw[g * LDW + k4 + a], Tj[(k4 + a) + (8 * nb + g) * LDT]);
+            __syncwarp();
+            Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
+            Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
+            if (TS) {
+              double* r0 = &R[(pc0 + 8 * nb + 2 * a) + (size_t)cc * NB];
+              r0[0] = __ldcg(r0) - o0;
+              r0[1] = __ldcg(r0 + 1) - o1;
+            }
+            __syncwarp();
+          }
+          // step C: C^T(col, r) += (-W'^T)(col, i) V_p(r, i)
+          for (int k4 = 0; k4 < IB; k4 += 4) {
+            const double af = Wsw[g * LDW + k4 + a];
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) {
+              if (!TS && 8 * rb + 7 < pc0) continue;
+              dmma(acc[rb][0], acc[rb][1], af, S.Vs[vsw(8 * rb + g, voff + k4 + a, LDV)]);
+            }
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int rb = 0; rb < RB; ++rb) {
+          if (!TS && 8 * rb + 7 < rlo) continue;
+          *reinterpret_cast<double2*>(B + 8 * rb + 2 * a + (size_t)cc * NB) = make_double2(acc[rb][0], acc[rb][1]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-    }
+    };
+    trailing(c0 + IB, fuse ? cend : NB, jc, jc);
+    if (fuse && last) trailing(cend, NB, 0, jc);  // the kept panels were written before earlier barriers
     __syncthreads();  // trailing writes visible before the next panel is staged
     TQ_PHASE(4);
   }
