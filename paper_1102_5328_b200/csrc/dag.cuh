@@ -262,7 +262,10 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     constexpr int PC = NPAN >= 3 ? NPAN - 3 : 0, PD = NPAN >= 2 ? NPAN - 2 : 0, PF = NPAN - 1;
     auto hook = [&](int p) {
       if (threadIdx.x != 0) return;
-      if (p == PC) nxt = atomicAdd(next, 1);
+      if (p == PC) {
+        nxt = atomicAdd(next, 1);
+        if constexpr (PC != PD) return;  // its result is first needed one panel later
+      }
       if (nxt >= nitems) return;
       if (p == PD) fetch_desc(nxt, slot ^ 1);
 #ifndef TILEQR_NO_HOOK_PREFETCH
