@@ -105,28 +105,63 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
                    "r"((uint32_t)((NB - c0 - IB) * NB * sizeof(double)))
                    : "memory");
 #endif
-    // panel columns: 8 loads in flight per thread before the shared stores
-    for (int idx0 = tid; idx0 < NB * IB; idx0 += 8 * kThreads) {
-      double v[8];
+    if constexpr (IB <= 16) {
+      // panel columns (and for TSQRT the R block): up to 16 + 2 loads in flight
+      // per thread before the shared stores -- the stage is one L2 round trip
+      constexpr int UV = (NB * IB + kThreads - 1) / kThreads < 16 ? (NB * IB + kThreads - 1) / kThreads : 16;
+      constexpr int UR = (IB * IB + kThreads - 1) / kThreads;
+      for (int idx0 = tid; idx0 < NB * IB; idx0 += UV * kThreads) {
+        double v[UV];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = idx0 + u * kThreads;
-        // GEQRT: rows above c0 are R rows of earlier inner panels that a
-        // concurrent TSQRT sub-task may be rewriting -- never read them (a
-        // stale line could even land in the L1 another CTA of this SM reads
-        // after its acquire); their operand entries are 0 anyway
-        v[u] = (idx < NB * IB && (TS || idx % NB >= c0)) ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
-      }
+        for (int u = 0; u < UV; ++u) {
+          const int idx = idx0 + u * kThreads;
+          // GEQRT: rows above c0 are R rows of earlier inner panels that a
+          // concurrent TSQRT sub-task may be rewriting -- never read them (a
+          // stale line could even land in the L1 another CTA of this SM reads
+          // after its acquire); their operand entries are 0 anyway
+          v[u] = (idx < NB * IB && (TS || idx % NB >= c0)) ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+        }
+        double rv[UR];
+        if (TS && idx0 == tid) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = idx0 + u * kThreads;
-        if (idx < NB * IB) S.Vs[vsw(idx % NB, idx / NB, LDV)] = v[u];
+          for (int u = 0; u < UR; ++u) {
+            const int idx = tid + u * kThreads, c = idx / IB, i = idx - c * IB;
+            rv[u] = (idx < IB * IB && i <= c) ? __ldcg(&R[(c0 + i) + (size_t)(c0 + c) * NB]) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UV; ++u) {
+          const int idx = idx0 + u * kThreads;
+          if (idx < NB * IB) S.Vs[vsw(idx % NB, idx / NB, LDV)] = v[u];
+        }
+        if (TS && idx0 == tid) {
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int idx = tid + u * kThreads, c = idx / IB, i = idx - c * IB;
+            if (idx < IB * IB) S.Rin[i * LDR + c] = rv[u];
+          }
+        }
       }
-    }
-    if (TS) {
-      for (int idx = tid; idx < IB * IB; idx += kThreads) {
-        const int c = idx / IB, i = idx - c * IB;
-        S.Rin[i * LDR + c] = (i <= c) ? __ldcg(&R[(c0 + i) + (size_t)(c0 + c) * NB]) : 0.0;
+    } else {  // IB > 16: 8 loads in flight, R block after (same-box A/B: the batched stage is slower here)
+      // panel columns: 8 loads in flight per thread before the shared stores
+      for (int idx0 = tid; idx0 < NB * IB; idx0 += 8 * kThreads) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = idx0 + u * kThreads;
+          v[u] = (idx < NB * IB && (TS || idx % NB >= c0)) ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = idx0 + u * kThreads;
+          if (idx < NB * IB) S.Vs[vsw(idx % NB, idx / NB, LDV)] = v[u];
+        }
+      }
+      if (TS) {
+        for (int idx = tid; idx < IB * IB; idx += kThreads) {
+          const int c = idx / IB, i = idx - c * IB;
+          S.Rin[i * LDR + c] = (i <= c) ? __ldcg(&R[(c0 + i) + (size_t)(c0 + c) * NB]) : 0.0;
+        }
       }
     }
     __syncthreads();
@@ -419,12 +454,13 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
           const double* Tj = (j == jc) ? S.Ts : S.Tsv + j * IB;
           // step A: W^T(col, i) = [TS: R(pc0+i, col)] + sum_r C^T(col, r) V_p(r, i);
           // two partial sums (k rows 2a and 2a+1) per output block
-          double wacc[4][2], wacc2[4][2];
+          double wacc[4][2], wacc2[4][2], rk[4][2];  // rk: the R rows, reused by step B
 #pragma unroll
           for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
             for (int jj = 0; jj < 2; ++jj) {
-              wacc[nb][jj] = (TS && nb < nbi) ? __ldcg(&R[(pc0 + 8 * nb + 2 * a + jj) + (size_t)cc * NB]) : 0.0;
+              rk[nb][jj] = (TS && nb < nbi) ? __ldcg(&R[(pc0 + 8 * nb + 2 * a + jj) + (size_t)cc * NB]) : 0.0;
+              wacc[nb][jj] = rk[nb][jj];
               wacc2[nb][jj] = 0.0;
             }
 #pragma unroll
@@ -450,19 +486,38 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
             }
           __syncwarp();
           // step B: W'^T = W^T T_p (descending blocks, in place); TS: R(pc0+i, col) -= W'
-          for (int nb = nbi - 1; nb >= 0; --nb) {
-            double o0 = 0.0, o1 = 0.0;
-            for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
-              dmma(o0, o1, Wsw[g * LDW + k4 + a], Tj[(k4 + a) + (8 * nb + g) * LDT]);
-            __syncwarp();
-            Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
-            Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
-            if (TS) {
-              double* r0 = &R[(pc0 + 8 * nb + 2 * a) + (size_t)cc * NB];
-              r0[0] = __ldcg(r0) - o0;
-              r0[1] = __ldcg(r0 + 1) - o1;
+          if constexpr (IB <= 16) {  // unrolled: the R rows come from rk (registers)
+#pragma unroll
+            for (int nb = 3; nb >= 0; --nb) {
+              if (nb >= nbi) continue;
+              double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+              for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
+                dmma(o0, o1, Wsw[g * LDW + k4 + a], Tj[(k4 + a) + (8 * nb + g) * LDT]);
+              __syncwarp();
+              Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
+              Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
+              if (TS) {  // R(pc0+i, col) -= W'  (this warp owns the column)
+                double* r0 = &R[(pc0 + 8 * nb + 2 * a) + (size_t)cc * NB];
+                *reinterpret_cast<double2*>(r0) = make_double2(rk[nb][0] - o0, rk[nb][1] - o1);
+              }
+              __syncwarp();
             }
-            __syncwarp();
+          } else {  // IB > 16: rolled (code size; same-box A/B), R rows reloaded
+            for (int nb = nbi - 1; nb >= 0; --nb) {
+              double o0 = 0.0, o1 = 0.0;
+              for (int k4 = 0; k4 < 8 * nb + 8; k4 += 4)
+                dmma(o0, o1, Wsw[g * LDW + k4 + a], Tj[(k4 + a) + (8 * nb + g) * LDT]);
+              __syncwarp();
+              Wsw[g * LDW + 8 * nb + 2 * a] = -o0;
+              Wsw[g * LDW + 8 * nb + 2 * a + 1] = -o1;
+              if (TS) {
+                double* r0 = &R[(pc0 + 8 * nb + 2 * a) + (size_t)cc * NB];
+                r0[0] = __ldcg(r0) - o0;
+                r0[1] = __ldcg(r0 + 1) - o1;
+              }
+              __syncwarp();
+            }
           }
           // step C: C^T(col, r) += (-W'^T)(col, i) V_p(r, i)
           for (int k4 = 0; k4 < IB; k4 += 4) {
