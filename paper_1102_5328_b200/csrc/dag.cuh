@@ -38,26 +38,34 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-// Update items of NB <= 128 run the barrier-free packed-reflector body
-// (update_v2.cuh, the whole packed tile staged by TMA); larger NB the staged
-// double-buffered body (update_dmma.cuh).
+// Update items run the barrier-free packed-reflector body (update_v2.cuh,
+// column groups of the packed tile streamed through a TMA ring) for every
+// NB of the DAG kernel (TILEQR_DAG_STAGED: the staged double-buffered body of
+// update_dmma.cuh for NB > 128, the previous design, for comparison).
 template <int NB>
-constexpr bool dag_v2() { return NB <= 128; }
+constexpr bool dag_v2() {
+#ifdef TILEQR_DAG_STAGED
+  return NB <= 128;
+#else
+  return NB <= 256;
+#endif
+}
 
-// Ring stages of the packed reflector tile per CTA: as many as fit next to
-// the panel body's shared memory in ~110 KB (2 CTAs per SM), at least 2.
+// Ring stages of the packed reflector tile per CTA: as many as fit in ~110 KB
+// (2 CTAs per SM, NB <= 128) or ~200 KB (1 CTA), at least 2, at most 8.
 template <int NB, int KW>
 constexpr int dag_stages() {
-  if constexpr (NB <= 128 && NB % KW == 0) {
+  if constexpr (dag_v2<NB>() && NB % KW == 0) {
     using P = v2::Pk<NB, KW>;
     constexpr size_t stage = (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double);
-    constexpr size_t budget = 110 * 1024;
+    constexpr size_t budget = dag_ctas_per_sm(NB) == 2 ? 110 * 1024 : 200 * 1024;
 #ifdef TILEQR_FULL_RING
     constexpr int s = P::NG;
 #else
     constexpr int s = (int)(budget / stage);
 #endif
-    return s < 2 ? 2 : (s > P::NG ? P::NG : s);
+    constexpr int s8 = s > 8 ? 8 : s;  // the kernel's mbarrier arrays hold 8
+    return s8 < 2 ? 2 : (s8 > P::NG ? P::NG : s8);
   } else {
     return 1;
   }

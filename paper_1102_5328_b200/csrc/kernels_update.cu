@@ -209,14 +209,15 @@ int launch_ssrfb(bool trans, int NB, int IB, int batch, const double* const* V2,
                               double* const* C2, cudaStream_t s);                                   \
   int launch_pack_nb##nb(bool larfb, int IB, int batch, const double* const* V, const double* const* T, \
                          double* const* Pk, cudaStream_t s);
-TQ_DECL_PK(32) TQ_DECL_PK(64) TQ_DECL_PK(96) TQ_DECL_PK(128)
+TQ_DECL_PK(32) TQ_DECL_PK(64) TQ_DECL_PK(96) TQ_DECL_PK(128) TQ_DECL_PK(160) TQ_DECL_PK(192) TQ_DECL_PK(224)
+TQ_DECL_PK(256)
 #undef TQ_DECL_PK
 
 bool v2_supported(int NB, int IB) {
   if (force_simt()) return false;
   const char* e = getenv("TILEQR_NO_V2");
   if (e && e[0] == '1') return false;
-  return (NB == 32 || NB == 64 || NB == 96 || NB == 128) && IB % 8 == 0 && IB >= 8 && IB <= 32 && NB % IB == 0;
+  return NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB >= 8 && IB <= 32 && NB % IB == 0;
 }
 
 size_t v2_pk_doubles(int NB, int IB) {
@@ -234,7 +235,11 @@ int launch_update_pk(bool larfb, int NB, int IB, int batch, const double* const*
     case 64: return launch_update_pk_nb64(larfb, IB, batch, Pk, C1, C2, s);
     case 96: return launch_update_pk_nb96(larfb, IB, batch, Pk, C1, C2, s);
     case 128: return launch_update_pk_nb128(larfb, IB, batch, Pk, C1, C2, s);
-    default: set_error("packed update: NB not in {32, 64, 96, 128}"); return TILEQR_ERR_CUDA;
+    case 160: return launch_update_pk_nb160(larfb, IB, batch, Pk, C1, C2, s);
+    case 192: return launch_update_pk_nb192(larfb, IB, batch, Pk, C1, C2, s);
+    case 224: return launch_update_pk_nb224(larfb, IB, batch, Pk, C1, C2, s);
+    case 256: return launch_update_pk_nb256(larfb, IB, batch, Pk, C1, C2, s);
+    default: set_error("packed update: NB not in {32, 64, ..., 256}"); return TILEQR_ERR_CUDA;
   }
 }
 
@@ -246,7 +251,11 @@ int launch_pack(bool larfb, int NB, int IB, int batch, const double* const* V, c
     case 64: return launch_pack_nb64(larfb, IB, batch, V, T, Pk, s);
     case 96: return launch_pack_nb96(larfb, IB, batch, V, T, Pk, s);
     case 128: return launch_pack_nb128(larfb, IB, batch, V, T, Pk, s);
-    default: set_error("pack: NB not in {32, 64, 96, 128}"); return TILEQR_ERR_CUDA;
+    case 160: return launch_pack_nb160(larfb, IB, batch, V, T, Pk, s);
+    case 192: return launch_pack_nb192(larfb, IB, batch, V, T, Pk, s);
+    case 224: return launch_pack_nb224(larfb, IB, batch, V, T, Pk, s);
+    case 256: return launch_pack_nb256(larfb, IB, batch, V, T, Pk, s);
+    default: set_error("pack: NB not in {32, 64, ..., 256}"); return TILEQR_ERR_CUDA;
   }
 }
 

@@ -401,7 +401,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       const int i = e / IB, r = e - i * IB;
       Tg[(size_t)(c0 + i) * IB + r] = (r <= i) ? S.Ts[r + i * LDT] : 0.0;
     }
-    if constexpr (NB <= 128) if (Vpk) {  // packed copy of V_p / T_p for the barrier-free update (update_v2.cuh)
+    if (Vpk) {  // packed copy of V_p / T_p for the barrier-free update (update_v2.cuh)
       auto vf = [&](int r, int i) { return S.Vs[vsw(r, i, LDV)]; };
       auto tf = [&](int l, int i) { return S.Ts[l + i * LDT]; };
       v2::pack_panel<NB, IB, kThreads>(Vpk, c0 / IB, vf, tf);

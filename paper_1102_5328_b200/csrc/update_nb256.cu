@@ -3,6 +3,7 @@
 // compiles them in parallel).
 #include "dag.cuh"
 #include "update_dmma.cuh"
+#include "update_v2.cuh"
 
 namespace tileqr {
 int launch_update_nb256(bool trans, bool larfb, int IB, int batch, const double* const* V,
@@ -13,5 +14,13 @@ int launch_update_nb256(bool trans, bool larfb, int IB, int batch, const double*
 int launch_dag_nb256(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
                      unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io) {
   return dag::launch_dag_nb<256>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+}
+int launch_update_pk_nb256(bool larfb, int IB, int batch, const double* const* Pk, double* const* C1,
+                          double* const* C2, cudaStream_t s) {
+  return v2::launch_update_v2<256>(larfb, IB, batch, Pk, C1, C2, s);
+}
+int launch_pack_nb256(bool larfb, int IB, int batch, const double* const* V, const double* const* T,
+                     double* const* Pk, cudaStream_t s) {
+  return v2::launch_pack<256>(larfb, IB, batch, V, T, Pk, s);
 }
 }  // namespace tileqr

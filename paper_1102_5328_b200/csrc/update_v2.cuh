@@ -387,8 +387,19 @@ constexpr int kWarpsB = 8;  // warps per CTA of the batched v2 kernels (same geo
 
 __host__ __device__ constexpr int v2_mb(int NB) { return (NB == 96 || NB == 128) ? 2 : 1; }
 
+// ring stages of the batched kernel: the whole packed tile when it fits
+// (NB <= 128), else as many column groups as fit in ~200 KB (refilled by TMA
+// as the panels advance, as in the DAG kernel)
 template <int NB, int IB>
-constexpr size_t v2_smem_bytes() { return Ring<NB, IB, Pk<NB, IB>::NG>::bytes; }
+constexpr int v2_stages() {
+  using P = Pk<NB, IB>;
+  constexpr size_t stage = (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double);
+  constexpr int s = (int)((200 * 1024) / stage);
+  return s >= P::NG ? P::NG : (s < 2 ? 2 : s);
+}
+
+template <int NB, int IB>
+constexpr size_t v2_smem_bytes() { return Ring<NB, IB, v2_stages<NB, IB>()>::bytes; }
 
 // warps of a CTA (W warps of 8*MB columns from col0) that own columns < NB
 template <int NB, int MB, int W>
@@ -402,7 +413,7 @@ template <int NB, int IB, bool LARFB>
 __global__ void __launch_bounds__(kWarpsB * 32, 1)
 update_v2_kernel(const double* const* Pkp, double* const* C1p, double* const* C2p) {
   constexpr int MB = v2_mb(NB);
-  constexpr int S = Pk<NB, IB>::NG;  // whole tile resident
+  constexpr int S = v2_stages<NB, IB>();  // whole tile resident for NB <= 128
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[S], empty[S];
   const int b = blockIdx.y;

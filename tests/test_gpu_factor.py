@@ -76,6 +76,8 @@ CASES = [
     (256, 256, 64, 1, 18),     # IB = 1
     (512, 512, 160, 40, 19),
     (384, 384, 192, 64, 20),
+    (600, 600, 256, 16, 22),   # NB > 128 on the packed update (dataflow kernel)
+    (500, 500, 160, 32, 23),
     (200, 200, 48, 6, 21),     # SIMT path (NB % 32 != 0)
     (64, 64, 64, 16, 22),      # single tile
     (1, 1, 32, 8, 23),
@@ -181,6 +183,8 @@ DAG_CASES = [
     (400, 900, 96, 32, 53),    # wide, NB=96 (2 update slabs of 8 warps)
     (1000, 1000, 192, 24, 54), # 3 column slabs per update
     (2048, 2048, 64, 8, 55),   # 32 x 32 tiles: ~11k tasks in flight
+    (1100, 1100, 256, 16, 56), # NB > 128: packed update through a refilled TMA ring, 8 warps
+    (700, 1000, 160, 32, 57),  # NB = 160, wide, ragged last slab
 ]
 
 

@@ -152,7 +152,7 @@ def test_rng_matches_synth_inputs(tq):
     assert np.array_equal(got, si.uniform(m, n, 4, offset=123))  # bit-exact
 
 
-PACKED = [(nb, ib) for nb in (32, 64, 96, 128) for ib in (8, 16, 24, 32) if nb % ib == 0]
+PACKED = [(nb, ib) for nb in (32, 64, 96, 128, 160, 192, 224, 256) for ib in (8, 16, 24, 32) if nb % ib == 0]
 
 
 @pytest.mark.parametrize("nb,ib", PACKED)
