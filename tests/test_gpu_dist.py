@@ -29,7 +29,8 @@ def local_to_lapack(buf, n, nb, mt, nloc):
     return full[:n, :n]
 
 
-@pytest.mark.parametrize("n,nb,ib", [(512, 128, 32), (600, 128, 16), (700, 64, 16), (300, 96, 12)])
+@pytest.mark.parametrize("n,nb,ib", [(512, 128, 32), (600, 128, 16), (700, 64, 16), (300, 96, 12),
+                                     (800, 256, 16), (500, 160, 32)])
 def test_dist_world1_bitwise_equals_factor(tq, n, nb, ib):
     mt = -(-n // nb)
     nloc = tq.dist_local_cols(n, nb)
