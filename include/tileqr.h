@@ -180,7 +180,10 @@ int tileqr_update_packed_batched(int larfb, int NB, int IB, int batch, const dou
  *     TILEQR_TUNE_SMALL_IB=1), 50 back-to-back launches on the same buffers
  *     ("No Flush"); rate = 50*batch*4*NB^3/t.
  *   Pre-selection: Property 1, upper convex hull (Property 2), then Heuristic
- *     0/1/2, cap 8.
+ *     0/1/2, cap 8.  Property 1 counts the IB values
+ *     whose Step-1 rate is within 0.5 % of the NB's best as tied and keeps
+ *     the largest (R13/R18: closer rates are below the timing's
+ *     repeatability; env TILEQR_TUNE_TIE sets the relative width).
  *   Step 2: for N' on a ladder ascending to N, time
  *     tileqr_factor 6x per surviving candidate (median), then drop NB2 when
  *     some NB1 > NB2 is strictly faster (Property 3, if payg != 0).
@@ -199,6 +202,13 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
  * out_nb/out_ib/out_gflops (capacity n) and their count to *n_out. */
 int tileqr_preselect(int n, const int* h_nb, const int* h_ib, const double* h_gflops, int heuristic,
                      int cap, int* h_out_nb, int* h_out_ib, double* h_out_gflops, int* n_out);
+/* Same with a Property-1 tie width: per NB, every IB whose rate is
+ * >= (1 - tie_rel) * the NB's best rate is tied and the largest is kept
+ * (tie_rel = 0: exact ties only, as tileqr_preselect).  Errors: as
+ * tileqr_preselect, -7 tie_rel not in [0, 1), -8 NULL outputs. */
+int tileqr_preselect_tie(int n, const int* h_nb, const int* h_ib, const double* h_gflops, int heuristic,
+                         int cap, double tie_rel, int* h_out_nb, int* h_out_ib, double* h_out_gflops,
+                         int* n_out);
 /* Property 3 prune: keep[i] = 0 when some j has nb[j] > nb[i] and
  * gflops[j] > gflops[i]; else 1. */
 int tileqr_payg_prune(int n, const int* h_nb, const double* h_gflops, int* h_keep);

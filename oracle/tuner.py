@@ -10,20 +10,26 @@ from __future__ import annotations
 from fractions import Fraction
 
 
-def orthogonal_prune(samples):
+def orthogonal_prune(samples, tie_rel: float = 0.0):
     """Property 1: per NB keep the IB with the highest rate.
 
-    samples: iterable of (nb, ib, gflops).  Ties -> larger IB.
-    Returns [(nb, ib, gflops)] sorted by nb.
+    samples: iterable of (nb, ib, gflops).  Ties -> larger IB; with
+    tie_rel > 0 every IB whose rate is >= (1 - tie_rel) * the NB's best rate
+    counts as tied (R18: rates closer than the timing's
+    repeatability are not distinguishable).  Returns [(nb, ib, gflops)] sorted
+    by nb, gflops being the kept IB's own rate.
     """
-    best = {}
+    rates = {}
     for nb, ib, g in samples:
-        cur = best.get(nb)
-        if cur is None or g > cur[1] or (g == cur[1] and ib > cur[0]):
-            best[nb] = (ib, g)
-    if not best:
+        rates.setdefault(nb, []).append((ib, g))
+    if not rates:
         raise ValueError("empty dataset")
-    return [(nb, best[nb][0], best[nb][1]) for nb in sorted(best)]
+    out = []
+    for nb in sorted(rates):
+        gmax = max(g for _, g in rates[nb])
+        ib, g = max((ib, g) for ib, g in rates[nb] if g >= gmax * (1.0 - tie_rel))
+        out.append((nb, ib, g))
+    return out
 
 
 def _cross(o, a, b):
@@ -92,9 +98,9 @@ def heuristic2(hull, cap: int = 8):
     return [hull[i] for i in sorted(best.values())]
 
 
-def preselect(samples, heuristic: int = 2, cap: int = 8):
+def preselect(samples, heuristic: int = 2, cap: int = 8, tie_rel: float = 0.0):
     """Step 1 pre-selection: Property 1 -> hull -> H0/H1/H2."""
-    hull = upper_hull(orthogonal_prune(samples))
+    hull = upper_hull(orthogonal_prune(samples, tie_rel))
     if heuristic == 0:
         return hull
     if heuristic == 1:

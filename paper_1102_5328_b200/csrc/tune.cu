@@ -33,12 +33,20 @@ struct Pt {
   double g;
 };
 
-std::vector<Pt> orthogonal_prune(const std::vector<Pt>& in) {
+// Property 1: per NB the IB of the highest rate; every IB within tie_rel of
+// that rate counts as tied and the largest tied IB is kept (R13,
+// R18), with its own rate.
+std::vector<Pt> orthogonal_prune(const std::vector<Pt>& in, double tie_rel) {
+  std::map<int, double> gmax;
+  for (const Pt& p : in) {
+    auto it = gmax.find(p.nb);
+    if (it == gmax.end() || p.g > it->second) gmax[p.nb] = p.g;
+  }
   std::map<int, Pt> best;
   for (const Pt& p : in) {
+    if (!(p.g >= gmax[p.nb] * (1.0 - tie_rel))) continue;
     auto it = best.find(p.nb);
-    if (it == best.end() || p.g > it->second.g || (p.g == it->second.g && p.ib > it->second.ib))
-      best[p.nb] = p;
+    if (it == best.end() || p.ib > it->second.ib || (p.ib == it->second.ib && p.g > it->second.g)) best[p.nb] = p;
   }
   std::vector<Pt> out;
   for (auto& kv : best) out.push_back(kv.second);
@@ -102,8 +110,8 @@ std::vector<Pt> heuristic2(const std::vector<Pt>& h, int cap) {
   return out;
 }
 
-std::vector<Pt> preselect(const std::vector<Pt>& samples, int heuristic, int cap) {
-  std::vector<Pt> hull = upper_hull(orthogonal_prune(samples));
+std::vector<Pt> preselect(const std::vector<Pt>& samples, int heuristic, int cap, double tie_rel) {
+  std::vector<Pt> hull = upper_hull(orthogonal_prune(samples, tie_rel));
   if (heuristic == 1) return heuristic1(hull, cap);
   if (heuristic == 2) return heuristic2(hull, cap);
   return hull;
@@ -135,16 +143,24 @@ extern "C" {
 
 int tileqr_preselect(int n, const int* h_nb, const int* h_ib, const double* h_gflops, int heuristic,
                      int cap, int* h_out_nb, int* h_out_ib, double* h_out_gflops, int* n_out) {
+  return tileqr_preselect_tie(n, h_nb, h_ib, h_gflops, heuristic, cap, 0.0, h_out_nb, h_out_ib, h_out_gflops,
+                              n_out);
+}
+
+int tileqr_preselect_tie(int n, const int* h_nb, const int* h_ib, const double* h_gflops, int heuristic,
+                         int cap, double tie_rel, int* h_out_nb, int* h_out_ib, double* h_out_gflops,
+                         int* n_out) {
   if (n < 1) { set_error("tileqr_preselect: empty dataset"); return -1; }
   if (!h_nb) return -2;
   if (!h_ib) return -3;
   if (!h_gflops) return -4;
   if (heuristic < 0 || heuristic > 2) return -5;
   if (cap < 1) return -6;
-  if (!h_out_nb || !h_out_ib || !h_out_gflops || !n_out) return -7;
+  if (!(tie_rel >= 0.0 && tie_rel < 1.0)) return -7;
+  if (!h_out_nb || !h_out_ib || !h_out_gflops || !n_out) return -8;
   std::vector<Pt> s;
   for (int i = 0; i < n; ++i) s.push_back({h_nb[i], h_ib[i], h_gflops[i]});
-  std::vector<Pt> out = preselect(s, heuristic, cap);
+  std::vector<Pt> out = preselect(s, heuristic, cap, tie_rel);
   for (size_t i = 0; i < out.size(); ++i) {
     h_out_nb[i] = out[i].nb;
     h_out_ib[i] = out[i].ib;
@@ -302,7 +318,12 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   pkbuf = nullptr;
   cudaFree(pkp);
   pkp = nullptr;
-  std::vector<Pt> cand = preselect(samples, heuristic, 8);
+  // Property-1 ties within the Step-1 timing's repeatability (R18;
+  // TILEQR_TUNE_TIE overrides the relative width)
+  double tie_rel = 0.005;
+  if (const char* e = getenv("TILEQR_TUNE_TIE")) tie_rel = atof(e);
+  if (!(tie_rel >= 0.0 && tie_rel < 1.0)) tie_rel = 0.005;
+  std::vector<Pt> cand = preselect(samples, heuristic, 8, tie_rel);
 
   // ---- Step 2: factorizations on a ladder ascending to N --------------------
   std::vector<int64_t> ladder;

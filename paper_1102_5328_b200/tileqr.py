@@ -47,6 +47,7 @@ _SIGS = {
     "tileqr_update_packed_batched": ([_i, _i, _i, _i, _p, _p, _p, _p], _i),
     "tileqr_tune": ([_i64, _i64, _i, _i, _i, _PI, _PI, ctypes.c_char_p], _i),
     "tileqr_preselect": ([_i, _PI, _PI, _PD, _i, _i, _PI, _PI, _PD, _PI], _i),
+    "tileqr_preselect_tie": ([_i, _PI, _PI, _PD, _i, _i, ctypes.c_double, _PI, _PI, _PD, _PI], _i),
     "tileqr_payg_prune": ([_i, _PI, _PD, _PI], _i),
     "tileqr_num_levels": ([_i64, _i64, ctypes.POINTER(_i64)], _i),
     "tileqr_dist_init": ([_i, _i, _p, _i], _i),
@@ -248,16 +249,16 @@ def tune(m: int, n: int, ngpus: int = 1, heuristic: int = 2, payg: bool = True,
     return nb.value, ib.value
 
 
-def preselect(samples, heuristic: int = 2, cap: int = 8):
-    """Host-only Step-1 pre-selection; samples [(nb, ib, gflops)]."""
+def preselect(samples, heuristic: int = 2, cap: int = 8, tie_rel: float = 0.0):
+    """Host-only Step-1 pre-selection; samples [(nb, ib, gflops)]; tie_rel: Property-1 tie width."""
     n = len(samples)
     nb = (ctypes.c_int * n)(*[s[0] for s in samples])
     ib = (ctypes.c_int * n)(*[s[1] for s in samples])
     g = (ctypes.c_double * n)(*[s[2] for s in samples])
     onb, oib, og = (ctypes.c_int * n)(), (ctypes.c_int * n)(), (ctypes.c_double * n)()
     cnt = ctypes.c_int()
-    _check(_lib.tileqr_preselect(n, nb, ib, g, heuristic, cap, onb, oib, og, ctypes.byref(cnt)),
-           "tileqr_preselect")
+    _check(_lib.tileqr_preselect_tie(n, nb, ib, g, heuristic, cap, tie_rel, onb, oib, og, ctypes.byref(cnt)),
+           "tileqr_preselect_tie")
     return [(onb[i], oib[i], og[i]) for i in range(cnt.value)]
 
 

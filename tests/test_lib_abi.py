@@ -80,6 +80,8 @@ def test_preselect_matches_oracle(tq):
             got = tq.preselect(samples, h, cap)
             exp = tuner.preselect(samples, h, cap)
             assert got == exp, (trial, h, cap)
+            tie = rnd.choice([0.005, 0.05, 0.3])
+            assert tq.preselect(samples, h, cap, tie) == tuner.preselect(samples, h, cap, tie), (trial, h, tie)
 
 
 def test_payg_prune_matches_oracle(tq):

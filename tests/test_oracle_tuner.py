@@ -37,6 +37,26 @@ def test_orthogonal_prune_brute_force():
             assert ib == max(x[1] for x in grp if x[2] == g)
 
 
+def test_orthogonal_prune_tie_width():  # DESIGN.md R18 (Step-1 rates of a B200 run, NB=128)
+    s = [(128, 8, 28394.0), (128, 16, 28379.0), (128, 32, 27771.0)]
+    assert tuner.orthogonal_prune(s) == [(128, 8, 28394.0)]             # exact rule: the argmax
+    assert tuner.orthogonal_prune(s, 0.005) == [(128, 16, 28379.0)]     # 0.05 % apart: tied, larger IB
+    assert tuner.orthogonal_prune(s, 0.05) == [(128, 32, 27771.0)]      # 2.2 % apart: tied at 5 %
+
+
+def test_orthogonal_prune_tie_width_brute_force():
+    rnd = random.Random(2)
+    for _ in range(50):
+        tie = rnd.choice([0.0, 0.01, 0.1, 0.5])
+        s = [(rnd.choice([64, 96, 128]), rnd.randint(1, 64), float(rnd.randint(1, 20))) for _ in range(30)]
+        for nb, ib, g in tuner.orthogonal_prune(s, tie):
+            grp = [x for x in s if x[0] == nb]
+            top = max(x[2] for x in grp)
+            tied = [x for x in grp if x[2] >= top * (1 - tie)]
+            assert ib == max(x[1] for x in tied)
+            assert g == max(x[2] for x in tied if x[1] == ib)
+
+
 def P(x, y):
     return (x, 0, y)
 
