@@ -241,6 +241,7 @@ def test_dataflow_kernel_stress_4096(tq, monkeypatch, ib):
     (400, 900, 96, 32, 72),      # wide
     (2048, 2048, 64, 8, 73),
     (300, 300, 48, 6, 74),       # level-synchronous fallback (no overlap)
+    (700, 900, 256, 16, 75),     # NB > 128: 8-warp dataflow kernel with the packed update
 ])
 def test_factor_host_equals_device_factor(tq, m, n, nb, ib, seed):
     """tileqr_factor_host (host buffers, copies overlapped with the dataflow
