@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU measurement round (run under gpurun from the repo root):
-#   GPU tests, smoke, autotune (optional), bench, ncu launch list, ncu full capture of SSRFB.
+#   GPU tests, smoke, autotune (optional), bench, ncu launch list, ncu full capture of the dataflow kernel.
 # Writes everything under gpurun_out/.
 OUT=gpurun_out
 R=${ROUND:-r01}
@@ -17,6 +17,7 @@ BCMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 if timeout 300 $BCMD > $OUT/bench_short.json 2>&1; then
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $OUT/launches.csv $BCMD > $OUT/ncu_launch.log 2>&1
   echo "ncu launches rc=$?" >> $OUT/ncu_launch.log
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:update_kernel -s 400 -c 1 -o $OUT/prof_ssrfb_bench -f $BCMD > $OUT/ncu_full.log 2>&1
+  # the dataflow kernel (one launch = the whole factorization): the 4th launch, after the 3 warm-up steps
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:dag_kernel -s 3 -c 1 -o $OUT/prof_dag_bench -f $BCMD > $OUT/ncu_full.log 2>&1
   echo "ncu full rc=$?" >> $OUT/ncu_full.log
 fi
