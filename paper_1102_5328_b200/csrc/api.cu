@@ -380,7 +380,10 @@ static int build_dag(FactorWS* ws, bool io) {
     }
   }
   // bottom levels (priority of ready items in the simulation below)
-  double wS = 4.0 * NB * NB * NB / 150.0, wP = 1200.0 * NB / NS;
+  // panel weight: twice the earlier 1200 ns per column (same-box sweep of
+  // TILEQR_DAG_WP at 10000^2: x2 -0.9 % (IB=16) / -1.2 % (IB=32), x0.5 and
+  // x3 slower)
+  double wS = 4.0 * NB * NB * NB / 150.0, wP = 2400.0 * NB / NS;
   if (const char* e = getenv("TILEQR_DAG_WS")) wS *= atof(e);  // diagnostics: priority weights
   if (const char* e = getenv("TILEQR_DAG_WP")) wP *= atof(e);
   const double wL = wS / 2, wIO = 10000.0;
