@@ -386,7 +386,9 @@ static int build_dag(FactorWS* ws, bool io) {
   double wS = 4.0 * NB * NB * NB / 150.0, wP = 2400.0 * NB / NS;
   if (const char* e = getenv("TILEQR_DAG_WS")) wS *= atof(e);  // diagnostics: priority weights
   if (const char* e = getenv("TILEQR_DAG_WP")) wP *= atof(e);
-  const double wL = wS / 2, wIO = 10000.0;
+  double wL = wS / 2;
+  const double wIO = 10000.0;
+  if (const char* e = getenv("TILEQR_DAG_WL")) wL *= atof(e);  // diagnostics
   auto weight = [&](int kind) {
     return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : kind == kArrive ? 0.0
          : (kind == dag::kLoad || kind == dag::kStore) ? wIO : wP;
@@ -416,7 +418,8 @@ static int build_dag(FactorWS* ws, bool io) {
   TQ_CUDA(cudaGetDevice(&dev0));
   TQ_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0));
   const int P = std::max(1, nsm0 * dag::dag_ctas_per_sm(NB));
-  const double cta_gflops = 220.0 / dag::dag_ctas_per_sm(NB);       // update rate per CTA
+  double cta_gflops = 220.0 / dag::dag_ctas_per_sm(NB);             // update rate per CTA
+  if (const char* e = getenv("TILEQR_DAG_CTAGF")) cta_gflops *= atof(e);  // diagnostics
   const double dS = 4.0 * NB * NB * cols / cta_gflops;               // ns per SSRFB slab
   // measured in the dataflow kernel at NB = 128 (10000^2): TSQRT and GEQRT
   // sub-tasks ~2-3 us per column (sharing their SM with an update CTA), LARFB
