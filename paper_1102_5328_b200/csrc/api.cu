@@ -344,7 +344,8 @@ static int build_dag(FactorWS* ws, bool io) {
   }
   const int cols = dag::dag_cols(NB);
   const int nslab = (NB + cols - 1) / cols;
-  constexpr int kIoTiles = 8;  // tiles per LOAD / STORE item
+  int kIoTiles = 8;  // tiles per LOAD / STORE item
+  if (const char* e = getenv("TILEQR_DAG_IOTILES")) kIoTiles = std::max(1, atoi(e));  // diagnostics
   const int nld = (int)((MT + kIoTiles - 1) / kIoTiles), nst = nld;
   auto parts = [&](int kind) {
     if (kind == dag::kLarfb || kind == dag::kSsrfb) return nslab;
