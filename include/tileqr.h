@@ -65,6 +65,26 @@ const char* tileqr_last_error(void);
 int tileqr_t_size(int64_t M, int64_t N, int NB, int IB, size_t* n_doubles);
 
 /* ------------------------------------------------------------------------
+ * tileqr_lookup -- (NB, IB) from the installed decision table of the
+ * autotuner: "the pre-built decision tree is used" when the user calls the
+ * library, by nearest-point interpolation on the tuned
+ * grid.  The table (tools/autotune.py -> tileqr_tune over
+ * the (N, ngpus) grid) is read from $TILEQR_TUNED_TABLE, else from
+ * tuned_table.json beside libtileqr.so.  Axes: the order of the problem (for
+ * M x N the square order with the same useful flop count, (3/4 *
+ * flops)^(1/3); R19) and ngpus; per-axis nearest grid value, ties
+ * toward the larger one.
+ *   Returns 0 (pair from the table) or TILEQR_ERR_NOT_INIT when no table is
+ *   installed -- *h_NB, *h_IB then hold the built-in default (128, 16).
+ *   Errors: -1 M < 0, -2 N < 0, -3 ngpus < 1, -4/-5 NULL outputs.
+ * Every entry point taking (NB, IB) -- tileqr_t_size, tileqr_factor,
+ * tileqr_factor_host, tileqr_apply_qt, tileqr_dist_factor -- accepts
+ * NB = IB = 0 as "the pair tileqr_lookup returns for this shape" (with the
+ * default when no table is installed).
+ * ------------------------------------------------------------------------ */
+int tileqr_lookup(int64_t M, int64_t N, int ngpus, int* h_NB, int* h_IB);
+
+/* ------------------------------------------------------------------------
  * tileqr_factor -- tile QR of the M x N matrix A (Fig. 1).
  *
  *   A  [in/out] device, M x N, leading dimension lda >= max(1, M).

@@ -192,6 +192,13 @@ struct FactorWS {
   dag::DagIO* d_io = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t io_ev[3] = {nullptr, nullptr, nullptr};
+  bool io_ready = false;  // st_in/st_out, copy streams and io_ev all created
+  // Ordering across callers: the workspace (tiles, T, packed tiles, DAG
+  // counters, staging) is shared by every call of this shape, so each call's
+  // stream waits for the previous call's last operation (this event) before
+  // touching it, whatever stream or host thread that call came from.
+  cudaEvent_t last_use = nullptr;
+  bool used = false;
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
   struct Rec { int kind; int64_t tasks; int64_t level; cudaEvent_t a, b; };
   int64_t cur_level = 0;
@@ -213,6 +220,7 @@ struct FactorWS {
     cudaFree(d_io);
     for (auto e : dag_ev) if (e) cudaEventDestroy(e);
     for (auto e : io_ev) if (e) cudaEventDestroy(e);
+    if (last_use) cudaEventDestroy(last_use);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
   }
@@ -742,6 +750,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
   TQ_CUDA(cudaStreamCreateWithPriority(&ws->s_update, cudaStreamNonBlocking, prio_lo));
   ws->ev.resize(9);
   for (auto& e : ws->ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TQ_CUDA(cudaEventCreateWithFlags(&ws->last_use, cudaEventDisableTiming));
   ws->use_dag = dag_enabled(NB, IB);
   if (ws->use_dag) {
     int rc = build_dag(ws.get(), false);
@@ -964,16 +973,39 @@ static int factor_host_dag(FactorWS* ws, const double* hA, int64_t lda, double* 
     if (rc) return rc;
   }
   if (int rc = stream_value_ops()) return rc;
-  if (!ws->st_in) {
-    if (cudaMalloc(&ws->st_in, (size_t)M * N * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&ws->st_out, (size_t)M * N * sizeof(double)) != cudaSuccess) {
+  if (!ws->io_ready) {
+    // every resource of the host pipeline, or none: a partial set is freed
+    // again so the next call retries from scratch
+    auto release = [&]() {
+      cudaFree(ws->st_in);
+      cudaFree(ws->st_out);
+      ws->st_in = ws->st_out = nullptr;
+      if (ws->s_h2d) cudaStreamDestroy(ws->s_h2d);
+      if (ws->s_d2h) cudaStreamDestroy(ws->s_d2h);
+      ws->s_h2d = ws->s_d2h = nullptr;
+      for (auto& e : ws->io_ev) {
+        if (e) cudaEventDestroy(e);
+        e = nullptr;
+      }
+    };
+    release();
+    bool ok = cudaMalloc(&ws->st_in, (size_t)M * N * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&ws->st_out, (size_t)M * N * sizeof(double)) == cudaSuccess;
+    if (!ok) {
       cudaGetLastError();
+      release();
       set_error("tileqr_factor_host: device allocation of the staging buffers failed");
       return TILEQR_ERR_ALLOC;
     }
-    TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_h2d, cudaStreamNonBlocking));
-    TQ_CUDA(cudaStreamCreateWithFlags(&ws->s_d2h, cudaStreamNonBlocking));
-    for (auto& e : ws->io_ev) TQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ok = cudaStreamCreateWithFlags(&ws->s_h2d, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&ws->s_d2h, cudaStreamNonBlocking) == cudaSuccess;
+    for (auto& e : ws->io_ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      cudaError_t e = cudaGetLastError();
+      release();
+      return cuda_fail(e, "tileqr_factor_host pipeline setup", __FILE__, __LINE__);
+    }
+    ws->io_ready = true;
   }
   int* ctr = L.d_ctr;
   TQ_CUDA(cudaMemsetAsync(ctr, 0, (size_t)(L.ntasks + 257) * sizeof(int), s));
@@ -1040,6 +1072,10 @@ const char* tileqr_last_error(void) { return g_last_error.c_str(); }
 int tileqr_t_size(int64_t M, int64_t N, int NB, int IB, size_t* n_doubles) {
   if (M < 0) return arg_error(1, "tileqr_t_size", "M < 0");
   if (N < 0) return arg_error(2, "tileqr_t_size", "N < 0");
+  if (NB == 0 && IB == 0) {  // "use the installed decision table" (table.cu)
+    bool from_table = false;
+    lookup_pair(M, N, 1, &NB, &IB, &from_table);
+  }
   if (NB < 1 || NB > 512) return arg_error(3, "tileqr_t_size", "NB not in [1, 512]");
   if (IB < 1 || IB > NB || NB % IB) return arg_error(4, "tileqr_t_size", "IB must divide NB");
   if (!n_doubles) return arg_error(5, "tileqr_t_size", "NULL output");
@@ -1063,6 +1099,10 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
   if (N < 0) return arg_error(2, fn, "N < 0");
   if (!A && M > 0 && N > 0) return arg_error(3, fn, "A is NULL");
   if (lda < std::max<int64_t>(1, M)) return arg_error(4, fn, "lda < max(1,M)");
+  if (NB == 0 && IB == 0) {  // "use the installed decision table" (table.cu)
+    bool from_table = false;
+    lookup_pair(M, N, 1, &NB, &IB, &from_table);
+  }
   if (NB < 1 || NB > 512) return arg_error(5, fn, "NB not in [1, 512]");
   if (IB < 1 || IB > NB || NB % IB) return arg_error(6, fn, "IB must divide NB");
   if (!T && M > 0 && N > 0) return arg_error(7, fn, "T is NULL");
@@ -1083,12 +1123,15 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
     int rc = create_ws(dev, M, N, NB, IB, &ws);
     if (rc) return rc;
   }
+  if (ws->used) TQ_CUDA(cudaStreamWaitEvent(s, ws->last_use, 0));  // previous user of the workspace
   int rc = launch_layout_to_tiles(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, d_info, s);
   if (rc) return rc;
   if ((rc = run_levels(ws, s))) return rc;
   if ((rc = launch_tiles_to_layout(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, s))) return rc;
   TQ_CUDA(cudaMemcpyAsync(T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
                           cudaMemcpyDeviceToDevice, s));
+  TQ_CUDA(cudaEventRecord(ws->last_use, s));
+  ws->used = true;
   return 0;
 }
 
@@ -1099,6 +1142,10 @@ int tileqr_factor_host(int64_t M, int64_t N, const double* h_A, int64_t lda, int
   if (N < 0) return arg_error(2, fn, "N < 0");
   if (!h_A && M > 0 && N > 0) return arg_error(3, fn, "h_A is NULL");
   if (lda < std::max<int64_t>(1, M)) return arg_error(4, fn, "lda < max(1,M)");
+  if (NB == 0 && IB == 0) {  // "use the installed decision table" (table.cu)
+    bool from_table = false;
+    lookup_pair(M, N, 1, &NB, &IB, &from_table);
+  }
   if (NB < 1 || NB > 512) return arg_error(5, fn, "NB not in [1, 512]");
   if (IB < 1 || IB > NB || NB % IB) return arg_error(6, fn, "IB must divide NB");
   if (!h_R && M > 0 && N > 0) return arg_error(7, fn, "h_R is NULL");
@@ -1121,7 +1168,14 @@ int tileqr_factor_host(int64_t M, int64_t N, const double* h_A, int64_t lda, int
     int rc = create_ws(dev, M, N, NB, IB, &ws);
     if (rc) return rc;
   }
-  if (ws->use_dag) return factor_host_dag(ws, h_A, lda, h_R, ldr, h_T, d_info, s);
+  if (ws->used) TQ_CUDA(cudaStreamWaitEvent(s, ws->last_use, 0));  // previous user of the workspace
+  if (ws->use_dag) {
+    const int rc = factor_host_dag(ws, h_A, lda, h_R, ldr, h_T, d_info, s);
+    if (rc) return rc;
+    TQ_CUDA(cudaEventRecord(ws->last_use, s));
+    ws->used = true;
+    return 0;
+  }
   // level-synchronous schedule: copy in, factor, copy out (no overlap)
   if (!ws->st_in) {
     if (cudaMalloc(&ws->st_in, (size_t)M * N * sizeof(double)) != cudaSuccess) {
@@ -1140,6 +1194,8 @@ int tileqr_factor_host(int64_t M, int64_t N, const double* h_A, int64_t lda, int
                             cudaMemcpyDeviceToHost, s));
   TQ_CUDA(cudaMemcpyAsync(h_T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
                           cudaMemcpyDeviceToHost, s));
+  TQ_CUDA(cudaEventRecord(ws->last_use, s));
+  ws->used = true;
   return 0;
 }
 
@@ -1155,6 +1211,10 @@ int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double
   if (!A && M > 0 && K > 0) return arg_error(5, fn, "A is NULL");
   if (lda < std::max<int64_t>(1, M)) return arg_error(6, fn, "lda < max(1,M)");
   if (!T && M > 0 && K > 0) return arg_error(7, fn, "T is NULL");
+  if (NB == 0 && IB == 0) {  // "use the installed decision table" (table.cu)
+    bool from_table = false;
+    lookup_pair(M, K, 1, &NB, &IB, &from_table);
+  }
   if (NB < 1 || NB > 512) return arg_error(8, fn, "NB not in [1, 512]");
   if (IB < 1 || IB > NB || NB % IB) return arg_error(9, fn, "IB must divide NB");
   if (!B && M > 0 && NRHS > 0) return arg_error(10, fn, "B is NULL");
@@ -1538,6 +1598,23 @@ int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, 
   }
   return 0;
 }
+
+}  // extern "C"
+
+namespace tileqr {
+// Free the cached workspace of one shape once its last use has completed
+// (the tuner calls this after timing a Step-2 candidate, so tuning does not
+// keep one workspace per candidate resident).
+void release_ws(int dev, int64_t M, int64_t N, int NB, int IB) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  if (it == g_ws.end()) return;
+  if (it->second->used) cudaEventSynchronize(it->second->last_use);
+  g_ws.erase(it);
+}
+}  // namespace tileqr
+
+extern "C" {
 
 void tileqr_finalize(void) {
   std::lock_guard<std::mutex> lock(g_mu);

@@ -329,7 +329,11 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     v2::fence_proxy_async_smem();
     __syncthreads();  // every write of the item issued; smem free for the next item
     if (threadIdx.x == 0) {
-      __threadfence();
+      // STORE counters are read by the copy engine (cuStreamWaitValue32 on
+      // the device-to-host stream), not by GPU threads: publish them at
+      // system scope
+      if (IO && it.kind == kStore) __threadfence_system();
+      else __threadfence();
       atomicAdd(done + it.task, 1);
       if (prof) prof[3 * (size_t)i + 2] = globaltimer();
     }

@@ -73,5 +73,10 @@ int launch_pack(bool larfb, int NB, int IB, int batch, const double* const* V, c
 
 // Which SSRFB implementation a (NB, IB) pair uses ("dmma" or "simt").
 const char* ssrfb_impl_name(int NB, int IB);
+// Decision-table lookup (table.cu): (NB, IB) for an M x N factorization on
+// ngpus GPUs; the built-in default when no table is installed (*from_table false).
+int lookup_pair(int64_t M, int64_t N, int ngpus, int* NB, int* IB, bool* from_table);
+// Free the cached tileqr_factor workspace of one shape (api.cu; waits for its last use).
+void release_ws(int dev, int64_t M, int64_t N, int NB, int IB);
 
 }  // namespace tileqr

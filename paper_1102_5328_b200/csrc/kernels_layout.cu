@@ -40,49 +40,99 @@ __device__ __forceinline__ double padded_value(int64_t i, int64_t j, int64_t M, 
   return (j >= N && i == j && j >= M) ? 1.0 : 0.0;
 }
 
+// One CTA per tile (m, n) (grid MT x NT): the tile's NB column segments of NB
+// rows are contiguous runs in both layouts, so an interior tile is a plain
+// strided-to-contiguous block copy.  VEC (NB, lda even, A 16-byte aligned):
+// 16-byte loads and stores, 8 in flight per thread; 32-bit index arithmetic
+// inside the tile (the earlier element-pair kernels spent their time in 64-bit
+// divisions: 57 % / 46 % of HBM, profiles/r02_ncu_layout_n10000_nb128.json).
+// Edge tiles (rows >= M or columns >= N inside) take the per-element path with
+// the padding of DESIGN.md R5.
+constexpr int kUnroll = 8;
+
+template <bool VEC>
 __global__ void __launch_bounds__(kThreads)
 layout_to_tiles_kernel(int64_t M, int64_t N, const double* __restrict__ A, int64_t lda, int NB,
-                       int64_t MT, int64_t NT, double* __restrict__ tiles, int* d_info) {
-  // work item = (global column j, tile row m, row pair within the tile)
-  const int64_t half = (NB + 1) / 2;
-  const int64_t ncols = NT * NB;
-  const int64_t per_col = MT * half;
-  const int64_t total = ncols * per_col;
+                       int64_t MT, double* __restrict__ tiles, int* d_info) {
+  const int64_t m = blockIdx.x, n = blockIdx.y;
+  const int64_t i0 = m * NB, j0 = n * NB;
+  double* __restrict__ dst = tiles + (m + n * MT) * (int64_t)NB * NB;
+  const int tid = threadIdx.x;
   int bad = 0;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = w / per_col;
-    const int64_t rem = w - j * per_col;
-    const int64_t m = rem / half;
-    const int64_t il = 2 * (rem - m * half);
-    const int64_t n = j / NB, jl = j - n * NB;
-    const int64_t i = m * NB + il;
-    double* dst = tiles + (m + n * MT) * (int64_t)NB * NB + il + jl * NB;
-    double v0 = padded_value(i, j, M, N, A, lda, &bad);
-    if (il + 1 < NB) {
-      double v1 = padded_value(i + 1, j, M, N, A, lda, &bad);
-      if ((NB & 1) == 0) {
-        *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
-      } else {
-        dst[0] = v0;
-        dst[1] = v1;
+  if (VEC && i0 + NB <= M && j0 + NB <= N) {
+    const int HP = NB >> 1, tot = NB * HP;
+    const double* __restrict__ src = A + i0 + j0 * lda;
+    for (int e0 = tid; e0 < tot; e0 += kUnroll * kThreads) {
+      double2 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e < tot) {
+          const int jl = e / HP, il = 2 * (e - jl * HP);
+          v[u] = __ldcs(reinterpret_cast<const double2*>(src + il + jl * lda));
+        }
       }
-    } else {
-      dst[0] = v0;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e < tot) {
+          if (!isfinite(v[u].x) || !isfinite(v[u].y)) bad = 1;
+          reinterpret_cast<double2*>(dst)[e] = v[u];  // element 2e = (il, jl): il + jl*NB = 2e
+        }
+      }
+    }
+  } else {
+    const int tot = NB * NB;
+    for (int e = tid; e < tot; e += kThreads) {
+      const int jl = e / NB, il = e - jl * NB;
+      const int64_t i = i0 + il, j = j0 + jl;
+      double v;
+      if (i < M && j < N) {
+        v = __ldcs(A + i + j * lda);
+        if (!isfinite(v)) bad = 1;
+      } else {
+        v = (j >= N && i == j && j >= M) ? 1.0 : 0.0;
+      }
+      dst[e] = v;
     }
   }
   if (bad && d_info) *d_info = 1;  // benign race: every writer stores 1
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(kThreads)
-tiles_to_layout_kernel(int64_t M, int64_t N, double* __restrict__ A, int64_t lda, int NB,
-                       int64_t MT, const double* __restrict__ tiles) {
-  const int64_t total = M * N;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = w / M, i = w - j * M;
-    const int64_t m = i / NB, il = i - m * NB, n = j / NB, jl = j - n * NB;
-    A[i + j * lda] = tiles[(m + n * MT) * (int64_t)NB * NB + il + jl * NB];
+tiles_to_layout_kernel(int64_t M, int64_t N, double* __restrict__ A, int64_t lda, int NB, int64_t MT,
+                       const double* __restrict__ tiles) {
+  const int64_t m = blockIdx.x, n = blockIdx.y;
+  const int64_t i0 = m * NB, j0 = n * NB;
+  const double* __restrict__ src = tiles + (m + n * MT) * (int64_t)NB * NB;
+  const int tid = threadIdx.x;
+  if (VEC && i0 + NB <= M && j0 + NB <= N) {
+    const int HP = NB >> 1, tot = NB * HP;
+    double* __restrict__ d = A + i0 + j0 * lda;
+    for (int e0 = tid; e0 < tot; e0 += kUnroll * kThreads) {
+      double2 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e < tot) v[u] = __ldcs(reinterpret_cast<const double2*>(src) + e);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int e = e0 + u * kThreads;
+        if (e < tot) {
+          const int jl = e / HP, il = 2 * (e - jl * HP);
+          __stcs(reinterpret_cast<double2*>(d + il + jl * lda), v[u]);
+        }
+      }
+    }
+  } else {
+    const int tot = NB * NB;
+    for (int e = tid; e < tot; e += kThreads) {
+      const int jl = e / NB, il = e - jl * NB;
+      const int64_t i = i0 + il, j = j0 + jl;
+      if (i < M && j < N) A[i + j * lda] = src[e];
+    }
   }
 }
 
@@ -164,19 +214,36 @@ uint64_t host_splitmix64(uint64_t x) {
 
 }  // namespace
 
+static bool layout_vec(const double* A, int64_t lda, int NB) {
+  return (NB % 2 == 0) && (lda % 2 == 0) && ((uintptr_t)A % 16 == 0);
+}
+
 int launch_layout_to_tiles(int64_t M, int64_t N, const double* A, int64_t lda, int NB, int64_t MT,
                            int64_t NT, double* tiles, int* d_info, cudaStream_t s) {
-  const int64_t work = NT * NB * MT * ((NB + 1) / 2);
-  layout_to_tiles_kernel<<<grid_for(work), kThreads, 0, s>>>(M, N, A, lda, NB, MT, NT, tiles,
-                                                              d_info);
+  if (MT <= 0 || NT <= 0) return 0;
+  if (NT > 65535) {
+    set_error("layout_to_tiles: more than 65535 tile columns");
+    return TILEQR_ERR_CUDA;
+  }
+  const dim3 grid((unsigned)MT, (unsigned)NT);
+  if (layout_vec(A, lda, NB)) layout_to_tiles_kernel<true><<<grid, kThreads, 0, s>>>(M, N, A, lda, NB, MT, tiles, d_info);
+  else layout_to_tiles_kernel<false><<<grid, kThreads, 0, s>>>(M, N, A, lda, NB, MT, tiles, d_info);
   TQ_LAUNCH_CHECK();
   return 0;
 }
 
 int launch_tiles_to_layout(int64_t M, int64_t N, double* A, int64_t lda, int NB, int64_t MT,
                            int64_t NT, const double* tiles, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return 0;
+  const int64_t mt = (M + NB - 1) / NB, nt = (N + NB - 1) / NB;  // only tiles holding real entries
   (void)NT;
-  tiles_to_layout_kernel<<<grid_for(M * N), kThreads, 0, s>>>(M, N, A, lda, NB, MT, tiles);
+  if (nt > 65535) {
+    set_error("tiles_to_layout: more than 65535 tile columns");
+    return TILEQR_ERR_CUDA;
+  }
+  const dim3 grid((unsigned)mt, (unsigned)nt);
+  if (layout_vec(A, lda, NB)) tiles_to_layout_kernel<true><<<grid, kThreads, 0, s>>>(M, N, A, lda, NB, MT, tiles);
+  else tiles_to_layout_kernel<false><<<grid, kThreads, 0, s>>>(M, N, A, lda, NB, MT, tiles);
   TQ_LAUNCH_CHECK();
   return 0;
 }

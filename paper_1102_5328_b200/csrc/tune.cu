@@ -121,7 +121,7 @@ std::string pts_json(const std::vector<Pt>& v) {
   std::string s = "[";
   char buf[128];
   for (size_t i = 0; i < v.size(); ++i) {
-    snprintf(buf, sizeof buf, "%s{\"nb\": %d, \"ib\": %d, \"gflops\": %.6f}", i ? ", " : "", v[i].nb,
+    snprintf(buf, sizeof buf, "%s{\"nb\": %d, \"ib\": %d, \"gflops\": %.17g}", i ? ", " : "", v[i].nb,
              v[i].ib, v[i].g);
     s += buf;
   }
@@ -372,14 +372,19 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
         cudaEventElapsedTime(&ms, e0, e1);
         if (r > 0) times.push_back(ms);
       }
+      {  // this candidate's workspace is not needed again at this N
+        int dev = 0;
+        cudaGetDevice(&dev);
+        release_ws(dev, m, n, p.nb, p.ib);
+      }
       std::sort(times.begin(), times.end());
       const double med = 0.5 * (times[2] + times[3]);
       const double flops = (m >= n) ? 2.0 * m * (double)n * n - 2.0 * (double)n * n * n / 3.0
                                     : 2.0 * n * (double)m * m - 2.0 * (double)m * m * m / 3.0;
       const double g = flops / (med * 1e-3) / 1e9;
       res.push_back({p.nb, p.ib, g});
-      char b[192];
-      snprintf(b, sizeof b, "%s{\"n\": %lld, \"nb\": %d, \"ib\": %d, \"median_ms\": %.4f, \"gflops\": %.3f}",
+      char b[256];
+      snprintf(b, sizeof b, "%s{\"n\": %lld, \"nb\": %d, \"ib\": %d, \"median_ms\": %.6f, \"gflops\": %.17g}",
                step2.size() > 1 ? ", " : "", (long long)n, p.nb, p.ib, med, g);
       step2 += b;
     }
@@ -404,9 +409,9 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   if (report_json_path) {
     FILE* f = fopen(report_json_path, "w");
     if (f) {
-      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d, \"step1_timing\": \"%s\",\n",
-              (long long)M, (long long)N, heuristic, payg, batch, reps, flush ? "flush" : "no_flush");
-      fprintf(f, " \"step1\": %s,\n \"candidates\": %s,\n \"step2\": %s,\n \"best\": {\"nb\": %d, \"ib\": %d, \"gflops\": %.3f}}\n",
+      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d, \"step1_timing\": \"%s\", \"tie_rel\": %.17g,\n",
+              (long long)M, (long long)N, heuristic, payg, batch, reps, flush ? "flush" : "no_flush", tie_rel);
+      fprintf(f, " \"step1\": %s,\n \"candidates\": %s,\n \"step2\": %s,\n \"best\": {\"nb\": %d, \"ib\": %d, \"gflops\": %.17g}}\n",
               pts_json(samples).c_str(), pts_json(cand).c_str(), step2.c_str(), best.nb, best.ib, best.g);
       fclose(f);
     }

@@ -35,6 +35,7 @@ _SIGS = {
     "tileqr_version": ([], ctypes.c_char_p),
     "tileqr_last_error": ([], ctypes.c_char_p),
     "tileqr_t_size": ([_i64, _i64, _i, _i, ctypes.POINTER(_sz)], _i),
+    "tileqr_lookup": ([_i64, _i64, _i, _PI, _PI], _i),
     "tileqr_factor": ([_i64, _i64, _p, _i64, _i, _i, _p, _p, _p], _i),
     "tileqr_factor_host": ([_i64, _i64, _p, _i64, _i, _i, _p, _i64, _p, _p, _p], _i),
     "tileqr_apply_qt": ([_c, _i64, _i64, _i64, _p, _i64, _p, _i, _i, _p, _i64, _p], _i),
@@ -108,6 +109,16 @@ def t_size(m: int, n: int, nb: int, ib: int) -> int:
     return out.value
 
 
+def lookup(m: int, n: int, ngpus: int = 1):
+    """(nb, ib, from_table): the installed decision table's pair for this shape
+    (built-in default and from_table False when no table is installed)."""
+    nb, ib = ctypes.c_int(), ctypes.c_int()
+    rc = _lib.tileqr_lookup(m, n, ngpus, ctypes.byref(nb), ctypes.byref(ib))
+    if rc not in (0, 4):
+        _check(rc, "tileqr_lookup")
+    return nb.value, ib.value, rc == 0
+
+
 def num_levels(mt: int, nt: int) -> int:
     out = _i64()
     _check(_lib.tileqr_num_levels(mt, nt, ctypes.byref(out)), "tileqr_num_levels")
@@ -166,14 +177,21 @@ def factor_host(hA: torch.Tensor, m: int, n: int, nb: int, ib: int, hR: torch.Te
     assert hA.dtype == torch.float64 and not hA.is_cuda and hA.is_contiguous()
     if hR is None:
         hR = hA
+    own = hT is None or info is None
     if hT is None:
         hT = torch.empty(max(1, t_size(m, n, nb, ib)), dtype=torch.float64, pin_memory=hA.is_pinned())
     if info is None:
         info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = _stream(stream)
     rc = _lib.tileqr_factor_host(m, n, hA.data_ptr(), lda if lda is not None else max(1, m), nb, ib,
                                  hR.data_ptr(), ldr if ldr is not None else max(1, m), hT.data_ptr(),
-                                 info.data_ptr(), _stream(stream))
+                                 info.data_ptr(), s)
     _check(rc, "tileqr_factor_host")
+    if own:
+        # buffers this wrapper allocated are still being written by queued
+        # copies: finish the call before handing them out, so dropping them
+        # cannot return a block to torch's allocator under an in-flight DMA
+        torch.cuda.ExternalStream(s).synchronize() if s else torch.cuda.synchronize()
     return hR, hT, info
 
 

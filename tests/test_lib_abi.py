@@ -90,3 +90,35 @@ def test_payg_prune_matches_oracle(tq):
     for _ in range(200):
         res = [(nb, 1, float(rnd.randint(0, 10))) for nb in rnd.sample(range(8, 512, 8), rnd.randint(1, 9))]
         assert tq.payg_prune(res) == tuner.payg_prune(res)
+
+
+def test_lookup_matches_oracle_nearest_point(tq, tmp_path, monkeypatch):
+    """tileqr_lookup (the library's decision-table interpolation, PAPER.md:631-635,
+    826-832) against oracle.tuner.lookup on a (N, ngpus) grid, square queries;
+    a rectangular query uses the square order of equal flop count (R19)."""
+    import json
+    from oracle import tuner
+    rnd = random.Random(5)
+    ns, gs = [500, 1000, 2000, 4000, 6000, 8000, 10000], [1, 2, 4, 8]
+    pairs = [(64, 16), (96, 32), (128, 16), (160, 32), (192, 24), (256, 32)]
+    table = {(n, g): rnd.choice(pairs) for n in ns for g in gs}
+    path = tmp_path / "table.json"
+    json.dump({"format_version": 1, "entries": [{"n": n, "ngpus": g, "nb": v[0], "ib": v[1]}
+                                                for (n, g), v in table.items()]}, open(path, "w"))
+    monkeypatch.setenv("TILEQR_TUNED_TABLE", str(path))
+    for _ in range(300):
+        n, g = rnd.randint(1, 12000), rnd.randint(1, 9)
+        assert tq.lookup(n, n, g) == (*tuner.lookup(table, n, g), True), (n, g)
+    for n in ns:  # on-grid points and exact midpoints (ties -> larger)
+        assert tq.lookup(n, n, 1)[:2] == table[(n, 1)]
+    assert tq.lookup(750, 750, 3)[:2] == table[(1000, 4)]
+    # 40000 x 1000: (3/4 * (2*M*N^2 - 2N^3/3))^(1/3) = 3904 -> grid order 4000
+    assert tq.lookup(40000, 1000, 1)[:2] == table[(4000, 1)]
+    assert tq.t_size(300, 300, 0, 0) == tq.t_size(300, 300, *tq.lookup(300, 300)[:2])
+    monkeypatch.setenv("TILEQR_TUNED_TABLE", str(tmp_path / "missing.json"))
+    assert tq.lookup(1000, 1000) == (128, 16, False)
+
+
+def test_installed_table_is_readable(tq):
+    nb, ib, found = tq.lookup(10000, 10000)
+    assert found and nb % ib == 0

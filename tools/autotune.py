@@ -46,7 +46,7 @@ def factor_rate(n, nb, ib, reps=6):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n", type=int, nargs="*", default=[2048, 10000])
+    ap.add_argument("--n", type=int, nargs="*", default=[500, 1000, 2000, 2048, 4000, 6000, 8000, 10000])  # P:612-623 grid + configs[2]
     ap.add_argument("--es", type=int, default=2048)
     ap.add_argument("--heuristic", type=int, default=2)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "tune_r01.json"))
@@ -84,10 +84,13 @@ def main():
         report["exhaustive_search"] = res
         print(json.dumps({k: v for k, v in res.items() if k != "all"}), flush=True)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
-    json.dump(report, open(a.out, "w"), indent=1)
+    json.dump(report, open(a.out + ".tmp", "w"), indent=1)
+    os.replace(a.out + ".tmp", a.out)
     table = {"format_version": 1, "machine": torch.cuda.get_device_name(0), "heuristic": a.heuristic,
              "payg": True, "entries": entries}
-    json.dump(table, open(a.table, "w"), indent=1)
+    tmp = a.table + ".tmp"  # written atomically: a reader never sees a partial table
+    json.dump(table, open(tmp, "w"), indent=1)
+    os.replace(tmp, a.table)
 
 
 if __name__ == "__main__":
