@@ -29,6 +29,7 @@
 
 #include "dag_item.h"
 #include "internal.h"
+#include "sched.h"
 
 namespace tileqr {
 
@@ -300,7 +301,7 @@ static int build_dag(FactorWS* ws, bool io) {
   auto idST = [&](int64_t n) { return ntask0 + NT + n; };
   auto idAR = [&](int64_t n) { return ntask0 + 2 * NT + n; };
   constexpr int kArrive = 6;  // host-only pseudo kind: set by the copy stream
-  struct Task { int kind; int k, m, n; int level; int ndep; int dep[3]; int s; };
+  using Task = sched::Task;
   std::vector<Task> tk(ntask);
   for (int64_t k = 0; k < KT; ++k) {
     for (int sub = 0; sub < NS; ++sub) {
@@ -361,33 +362,6 @@ static int build_dag(FactorWS* ws, bool io) {
     if (kind == dag::kStore) return nst;
     return 1;
   };
-  // successors (CSR) and a topological order (Kahn)
-  std::vector<int64_t> soff(ntask + 1, 0);
-  for (int64_t i = 0; i < ntask; ++i)
-    for (int d = 0; d < tk[i].ndep; ++d) ++soff[tk[i].dep[d] + 1];
-  for (int64_t i = 0; i < ntask; ++i) soff[i + 1] += soff[i];
-  std::vector<int> succ_l(soff[ntask]);
-  {
-    std::vector<int64_t> fill(soff.begin(), soff.end() - 1);
-    for (int64_t i = 0; i < ntask; ++i)
-      for (int d = 0; d < tk[i].ndep; ++d) succ_l[fill[tk[i].dep[d]]++] = (int)i;
-  }
-  std::vector<int> topo;
-  topo.reserve(ntask);
-  {
-    std::vector<int> indeg(ntask);
-    for (int64_t i = 0; i < ntask; ++i) {
-      indeg[i] = tk[i].ndep;
-      if (indeg[i] == 0) topo.push_back((int)i);
-    }
-    for (size_t q = 0; q < topo.size(); ++q)
-      for (int64_t e = soff[topo[q]]; e < soff[topo[q] + 1]; ++e)
-        if (--indeg[succ_l[e]] == 0) topo.push_back(succ_l[e]);
-    if ((int64_t)topo.size() != ntask) {
-      set_error("tileqr_factor: internal error: the task graph has a cycle");
-      return TILEQR_ERR_CUDA;
-    }
-  }
   // bottom levels (priority of ready items in the simulation below)
   // panel weight: twice the earlier 1200 ns per column (same-box sweep of
   // TILEQR_DAG_WP at 10000^2: x2 -0.9 % (IB=16) / -1.2 % (IB=32), x0.5 and
@@ -402,27 +376,23 @@ static int build_dag(FactorWS* ws, bool io) {
     return kind == dag::kSsrfb ? wS : kind == dag::kLarfb ? wL : kind == kArrive ? 0.0
          : (kind == dag::kLoad || kind == dag::kStore) ? wIO : wP;
   };
-  std::vector<double> bl(ntask, 0.0);
-  for (int64_t q = ntask - 1; q >= 0; --q) {
-    const int i = topo[q];
-    double mx = 0.0;
-    for (int64_t e = soff[i]; e < soff[i + 1]; ++e) mx = std::max(mx, bl[succ_l[e]]);
-    bl[i] = weight(tk[i].kind) + mx;
-  }
+  sched::Params prm;
+  prm.parts = parts;
+  prm.weight = weight;
   // LOAD / STORE items start as soon as they are ready: they gate everything
   // downstream (LOAD) or the device-to-host copy (STORE) and are cheap
+  prm.bl_override.assign(ntask, -1.0);
   for (int64_t i = ntask0; i < ntask; ++i)
-    if (tk[i].kind == dag::kLoad || tk[i].kind == dag::kStore) bl[i] = 1e30;
+    if (tk[i].kind == dag::kLoad || tk[i].kind == dag::kStore) prm.bl_override[i] = 1e30;
 
-  // Claim order: a list schedule simulated on the host -- P workers (the
-  // resident CTAs), rough per-item durations, ready items started in bottom-
-  // level order -- and the items sorted by their simulated start time.  A
-  // CTA that claims an item blocks until its inputs are final, so claiming in
-  // an order the DAG can actually keep up with avoids head-of-line blocking
-  // (pure bottom-level order parks hundreds of CTAs on far-future items while
-  // the first panels run).  Start times respect dependencies strictly, so the
-  // order is topological (deadlock-free claiming).  ARRIVE pseudo-tasks (host
-  // pipeline) complete at the time their column's copy is expected to land.
+  // Claim order: a list schedule simulated on the host (sched.h) -- P workers
+  // (the resident CTAs), rough per-item durations, ready items started in
+  // bottom-level order -- and the items sorted by their simulated start time.
+  // A CTA that claims an item blocks until its inputs are final, so claiming
+  // in an order the DAG can actually keep up with avoids head-of-line
+  // blocking (pure bottom-level order parks hundreds of CTAs on far-future
+  // items while the first panels run).  ARRIVE pseudo-tasks (host pipeline)
+  // complete at the time their column's copy is expected to land.
   int dev0 = 0, nsm0 = 0;
   TQ_CUDA(cudaGetDevice(&dev0));
   TQ_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0));
@@ -443,87 +413,34 @@ static int build_dag(FactorWS* ws, bool io) {
   double h2d_gbs = 54.0;  // host link, measured while the kernel runs (54 GB/s; 30-100 in the sim: +-3 %)
   if (const char* e = getenv("TILEQR_DAG_H2D_GBS")) h2d_gbs = atof(e);  // diagnostics
   const double tcol = (double)MT * NB * NB * 8 / h2d_gbs;
-  auto dur = [&](int kind) {
+  for (int64_t i = ntask0; i < ntask; ++i)
+    if (tk[i].kind == kArrive) {
+      tk[i].worker = false;
+      tk[i].fixed = tcol * (tk[i].n + 1);
+    }
+  prm.dur = [&](int kind) {
     switch (kind) {
       case dag::kSsrfb: return dS + hand;
       case dag::kLarfb: return dL;
       case dag::kTsqrt: return dT;
       case dag::kGeqrt: return dG;
+      case kArrive: return 0.0;
       default: return dIO;
     }
   };
-  std::vector<int> indeg(ntask), left(ntask);
-  for (int64_t i = 0; i < ntask; ++i) {
-    indeg[i] = tk[i].ndep;
-    left[i] = parts(tk[i].kind);
+  prm.npools = 1;
+  prm.workers = P;
+  std::vector<sched::Slot> sched;
+  const char* ord = getenv("TILEQR_DAG_ORDER");  // diagnostics: "bl" = pure bottom-level order
+  const int src = sched::simulate(tk, prm, &sched, ord && strcmp(ord, "bl") == 0);
+  if (src == -1) {
+    set_error("tileqr_factor: internal error: the task graph has a cycle");
+    return TILEQR_ERR_CUDA;
   }
-  struct Rd { double bl; int level, s, task, slab; };
-  auto rd_less = [](const Rd& a, const Rd& b) {  // max-heap on priority
-    if (a.bl != b.bl) return a.bl < b.bl;
-    if (a.level != b.level) return a.level > b.level;
-    if (a.s != b.s) return a.s > b.s;
-    if (a.task != b.task) return a.task > b.task;
-    return a.slab > b.slab;
-  };
-  std::vector<Rd> ready;
-  auto push_task = [&](int i) {
-    for (int sl = 0; sl < parts(tk[i].kind); ++sl) {
-      ready.push_back({bl[i], tk[i].level, tk[i].s, i, sl});
-      std::push_heap(ready.begin(), ready.end(), rd_less);
-    }
-  };
-  struct Ev { double t; int task; bool worker; };
-  auto ev_greater = [](const Ev& a, const Ev& b) { return a.t > b.t; };
-  std::vector<Ev> events;
-  for (int64_t i = 0; i < ntask; ++i) {
-    if (indeg[i] != 0) continue;
-    if (tk[i].kind == kArrive) {  // completes without a worker when its copy lands
-      events.push_back({tcol * (tk[i].n + 1), (int)i, false});
-      std::push_heap(events.begin(), events.end(), ev_greater);
-    } else {
-      push_task((int)i);
-    }
-  }
-  struct Slot { double start; double bl; int task, slab; };
-  std::vector<Slot> sched;
-  double now = 0.0;
-  int freew = P;
-  while (!ready.empty() || !events.empty()) {
-    while (freew > 0 && !ready.empty()) {
-      std::pop_heap(ready.begin(), ready.end(), rd_less);
-      const Rd r = ready.back();
-      ready.pop_back();
-      sched.push_back({now, r.bl, r.task, r.slab});
-      events.push_back({now + dur(tk[r.task].kind), r.task, true});
-      std::push_heap(events.begin(), events.end(), ev_greater);
-      --freew;
-    }
-    if (events.empty()) break;
-    std::pop_heap(events.begin(), events.end(), ev_greater);
-    const Ev e = events.back();
-    events.pop_back();
-    now = e.t;
-    if (e.worker) ++freew;
-    if (--left[e.task] <= 0)
-      for (int64_t q = soff[e.task]; q < soff[e.task + 1]; ++q)
-        if (--indeg[succ_l[q]] == 0) push_task(succ_l[q]);
-  }
-  int64_t nitems_expect = 0;
-  for (int64_t i = 0; i < ntask; ++i)
-    if (tk[i].kind != kArrive) nitems_expect += parts(tk[i].kind);
-  if ((int64_t)sched.size() != nitems_expect) {
+  if (src) {
     set_error("tileqr_factor: internal error in the DAG schedule simulation");
     return TILEQR_ERR_CUDA;
   }
-  const char* ord = getenv("TILEQR_DAG_ORDER");  // diagnostics: "bl" = pure bottom-level order
-  if (ord && strcmp(ord, "bl") == 0)
-    std::stable_sort(sched.begin(), sched.end(), [&](const Slot& a, const Slot& b) {
-      if (a.bl != b.bl) return a.bl > b.bl;
-      if (a.task != b.task) return a.task < b.task;
-      return a.slab < b.slab;
-    });
-  else
-    std::stable_sort(sched.begin(), sched.end(), [](const Slot& a, const Slot& b) { return a.start < b.start; });
   const size_t tile = (size_t)NB * NB;
   double* A = ws->tiles;
   double* Tw = ws->Tws;
@@ -536,7 +453,7 @@ static int build_dag(FactorWS* ws, bool io) {
   L.item_kind.clear();
   L.item_level.clear();
   L.item_info.clear();
-  for (const Slot& sl : sched) {
+  for (const sched::Slot& sl : sched) {
     const int i = sl.task;
     const Task& t = tk[i];
     dag::Item it{};
