@@ -393,15 +393,17 @@ def run_tileqr_dist(args, rank, world, local_rank):
     mt = -(-n // nb)
     nloc = tq.dist_local_cols(n, nb)
     A0 = torch.empty(max(1, nloc * mt * nb * nb), dtype=torch.float64, device=dev)
-    tq.dist_fill_uniform(n, nb, A0, seed)
+    tq.dist_fill_uniform(n, n, nb, A0, seed)
     A = torch.empty_like(A0)
     T = torch.empty(max(1, nloc * mt * ib * nb), dtype=torch.float64, device=dev)
     info = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
+    dataflow = tq.factor_schedule(nb, ib) == "dag" and os.environ.get("TILEQR_DIST_SCHED") != "levels"
+
     def step():
         A.copy_(A0)
-        tq.dist_factor(n, A, nb, ib, T, info)
+        tq.dist_factor(n, n, A, nb, ib, T, info)
 
     for _ in range(args.warmup):
         step()
@@ -423,25 +425,81 @@ def run_tileqr_dist(args, rank, world, local_rank):
     dist.all_reduce(bad, op=dist.ReduceOp.MAX)
     flops = qr_flops(n, n)
     value = flops / (ms * 1e-3) / 1e9
-    launches = 2  # zero-info + non-finite scan
-    for t in range(3 * mt - 2):
-        panel, _, upd = tq.dist_plan_level(mt, world, rank, t)
-        launches += len({q[0] for q in panel}) + len({q[0] for q in upd})
+    if dataflow:  # zero-info, non-finite scan, the persistent dataflow kernel
+        launches = 3
+    else:
+        launches = 2  # zero-info + non-finite scan
+        for t in range(3 * mt - 2):
+            panel, _, upd = tq.dist_plan_level(mt, world, rank, t)
+            launches += len({q[0] for q in panel}) + len({q[0] for q in upd})
+    verify = verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nloc) if args.verify else None
     if rank == 0:
         line = {"metric": "tile-QR FP64 GFLOP/s", "value": round(value, 2), "unit": "GFLOP/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": f"synthetic: i.i.d. uniform(-0.5,0.5), splitmix64 counter generator, seed {seed}",
                 "config": {"workload": wl["name"], "M": n, "N": n, "NB": nb, "IB": ib, "nb_ib_source": src,
-                           "parallelism": f"1D block-cyclic tile columns over {world} GPUs, NCCL broadcast "
-                                          "of panel V/T per DAG level",
+                           "parallelism": (f"1D block-cyclic tile columns over {world} GPUs; each rank runs its "
+                                           "share of the DAG in the persistent dataflow kernel, packed panel "
+                                           "V/T tiles pushed to the consumers over peer memory (NVLink)")
+                           if dataflow else (f"1D block-cyclic tile columns over {world} GPUs, NCCL broadcast "
+                                             "of panel V/T per DAG level"),
+                           "schedule": "dataflow" if dataflow else "levels",
                            "l2": "per-rank input > 126 MB L2; A restored from a pristine device copy each step"},
                 "pct_fp64_peak": round(100 * value / (world * FP64_PEAK_TFLOPS * 1e3), 2),
                 "roofline": None, "cpu_baseline": None, "e2e": None, "nonfinite": int(bad.item()),
-                "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+                "gpu_launches": launches * args.steps, "clocks": clk.summary(), "verify": verify}
         print(json.dumps(line), flush=True)
     tq.dist_finalize()
     dist.destroy_process_group()
+
+
+def verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nloc):
+    """P>1 verification: every rank's factored tile columns and T tiles are
+    sent to rank 0, which factors the same matrix on its own GPU with
+    tileqr_factor and compares BITWISE (the distributed result must be
+    identical for the same (NB, IB))."""
+    import torch
+    torch.cuda.synchronize()
+    ok = True
+    if rank == 0:
+        ref = torch.empty((n, n), dtype=torch.float64, device=dev)
+        tq.rng_uniform(ref, n, n, seed=seed)
+        Tref, _ = tq.factor(ref, n, n, nb, ib)
+        torch.cuda.synchronize()
+        refm = ref.t()   # the factored matrix (column-major storage)
+        nt = mt
+        for r in range(world):
+            cols = list(range(r, nt, world))
+            if not cols:
+                continue
+            if r == 0:
+                buf, tb = A, T
+            else:
+                buf = torch.empty(len(cols) * mt * nb * nb, dtype=torch.float64, device=dev)
+                tb = torch.empty(len(cols) * mt * ib * nb, dtype=torch.float64, device=dev)
+                dist.recv(buf, src=r)
+                dist.recv(tb, src=r)
+            v = buf.view(len(cols), mt, nb, nb)
+            tv = tb.view(len(cols), mt, nb * ib)
+            for j, c in enumerate(cols):
+                for m in range(mt):
+                    i0, i1 = m * nb, min(n, (m + 1) * nb)
+                    j0, j1 = c * nb, min(n, (c + 1) * nb)
+                    got = v[j, m].t()[: i1 - i0, : j1 - j0]
+                    ok = ok and bool(torch.equal(got, refm[i0:i1, j0:j1]))
+                    if m >= c:
+                        o = (m + c * mt) * ib * nb
+                        ok = ok and bool(torch.equal(tv[j, m], Tref[o:o + ib * nb]))
+        del ref, Tref
+    elif nloc > 0:
+        dist.send(A, dst=0)
+        dist.send(T, dst=0)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.broadcast(flag, src=0)
+    return {"bitwise_equal_to_single_gpu": bool(flag.item()),
+            "how": "all ranks' tile columns and T gathered on rank 0 and compared with tileqr_factor of the same "
+                   "matrix on rank 0's GPU"}
 
 
 def main():
@@ -455,6 +513,7 @@ def main():
     ap.add_argument("--ib", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--verify", action="store_true", help="N>1: bitwise check against a 1-GPU tileqr_factor")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "tileqr":
         ap.error("--warmup must be >= 3")

@@ -210,7 +210,13 @@ int tileqr_update_packed_batched(int larfb, int NB, int IB, int batch, const dou
  *   Returns the best (NB, IB) at N in *h_NB, *h_IB.  Synchronizes the current
  *   device.  report_json_path (nullable) receives the Step-1 data set, the
  *   candidate set and every Step-2 sample as JSON.
- *   Errors: -1 M, -2 N, -3 ngpus (must be 1 here; see tileqr_dist_factor),
+ *   ngpus > 1: collective over the nranks == ngpus ranks of tileqr_dist_init
+ *     (square problems): every rank runs Step 1, all decide on rank 0's
+ *     Step-1 data set (NCCL broadcast), and Step 2 times tileqr_dist_factor,
+ *     each run's time the max over ranks (PAPER.md:620-623 tunes per core
+ *     count; here per GPU count).  TILEQR_TUNE_DIST=1 takes that path on one
+ *     rank too.
+ *   Errors: -1 M, -2 N, -3 ngpus (< 1, or != the dist ranks, or M != N),
  *   -4 heuristic not in {0,1,2}, -6/-7 NULL outputs.
  * ------------------------------------------------------------------------ */
 int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h_NB, int* h_IB,
@@ -238,39 +244,81 @@ int tileqr_payg_prune(int n, const int* h_nb, const double* h_gflops, int* h_kee
 int tileqr_num_levels(int64_t MT, int64_t NT, int64_t* n_levels);
 
 /* ------------------------------------------------------------------------
- * Multi-GPU: one process per GPU, tile columns 1D block-cyclic (tile column
- * n lives on rank n mod nranks), panel V/T tiles broadcast from the owner of
- * tile column k with NCCL over NVLink each DAG level.
+ * Multi-GPU: one process per GPU, tile columns 1D
+ * block-cyclic -- tile column n lives on rank n mod nranks, stored locally
+ * (local column j <-> global n = rank + j*nranks).  GEQRT(k) and the TSQRT
+ * chain of panel k run on the owner of column k; LARFB(k,n) / SSRFB(k,m,n)
+ * on the owner of column n.  Two schedules:
+ *  - dataflow (default for NB % 32 == 0, NB <= 256, IB in {8,16,24,32}):
+ *    each rank runs its share of the DAG in the persistent dataflow kernel;
+ *    the panel broadcast is fused into it -- the owner pushes every packed
+ *    reflector tile (V and T) over peer memory (NVLink, buffers mapped with
+ *    cudaIpc, handles exchanged over NCCL) into each consumer's slot and
+ *    raises the consumer's arrival counter, which its update items acquire
+ *    at system scope.  No collective on the data path, no level barriers.
+ *  - levels (TILEQR_DIST_SCHED=levels or other (NB, IB); square only): the
+ *    level-synchronous launcher with one grouped ncclBroadcast of the level's
+ *    panel tiles per DAG level (the NCCL baseline).
+ * Both are bitwise equal to tileqr_factor for the same (NB, IB).
  * ------------------------------------------------------------------------ */
 /* h_nccl_unique_id: 128-byte ncclUniqueId from rank 0 (e.g. via
  * torch.distributed); device: CUDA ordinal this rank uses. */
 int tileqr_dist_init(int nranks, int rank, const void* h_nccl_unique_id, int device);
 /* Writes a fresh ncclUniqueId (128 bytes) into h_id (rank 0 only). */
 int tileqr_dist_unique_id(void* h_id);
-/* Local tile storage of an N x N factorization (square, NB | padded N):
+/* Local tile storage of an M x N factorization (padded as tileqr_factor):
  * n_local = number of tile columns owned by this rank; A_local holds them in
  * tile layout: local column j (global n = rank + j*nranks) has its MT tiles
- * at A_local + (m + j*MT)*NB*NB, column-major within a tile (ld = NB).
- * T_local: tile (m, j) at (m + j*MT)*IB*NB. */
+ * (MT = ceil(M/NB)) at A_local + (m + j*MT)*NB*NB, column-major within a
+ * tile (ld = NB).  T_local: tile (m, j) at (m + j*MT)*IB*NB. */
 int tileqr_dist_local_cols(int64_t N, int NB, int* n_local);
 /* Fill this rank's local tile columns with the synthetic generator below
- * (global idx = i + j*N), zero/identity padding as tileqr_factor does. */
-int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed,
+ * (global idx = i + j*M of the M x N matrix), zero / identity padding as
+ * tileqr_factor does.  Errors: -1 M, -2 N, -3 NB, -4 A_local NULL. */
+int tileqr_dist_fill_uniform(int64_t M, int64_t N, int NB, double* A_local, uint64_t seed,
                              tileqr_stream_t stream);
-/* Host-only schedule of one DAG level for `rank` of `nranks` (square MT x MT
- * tiles), exported so the multi-GPU plan can be tested without GPUs.  Writes
- * 5-tuples (kind, k, m, n, root) to h_out (capacity `cap` int64s): first the
- * rank's panel tasks (kind 0 GEQRT(k), 1 TSQRT(k,m)), then the level's
- * broadcast items (kind 4: V/T of tile (m,k) from root = k mod nranks, same
- * list and order on every rank), then the rank's update tasks (2 LARFB(k,n),
- * 3 SSRFB(k,m,n), n = local columns); h_counts[3] = the three counts.
+/* Host-only schedule of one DAG level of the LEVEL-SYNCHRONOUS path for
+ * `rank` of `nranks` (square MT x MT tiles), exported so the multi-GPU plan
+ * can be tested without GPUs.  Writes 5-tuples (kind, k, m, n, root) to h_out
+ * (capacity `cap` int64s): first the rank's panel tasks (kind 0 GEQRT(k), 1
+ * TSQRT(k,m)), then the level's broadcast items (kind 4: V/T of tile (m,k)
+ * from root = k mod nranks, same list and order on every rank), then the
+ * rank's update tasks (2 LARFB(k,n), 3 SSRFB(k,m,n), n = local columns);
+ * h_counts[3] = the three counts.
  * Errors: -1..-4 bad MT/nranks/rank/level, -6 capacity too small, -7 NULL. */
 int tileqr_dist_plan_level(int64_t MT, int nranks, int rank, int64_t level, int64_t* h_out,
                            int64_t cap, int64_t* h_counts);
-/* Factor the distributed matrix in place; d_info as tileqr_factor. */
-int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
+/* Host-only work list of one rank under the DATAFLOW schedule (the items its
+ * persistent kernel claims, in claim order), for CPU tests of the plan:
+ * per item 10 int64 (kind, k, m, n, s, task, ndep, dep0, dep1, dep2) with kind
+ * 0 GEQRT, 1 TSQRT, 2 LARFB, 3 SSRFB, 7 COPY; s = the panel sub-task (inner
+ * panels [s*sub_cols, (s+1)*sub_cols)), the update slab, or for COPY the
+ * destination rank; task / dep = global task ids (a dependency on an id of
+ * kind 6 ARRIVE is the arrival of the COPY of reflector tile (k, m) at this
+ * rank).  workers: resident CTAs per rank in the schedule simulation;
+ * sub_cols: columns per panel sub-task (IB | sub_cols | NB).  *h_count
+ * receives the item count; h_out (capacity cap int64s) may be NULL.
+ * Errors: -1 M, -2 N, -3 NB/IB, -5 nranks, -6 rank, -7 workers, -8 sub_cols,
+ * -10 capacity too small, -11 h_count NULL. */
+int tileqr_dist_plan_items(int64_t M, int64_t N, int NB, int IB, int nranks, int rank, int workers,
+                           int sub_cols, int64_t* h_out, int64_t cap, int64_t* h_count);
+/* Factor the distributed M x N matrix in place (NB = IB = 0: the decision
+ * table at (order, nranks)); d_info as tileqr_factor.  Collective: every rank
+ * calls it with the same arguments.  Errors: -1 M, -2 N, -3 A_local NULL,
+ * -4 NB, -5 IB, -6 T_local NULL; -1 also for M != N on the levels path. */
+int tileqr_dist_factor(int64_t M, int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
                        tileqr_stream_t stream);
 void tileqr_dist_finalize(void);
+/* The dataflow multi-rank factorization with nranks EMULATED ranks on the
+ * current GPU (one process, no NCCL): rank r's local columns in
+ * h_A_local[r] / h_T_local[r] (device pointers, layout as above), the
+ * packed-tile pushes of the COPY items going to the other ranks' buffers on
+ * the same device.  Same work lists and kernel code as tileqr_dist_factor,
+ * all ranks' items in one launch -- the way the multi-rank path is tested on
+ * a single GPU.  Errors: -1 nranks, -2 M, -3 N, -4 NULL buffers, -5 NB/IB,
+ * -6 (NB, IB) outside the dataflow set, -7 h_T_local NULL. */
+int tileqr_dist_emulate(int nranks, int64_t M, int64_t N, double* const* h_A_local, int NB, int IB,
+                        double* const* h_T_local, int* d_info, tileqr_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Utilities.

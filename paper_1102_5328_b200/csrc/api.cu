@@ -35,22 +35,22 @@ namespace tileqr {
 
 #define TQ_DECL_DAG(nb)                                                                        \
   int launch_dag_nb##nb(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm, \
-                        unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io);
+                        unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io, int mode);
 TQ_DECL_DAG(32) TQ_DECL_DAG(64) TQ_DECL_DAG(96) TQ_DECL_DAG(128) TQ_DECL_DAG(160) TQ_DECL_DAG(192)
 TQ_DECL_DAG(224) TQ_DECL_DAG(256)
 #undef TQ_DECL_DAG
 
-static int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                      unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io) {
+int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
+               unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io, int mode) {
   switch (NB) {
-    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 32: return launch_dag_nb32(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 64: return launch_dag_nb64(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 96: return launch_dag_nb96(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 128: return launch_dag_nb128(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 160: return launch_dag_nb160(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 192: return launch_dag_nb192(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 224: return launch_dag_nb224(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 256: return launch_dag_nb256(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
     default: return TILEQR_ERR_CUDA;
   }
 }
@@ -247,8 +247,10 @@ static bool dag_enabled(int NB, int IB) {
   return dag::dag_supported(NB, IB) && (NB > 128 || v2_supported(NB, IB));
 }
 
+bool dag_path_supported(int NB, int IB) { return dag::dag_supported(NB, IB) && v2_supported(NB, IB); }
+
 // Columns of one GEQRT / TSQRT sub-task (a multiple of IB).
-static int panel_sub_cols(int NB, int IB) {
+int panel_sub_cols(int NB, int IB) {
   const char* e = getenv("TILEQR_PANEL_SUB");
   int sc = e ? atoi(e) : 32;
   if (sc <= 0 || sc >= NB) sc = NB;
@@ -300,7 +302,7 @@ static int build_dag(FactorWS* ws, bool io) {
   auto idLD = [&](int64_t n) { return ntask0 + n; };
   auto idST = [&](int64_t n) { return ntask0 + NT + n; };
   auto idAR = [&](int64_t n) { return ntask0 + 2 * NT + n; };
-  constexpr int kArrive = 6;  // host-only pseudo kind: set by the copy stream
+  constexpr int kArrive = dag::kArrive;  // host-only pseudo kind: set by the copy stream
   using Task = sched::Task;
   std::vector<Task> tk(ntask);
   for (int64_t k = 0; k < KT; ++k) {
@@ -532,7 +534,7 @@ static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStre
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
   int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, ws->nsm, prof, stream,
-                      &ws->dag_grid, io);
+                      &ws->dag_grid, io, io ? dag::kModeIO : dag::kModePlain);
   if (rc) return rc;
   if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
   ws->dag_timed = g_timing != 0;

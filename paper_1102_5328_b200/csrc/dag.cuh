@@ -37,6 +37,32 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+  int v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// COPY item (multi-rank dataflow): push one packed reflector
+// tile (V_p and T_p of every inner panel, update_v2.cuh layout) from this
+// rank's slot to the same slot of a peer rank -- a peer-mapped (NVLink)
+// pointer, or another buffer of the same GPU when the ranks are emulated.
+// The source was just written by a panel item on another SM: L2 loads.
+static __device__ __noinline__ void copy_body(const double* __restrict__ src, double* __restrict__ dst, int ndbl) {
+  const int n2 = ndbl >> 1;
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* d2 = reinterpret_cast<double2*>(dst);
+  for (int e0 = threadIdx.x; e0 < n2; e0 += 4 * blockDim.x) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + u * (int)blockDim.x < n2) v[u] = __ldcg(s2 + e0 + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + u * (int)blockDim.x < n2) d2[e0 + u * blockDim.x] = v[u];
+  }
+  if ((ndbl & 1) && threadIdx.x == 0) dst[ndbl - 1] = __ldcg(src + ndbl - 1);
+}
 
 // Update items run the barrier-free packed-reflector body (update_v2.cuh,
 // column groups of the packed tile streamed through a TMA ring) for every
@@ -203,7 +229,7 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 // IO: the instantiation for tileqr_factor_host, with the LOAD / STORE items
 // (their code in the kernel costs the device-only factorization ~1.8 %, same
 // box A/B, so tileqr_factor runs an instantiation without them).
-template <int NB, int KW, bool IO>
+template <int NB, int KW, int MODE>
 __global__ void __launch_bounds__(dag_warps(NB) * 32, dag_ctas_per_sm(NB))
 dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int IB,
            unsigned long long* prof, const DagIO* io) {
@@ -238,17 +264,34 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         const Item& it = s_desc[slot];
         int need[3], got[3];
         const int nd = it.ndep;
+        if constexpr (MODE == kModeDist) {  // peer-written counters: system scope
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {  // all flags in flight at once
-          need[d] = d < nd ? it.need[d] : 0;
-          got[d] = d < nd ? ld_acquire(done + it.dep[d]) : 0;
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-          while (got[d] < need[d]) {
-            __nanosleep(64);
-            got[d] = ld_acquire(done + it.dep[d]);
+          for (int d = 0; d < 3; ++d) {
+            need[d] = d < nd ? it.need[d] : 0;
+            got[d] = d >= nd ? 0 : need[d] < 0 ? ld_acquire_sys(done + it.dep[d]) : ld_acquire(done + it.dep[d]);
           }
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const bool sys = need[d] < 0;
+            const int want = sys ? -need[d] : need[d];
+            while (got[d] < want) {
+              __nanosleep(64);
+              got[d] = sys ? ld_acquire_sys(done + it.dep[d]) : ld_acquire(done + it.dep[d]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {  // all flags in flight at once
+            need[d] = d < nd ? it.need[d] : 0;
+            got[d] = d < nd ? ld_acquire(done + it.dep[d]) : 0;
+          }
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            while (got[d] < need[d]) {
+              __nanosleep(64);
+              got[d] = ld_acquire(done + it.dep[d]);
+            }
+        }
         if (prof) prof[3 * (size_t)cur + 1] = globaltimer();
         if constexpr (V2) {
           if (it.kind == kLarfb || it.kind == kSsrfb) {
@@ -309,10 +352,13 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
                                                                      it.p[2], 1, it.col0, smem);
         break;
       case kLoad:
-        if constexpr (IO) load_body<NB>(io, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
+        if constexpr (MODE == kModeIO) load_body<NB>(io, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
         break;
       case kStore:
-        if constexpr (IO) store_body<NB>(io, it.aux[0], it.aux[2], it.aux[3]);
+        if constexpr (MODE == kModeIO) store_body<NB>(io, it.aux[0], it.aux[2], it.aux[3]);
+        break;
+      case kCopy:
+        if constexpr (MODE == kModeDist) copy_body(it.p[0], it.p[1], it.aux[0]);
         break;
       default:  // SSRFB: columns as LARFB
         if (it.aux[0] <= it.col0) break;
@@ -332,8 +378,16 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       // STORE counters are read by the copy engine (cuStreamWaitValue32 on
       // the device-to-host stream), not by GPU threads: publish them at
       // system scope
-      if (IO && it.kind == kStore) __threadfence_system();
-      else __threadfence();
+      if (MODE == kModeIO && it.kind == kStore) {
+        __threadfence_system();
+      } else if (MODE == kModeDist && it.kind == kCopy) {
+        // the pushed tile (NVLink stores of every thread, ordered before this
+        // point by the CTA barrier) is released to the peer at system scope
+        __threadfence_system();
+        atomicAdd_system(reinterpret_cast<int*>(it.p[2]), 1);
+      } else {
+        __threadfence();
+      }
       atomicAdd(done + it.task, 1);
       if (prof) prof[3 * (size_t)i + 2] = globaltimer();
     }
@@ -343,8 +397,9 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
 
 template <int NB, int KW>
 int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                 unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io) {
-  auto kern = io ? dag_kernel<NB, KW, true> : dag_kernel<NB, KW, false>;
+                 unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io, int mode) {
+  auto kern = mode == kModeIO ? dag_kernel<NB, KW, kModeIO>
+            : mode == kModeDist ? dag_kernel<NB, KW, kModeDist> : dag_kernel<NB, KW, kModePlain>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -369,15 +424,15 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
 
 template <int NB>
 int launch_dag_nb(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
-                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io) {
+                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io, int mode) {
   switch (IB) {
-    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
-    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 8: return launch_dag_t<NB, 8>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
+    case 16: return launch_dag_t<NB, 16>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
     case 24:
-      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+      if constexpr (NB % 24 == 0) return launch_dag_t<NB, 24>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
       set_error("DAG kernel: IB does not divide NB");
       return TILEQR_ERR_CUDA;
-    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+    case 32: return launch_dag_t<NB, 32>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
     default: set_error("DAG kernel: IB not in {8,16,24,32}"); return TILEQR_ERR_CUDA;
   }
 }

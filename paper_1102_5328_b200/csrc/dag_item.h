@@ -17,7 +17,14 @@ __host__ __device__ constexpr int dag_warps(int NB) { return NB <= 128 ? 4 : 8; 
 __host__ __device__ constexpr int dag_ctas_per_sm(int NB) { return NB <= 128 ? 2 : 1; }
 #endif
 
-enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3, kLoad = 4, kStore = 5 };
+enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3, kLoad = 4, kStore = 5,
+            kArrive = 6,  // host-only pseudo task: completed by a copy engine / a peer, not by a CTA
+            kCopy = 7 };  // multi-rank dataflow: push a packed reflector tile to a peer rank
+
+// Kernel instantiations of the dataflow kernel (dag.cuh): the device-only
+// factorization, the host-buffer pipeline (LOAD / STORE items) and the
+// multi-rank dataflow factorization (COPY items, system-scope signals).
+enum Mode { kModePlain = 0, kModeIO = 1, kModeDist = 2 };
 
 // One work item: a whole panel task, or a column slab of an update task.
 struct Item {
@@ -27,10 +34,12 @@ struct Item {
                  // sub-task's inner-panel columns [col0 & 0xffff, col0 >> 16)
   int ndep;
   int dep[3];    // tasks whose counters must reach need[] before the item runs
-  int need[3];
+  int need[3];   // required counts; negative (-count) in the multi-rank kernel: the counter
+                 // is written by a peer GPU, so it is acquired at system scope
   double* p[4];  // GEQRT: A, -, T; TSQRT: R, A2, T; LARFB: V, T, C; SSRFB: V2, T, C1, C2
   double* pk;    // packed reflector tile (NB <= 128): written by GEQRT/TSQRT, read by LARFB/SSRFB
-  int aux[4];    // LOAD / STORE (host-buffer pipeline): tile column n, tile rows [aux[1], aux[2]);
+  int aux[4];    // COPY: aux[0] = doubles to push from p[0] to p[1], then +1 on the peer counter (int*)p[2];
+                 // LOAD / STORE (host-buffer pipeline): tile column n, tile rows [aux[1], aux[2]);
                  // LARFB / SSRFB: aux[0] = column limit in the tile (N - n*NB, at most NB):
                  // the columns past it are padding, which every update leaves exactly as is
 };

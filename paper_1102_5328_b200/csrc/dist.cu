@@ -29,11 +29,13 @@
 #include <string>
 #include <vector>
 
+#include "dag_item.h"
+#include "dist_dag.h"
 #include "internal.h"
 
 namespace tileqr {
 
-int launch_dist_fill(int64_t N, int NB, int64_t MT, int nranks, int rank, int64_t nloc, double* A,
+int launch_dist_fill(int64_t M, int64_t N, int NB, int64_t MT, int nranks, int rank, int64_t nloc, double* A,
                      uint64_t seed, cudaStream_t s);
 int launch_nonfinite_check(const double* A, int64_t n, int* d_info, cudaStream_t s);
 
@@ -124,6 +126,145 @@ struct DistState {
 
 DistState g_d;
 
+// Multi-rank dataflow path (dist_dag.cu): this rank's work list, its slot and
+// counter buffers, and the peers' slot / counter buffers mapped with cudaIpc.
+struct DistDag {
+  int64_t M = -1, N = -1;
+  int NB = 0, IB = 0, SC = 0;
+  double* A = nullptr;
+  double* T = nullptr;
+  std::shared_ptr<dd::Plan> plan;
+  double* slots = nullptr;
+  int* ctr = nullptr;   // [claim cursor | 256 | ntask counters]
+  int* red = nullptr;   // barrier scratch
+  std::vector<double*> peer_slots;
+  std::vector<int*> peer_ctr;
+  dag::Item* d_items = nullptr;
+  int nitems = 0, nsm = 0;
+  void release() {
+    for (size_t r = 0; r < peer_slots.size(); ++r)
+      if ((int)r != g_d.rank) {
+        if (peer_slots[r]) cudaIpcCloseMemHandle(peer_slots[r]);
+        if (peer_ctr[r]) cudaIpcCloseMemHandle(peer_ctr[r]);
+      }
+    peer_slots.clear();
+    peer_ctr.clear();
+    cudaFree(slots);
+    cudaFree(ctr);
+    cudaFree(red);
+    cudaFree(d_items);
+    slots = nullptr;
+    ctr = red = nullptr;
+    d_items = nullptr;
+    plan.reset();
+    M = N = -1;
+  }
+};
+DistDag g_dd;
+
+// Build (or reuse) this rank's dataflow work list for (M, N, NB, IB).
+int dd_prepare(int64_t M, int64_t N, double* A_local, int NB, int IB, double* T_local, cudaStream_t s) {
+  const int SC = panel_sub_cols(NB, IB);
+  if (g_dd.plan && g_dd.M == M && g_dd.N == N && g_dd.NB == NB && g_dd.IB == IB && g_dd.SC == SC &&
+      g_dd.A == A_local && g_dd.T == T_local)
+    return 0;
+  g_dd.release();
+  const int P = g_d.nranks, me = g_d.rank;
+  TQ_CUDA(cudaDeviceGetAttribute(&g_dd.nsm, cudaDevAttrMultiProcessorCount, g_d.device));
+  int rc = dd::build_plan(M, N, NB, IB, P, g_dd.nsm * dag::dag_ctas_per_sm(NB), SC, &g_dd.plan);
+  if (rc) return rc;
+  const dd::Plan& p = *g_dd.plan;
+  const size_t pkd = v2_pk_doubles(NB, IB);
+  if (cudaMalloc(&g_dd.slots, std::max<size_t>(1, (size_t)p.nslots() * pkd) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&g_dd.ctr, (size_t)(257 + p.ntask) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&g_dd.red, 64 * P) != cudaSuccess) {
+    cudaGetLastError();
+    g_dd.release();
+    set_error("tileqr_dist_factor: workspace allocation failed");
+    return TILEQR_ERR_ALLOC;
+  }
+  g_dd.peer_slots.assign(P, nullptr);
+  g_dd.peer_ctr.assign(P, nullptr);
+  g_dd.peer_slots[me] = g_dd.slots;
+  g_dd.peer_ctr[me] = g_dd.ctr;
+  if (P > 1) {  // exchange the slot / counter buffers: cudaIpc handles all-gathered over NCCL
+    cudaIpcMemHandle_t h[2];
+    TQ_CUDA(cudaIpcGetMemHandle(&h[0], g_dd.slots));
+    TQ_CUDA(cudaIpcGetMemHandle(&h[1], g_dd.ctr));
+    char* d_h = nullptr;
+    TQ_CUDA(cudaMalloc(&d_h, sizeof h * P));
+    TQ_CUDA(cudaMemcpy(d_h + sizeof h * me, h, sizeof h, cudaMemcpyHostToDevice));
+    ncclResult_t nr = ncclAllGather(d_h + sizeof h * me, d_h, sizeof h, ncclChar, g_d.comm, s);
+    std::vector<cudaIpcMemHandle_t> all(2 * P);
+    cudaError_t ce = nr == ncclSuccess ? cudaStreamSynchronize(s) : cudaSuccess;
+    if (nr == ncclSuccess && ce == cudaSuccess)
+      ce = cudaMemcpy(all.data(), d_h, sizeof h * P, cudaMemcpyDeviceToHost);
+    cudaFree(d_h);
+    if (nr != ncclSuccess) {
+      g_dd.release();
+      set_error(std::string("tileqr_dist_factor: handle exchange failed: ") + ncclGetErrorString(nr));
+      return TILEQR_ERR_NCCL;
+    }
+    if (ce != cudaSuccess) { g_dd.release(); return cuda_fail(ce, "handle exchange", __FILE__, __LINE__); }
+    for (int r = 0; r < P; ++r) {
+      if (r == me) continue;
+      void* ps = nullptr;
+      void* pc = nullptr;
+      cudaError_t e1 = cudaIpcOpenMemHandle(&ps, all[2 * r], cudaIpcMemLazyEnablePeerAccess);
+      cudaError_t e2 = e1 == cudaSuccess ? cudaIpcOpenMemHandle(&pc, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess)
+                                         : e1;
+      g_dd.peer_slots[r] = static_cast<double*>(ps);
+      g_dd.peer_ctr[r] = static_cast<int*>(pc);
+      if (e2 != cudaSuccess) {
+        g_dd.release();
+        return cuda_fail(e2, "cudaIpcOpenMemHandle (peer slots / counters)", __FILE__, __LINE__);
+      }
+    }
+  }
+  std::vector<dd::RankBufs> bufs(P);
+  for (int r = 0; r < P; ++r)
+    bufs[r] = {r == me ? A_local : nullptr, r == me ? T_local : nullptr, g_dd.peer_slots[r], g_dd.peer_ctr[r] + 257};
+  std::vector<dag::Item> items;
+  rc = dd::emit_items(p, me, bufs, false, &items);
+  if (rc) { g_dd.release(); return rc; }
+  g_dd.nitems = (int)items.size();
+  if (cudaMalloc(&g_dd.d_items, std::max<size_t>(1, items.size()) * sizeof(dag::Item)) != cudaSuccess) {
+    cudaGetLastError();
+    g_dd.release();
+    set_error("tileqr_dist_factor: work list allocation failed");
+    return TILEQR_ERR_ALLOC;
+  }
+  TQ_CUDA(cudaMemcpy(g_dd.d_items, items.data(), items.size() * sizeof(dag::Item), cudaMemcpyHostToDevice));
+  g_dd.M = M; g_dd.N = N; g_dd.NB = NB; g_dd.IB = IB; g_dd.SC = SC;
+  g_dd.A = A_local; g_dd.T = T_local;
+  return 0;
+}
+
+// The dataflow factorization of this rank's columns: counters zeroed, a
+// barrier (every rank's counters are zero before any peer pushes into them),
+// then the persistent kernel.  No collective on the data path.
+int dd_factor(int64_t M, int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info, cudaStream_t s) {
+  int rc = dd_prepare(M, N, A_local, NB, IB, T_local, s);
+  if (rc) return rc;
+  const dd::Plan& p = *g_dd.plan;
+  const int64_t nloc = dd::local_cols(p.NT, g_d.nranks, g_d.rank);
+  if (nloc > 0 && d_info) {
+    rc = launch_nonfinite_check(A_local, nloc * p.MT * NB * (int64_t)NB, d_info, s);
+    if (rc) return rc;
+  }
+  TQ_CUDA(cudaMemsetAsync(g_dd.ctr, 0, (size_t)(257 + p.ntask) * sizeof(int), s));
+  if (g_d.nranks > 1) TQ_NCCL(ncclAllReduce(g_dd.red, g_dd.red, 1, ncclInt, ncclSum, g_d.comm, s));
+  int grid = 0;
+  return launch_dag(NB, IB, g_dd.d_items, g_dd.nitems, g_dd.ctr, g_dd.ctr + 257, g_dd.nsm, nullptr, s, &grid,
+                    nullptr, dag::kModeDist);
+}
+
+bool dist_dataflow(int NB, int IB) {
+  const char* e = getenv("TILEQR_DIST_SCHED");
+  if (e && strcmp(e, "levels") == 0) return false;
+  return dag_path_supported(NB, IB);
+}
+
 int64_t slot_off(int64_t MT, int64_t k) { return k * MT - k * (k - 1) / 2; }
 
 void free_shape() {
@@ -140,6 +281,43 @@ void free_shape() {
 }
 
 }  // namespace
+
+// ---- collectives for tileqr_tune (ngpus > 1), over the library's comm -----
+int dist_ranks(int* nranks, int* rank) {
+  if (!g_d.init) {
+    set_error("tileqr_dist_init not called");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  *nranks = g_d.nranks;
+  *rank = g_d.rank;
+  return 0;
+}
+
+// op 0: broadcast h[0:n] from rank 0; op 1: element-wise max over ranks.
+int dist_host_collective(double* h, int n, int op) {
+  if (!g_d.init) return TILEQR_ERR_NOT_INIT;
+  if (n <= 0) return 0;
+  double* d = nullptr;
+  TQ_CUDA(cudaMalloc(&d, n * sizeof(double)));
+  cudaStream_t s = g_d.sc;
+  int rc = 0;
+  cudaError_t e = cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, s);
+  ncclResult_t r = ncclSuccess;
+  if (e == cudaSuccess)
+    r = op == 0 ? ncclBroadcast(d, d, n, ncclDouble, 0, g_d.comm, s)
+                : ncclAllReduce(d, d, n, ncclDouble, ncclMax, g_d.comm, s);
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && r == ncclSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(d);
+  if (r != ncclSuccess) {
+    set_error(std::string("tileqr_tune: NCCL collective failed: ") + ncclGetErrorString(r));
+    rc = TILEQR_ERR_NCCL;
+  } else if (e != cudaSuccess) {
+    rc = cuda_fail(e, "tileqr_tune collective", __FILE__, __LINE__);
+  }
+  return rc;
+}
+
 }  // namespace tileqr
 
 using namespace tileqr;
@@ -192,10 +370,11 @@ int tileqr_dist_local_cols(int64_t N, int NB, int* n_local) {
   return 0;
 }
 
-int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed,
+int tileqr_dist_fill_uniform(int64_t M, int64_t N, int NB, double* A_local, uint64_t seed,
                              tileqr_stream_t stream) {
-  if (N < 0) return -1;
-  if (NB < 1 || NB > 512) return -2;
+  if (M < 0) return -1;
+  if (N < 0) return -2;
+  if (NB < 1 || NB > 512) return -3;
   if (!g_d.init) {
     set_error("tileqr_dist_fill_uniform: tileqr_dist_init not called");
     return TILEQR_ERR_NOT_INIT;
@@ -203,10 +382,10 @@ int tileqr_dist_fill_uniform(int64_t N, int NB, double* A_local, uint64_t seed,
   int nloc = 0;
   int rc = tileqr_dist_local_cols(N, NB, &nloc);
   if (rc) return rc;
-  if (nloc == 0 || N == 0) return 0;
-  if (!A_local) return -3;
-  const int64_t MT = (N + NB - 1) / NB;
-  return launch_dist_fill(N, NB, MT, g_d.nranks, g_d.rank, nloc, A_local, seed,
+  if (nloc == 0 || N == 0 || M == 0) return 0;
+  if (!A_local) return -4;
+  const int64_t MT = (M + NB - 1) / NB;
+  return launch_dist_fill(M, N, NB, MT, g_d.nranks, g_d.rank, nloc, A_local, seed,
                           reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -239,27 +418,41 @@ int tileqr_dist_plan_level(int64_t MT, int nranks, int rank, int64_t level, int6
   return 0;
 }
 
-int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
+int tileqr_dist_factor(int64_t M, int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
                        tileqr_stream_t stream) {
-  if (N < 0) return -1;
-  if (NB < 1 || NB > 512) return -3;
-  if (IB < 1 || IB > NB || NB % IB) return -4;
+  if (M < 0) return -1;
+  if (N < 0) return -2;
   if (!g_d.init) {
     set_error("tileqr_dist_factor: tileqr_dist_init not called");
     return TILEQR_ERR_NOT_INIT;
   }
+  if (NB == 0 && IB == 0) {  // the installed decision table at (order, nranks)
+    bool f = false;
+    lookup_pair(M, N, g_d.nranks, &NB, &IB, &f);
+  }
+  if (NB < 1 || NB > 512) return -4;
+  if (IB < 1 || IB > NB || NB % IB) return -5;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (d_info) {
     int rc = launch_zero_int(d_info, s);
     if (rc) return rc;
   }
-  if (N == 0) return 0;
+  if (M == 0 || N == 0) return 0;
+  {
+    int nl = 0;
+    tileqr_dist_local_cols(N, NB, &nl);
+    if (nl > 0 && !A_local) return -3;
+    if (nl > 0 && !T_local) return -6;
+  }
+  if (dist_dataflow(NB, IB)) return dd_factor(M, N, A_local, NB, IB, T_local, d_info, s);
+  if (M != N) {
+    set_error("tileqr_dist_factor: the level-synchronous (NCCL broadcast) path is square only");
+    return -1;
+  }
   const int P = g_d.nranks, me = g_d.rank;
   const int64_t MT = (N + NB - 1) / NB;
   int nloc = 0;
   tileqr_dist_local_cols(N, NB, &nloc);
-  if (nloc > 0 && !A_local) return -2;
-  if (nloc > 0 && !T_local) return -5;
   const size_t tile = (size_t)NB * NB, ttile = (size_t)IB * NB;
   auto loc = [&](int64_t m, int64_t n) { return A_local + (size_t)(m + (n / P) * MT) * tile; };
   auto locT = [&](int64_t m, int64_t n) { return T_local + (size_t)(m + (n / P) * MT) * ttile; };
@@ -406,6 +599,7 @@ int tileqr_dist_factor(int64_t N, double* A_local, int NB, int IB, double* T_loc
 void tileqr_dist_finalize(void) {
   if (!g_d.init) return;
   cudaDeviceSynchronize();
+  g_dd.release();
   free_shape();
   if (g_d.comm) ncclCommDestroy(g_d.comm);
   for (cudaStream_t st : {g_d.sp, g_d.su, g_d.sc})

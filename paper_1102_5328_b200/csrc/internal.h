@@ -76,6 +76,15 @@ const char* ssrfb_impl_name(int NB, int IB);
 // Decision-table lookup (table.cu): (NB, IB) for an M x N factorization on
 // ngpus GPUs; the built-in default when no table is installed (*from_table false).
 int lookup_pair(int64_t M, int64_t N, int ngpus, int* NB, int* IB, bool* from_table);
+// ---- dataflow kernel (dag.cuh, launched through api.cu) ----------------------
+namespace dag { struct Item; struct DagIO; }
+int launch_dag(int NB, int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
+               unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io, int mode);
+int panel_sub_cols(int NB, int IB);       // columns of one GEQRT / TSQRT sub-task
+bool dag_path_supported(int NB, int IB);  // the dataflow kernel with packed reflector tiles runs (NB, IB)
+// ---- multi-GPU helpers (dist.cu) for tileqr_tune with ngpus > 1 -----------------
+int dist_ranks(int* nranks, int* rank);
+int dist_host_collective(double* h, int n, int op);  // op 0: broadcast from rank 0, 1: max over ranks
 // Free the cached tileqr_factor workspace of one shape (api.cu; waits for its last use).
 void release_ws(int dev, int64_t M, int64_t N, int NB, int IB);
 

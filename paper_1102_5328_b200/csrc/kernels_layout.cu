@@ -175,7 +175,7 @@ __global__ void zero_int_kernel(int* p) { *p = 0; }
 // (m, n) is the generator's value at global (i, c) = (m*NB+il, n*NB+jl),
 // idx = i + c*N, with the same padding as layout_to_tiles.
 __global__ void __launch_bounds__(kThreads)
-dist_fill_kernel(int64_t N, int NB, int64_t MT, int P, int rank, int64_t nloc, double* __restrict__ A,
+dist_fill_kernel(int64_t M, int64_t N, int NB, int64_t MT, int P, int rank, int64_t nloc, double* __restrict__ A,
                  uint64_t key) {
   const int64_t tile = (int64_t)NB * NB;
   const int64_t total = nloc * MT * tile;
@@ -186,11 +186,11 @@ dist_fill_kernel(int64_t N, int NB, int64_t MT, int P, int rank, int64_t nloc, d
     const int64_t jl = e / NB, il = e - jl * NB;
     const int64_t i = m * NB + il, c = (rank + j * P) * NB + jl;
     double v;
-    if (i < N && c < N) {
-      const uint64_t bits = splitmix64(key + (uint64_t)(i + c * N)) >> 11;
+    if (i < M && c < N) {
+      const uint64_t bits = splitmix64(key + (uint64_t)(i + c * M)) >> 11;
       v = (double)bits * 0x1.0p-53 - 0.5;
     } else {
-      v = (c >= N && i == c) ? 1.0 : 0.0;
+      v = (c >= N && i == c && c >= M) ? 1.0 : 0.0;
     }
     A[w] = v;
   }
@@ -265,9 +265,9 @@ int launch_rng_uniform(int64_t M, int64_t N, double* A, int64_t lda, uint64_t se
   return 0;
 }
 
-int launch_dist_fill(int64_t N, int NB, int64_t MT, int nranks, int rank, int64_t nloc, double* A,
+int launch_dist_fill(int64_t M, int64_t N, int NB, int64_t MT, int nranks, int rank, int64_t nloc, double* A,
                      uint64_t seed, cudaStream_t s) {
-  dist_fill_kernel<<<grid_for(nloc * MT * NB * NB), kThreads, 0, s>>>(N, NB, MT, nranks, rank, nloc, A,
+  dist_fill_kernel<<<grid_for(nloc * MT * NB * NB), kThreads, 0, s>>>(M, N, NB, MT, nranks, rank, nloc, A,
                                                                       host_splitmix64(seed));
   TQ_LAUNCH_CHECK();
   return 0;

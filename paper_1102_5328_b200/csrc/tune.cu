@@ -189,7 +189,21 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   char msg[256];
   if (M < 1) { snprintf(msg, sizeof msg, "%s: M < 1", fn); set_error(msg); return -1; }
   if (N < 1) { snprintf(msg, sizeof msg, "%s: N < 1", fn); set_error(msg); return -2; }
-  if (ngpus != 1) { snprintf(msg, sizeof msg, "%s: ngpus must be 1 (per-rank tuning)", fn); set_error(msg); return -3; }
+  int P = 1, me = 0;
+  if (ngpus < 1) { snprintf(msg, sizeof msg, "%s: ngpus < 1", fn); set_error(msg); return -3; }
+  if (ngpus > 1 && M != N) { snprintf(msg, sizeof msg, "%s: ngpus > 1 tunes square problems", fn); set_error(msg); return -3; }
+  if (ngpus > 1) {  // collective over the ranks of tileqr_dist_init: Step 2 times tileqr_dist_factor
+    if (dist_ranks(&P, &me) || P != ngpus) {
+      snprintf(msg, sizeof msg, "%s: ngpus = %d needs tileqr_dist_init with as many ranks", fn, ngpus);
+      set_error(msg);
+      return -3;
+    }
+  }
+  // TILEQR_TUNE_DIST=1 (with tileqr_dist_init done): Step 2 through tileqr_dist_factor even on one
+  // rank -- the ngpus > 1 code path on a single GPU (tests)
+  bool use_dist = P > 1;
+  if (const char* e = getenv("TILEQR_TUNE_DIST"))
+    if (e[0] == '1' && dist_ranks(&P, &me) == 0 && P == ngpus) use_dist = true;
   if (heuristic < 0 || heuristic > 2) { set_error("tileqr_tune: heuristic not in {0,1,2}"); return -4; }
   if (!h_NB) return -6;
   if (!h_IB) return -7;
@@ -318,6 +332,12 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   pkbuf = nullptr;
   cudaFree(pkp);
   pkp = nullptr;
+  if (use_dist) {  // every rank decides on rank 0's Step-1 data set (identical candidates everywhere)
+    std::vector<double> g(samples.size());
+    for (size_t i = 0; i < samples.size(); ++i) g[i] = samples[i].g;
+    TQ_TRY(dist_host_collective(g.data(), (int)g.size(), 0));
+    for (size_t i = 0; i < samples.size(); ++i) samples[i].g = g[i];
+  }
   // Property-1 ties within the Step-1 timing's repeatability (R18;
   // TILEQR_TUNE_TIE overrides the relative width)
   double tie_rel = 0.005;
@@ -349,19 +369,51 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
       tileqr_t_size(m, n, p.nb, p.ib, &t);
       tmax = std::max(tmax, t);
     }
-    if (cudaMalloc(&A0, (size_t)m * n * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&A, (size_t)m * n * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&T, std::max<size_t>(tmax, 1) * sizeof(double)) != cudaSuccess ||
+    const size_t nmat = use_dist ? 1 : (size_t)m * n;  // ngpus > 1: per-candidate local buffers below
+    if (cudaMalloc(&A0, nmat * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&A, nmat * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&T, (use_dist ? 1 : std::max<size_t>(tmax, 1)) * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&dinfo, sizeof(int)) != cudaSuccess) {
       cudaGetLastError();
       set_error("tileqr_tune: step-2 allocation failed");
       cleanup();
       return TILEQR_ERR_ALLOC;
     }
-    TQ_TRY(launch_rng_uniform(m, n, A0, m, 3, 0, s));
+    if (!use_dist) TQ_TRY(launch_rng_uniform(m, n, A0, m, 3, 0, s));
     std::vector<Pt> res;
     for (const Pt& p : alive) {
       std::vector<float> times;
+      if (use_dist) {  // tileqr_dist_factor on every rank; each run's time is the max over ranks
+        int nloc = 0;
+        TQ_TRY(tileqr_dist_local_cols(n, p.nb, &nloc));
+        const int64_t mt = (m + p.nb - 1) / p.nb;
+        double *dA0 = nullptr, *dA = nullptr, *dT = nullptr;
+        const size_t na = std::max<size_t>(1, (size_t)nloc * mt * p.nb * p.nb), nt = std::max<size_t>(1, (size_t)nloc * mt * p.ib * p.nb);
+        if (cudaMalloc(&dA0, na * 8) != cudaSuccess || cudaMalloc(&dA, na * 8) != cudaSuccess ||
+            cudaMalloc(&dT, nt * 8) != cudaSuccess) {
+          cudaGetLastError();
+          cudaFree(dA0); cudaFree(dA); cudaFree(dT);
+          set_error("tileqr_tune: step-2 allocation failed");
+          cleanup();
+          return TILEQR_ERR_ALLOC;
+        }
+        int rc2 = tileqr_dist_fill_uniform(m, n, p.nb, dA0, 3, (tileqr_stream_t)s);
+        std::vector<double> tm(7, 0.0);
+        for (int r = 0; r < 7 && !rc2; ++r) {
+          cudaMemcpyAsync(dA, dA0, na * 8, cudaMemcpyDeviceToDevice, s);
+          cudaEventRecord(e0, s);
+          rc2 = tileqr_dist_factor(m, n, dA, p.nb, p.ib, dT, dinfo, (tileqr_stream_t)s);
+          cudaEventRecord(e1, s);
+          cudaEventSynchronize(e1);
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, e0, e1);
+          tm[r] = ms;
+        }
+        if (!rc2) rc2 = dist_host_collective(tm.data(), 7, 1);
+        cudaFree(dA0); cudaFree(dA); cudaFree(dT);
+        TQ_TRY(rc2);
+        for (int r = 1; r < 7; ++r) times.push_back((float)tm[r]);
+      } else {
       for (int r = 0; r < 7; ++r) {  // 1 warm-up + 6 timed runs
         TQ_TRY(cudaMemcpyAsync(A, A0, (size_t)m * n * sizeof(double), cudaMemcpyDeviceToDevice, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
         TQ_TRY(cudaEventRecord(e0, s) == cudaSuccess ? 0 : TILEQR_ERR_CUDA);
@@ -377,6 +429,7 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
         cudaGetDevice(&dev);
         release_ws(dev, m, n, p.nb, p.ib);
       }
+      }  // single GPU
       std::sort(times.begin(), times.end());
       const double med = 0.5 * (times[2] + times[3]);
       const double flops = (m >= n) ? 2.0 * m * (double)n * n - 2.0 * (double)n * n * n / 3.0
@@ -409,8 +462,8 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
   if (report_json_path) {
     FILE* f = fopen(report_json_path, "w");
     if (f) {
-      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d, \"step1_timing\": \"%s\", \"tie_rel\": %.17g,\n",
-              (long long)M, (long long)N, heuristic, payg, batch, reps, flush ? "flush" : "no_flush", tie_rel);
+      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"heuristic\": %d, \"payg\": %d, \"batch\": %d, \"reps\": %d, \"step1_timing\": \"%s\", \"tie_rel\": %.17g, \"ngpus\": %d,\n",
+              (long long)M, (long long)N, heuristic, payg, batch, reps, flush ? "flush" : "no_flush", tie_rel, P);
       fprintf(f, " \"step1\": %s,\n \"candidates\": %s,\n \"step2\": %s,\n \"best\": {\"nb\": %d, \"ib\": %d, \"gflops\": %.17g}}\n",
               pts_json(samples).c_str(), pts_json(cand).c_str(), step2.c_str(), best.nb, best.ib, best.g);
       fclose(f);

@@ -12,8 +12,9 @@ int launch_update_nb64(bool trans, bool larfb, int IB, int batch, const double* 
   return upd::launch_update_dmma<64>(trans, larfb, IB, batch, V, T, C1, C2, ncols, s);
 }
 int launch_dag_nb64(int IB, const dag::Item* items, int nitems, int* next, int* done, int nsm,
-                     unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io) {
-  return dag::launch_dag_nb<64>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io);
+                     unsigned long long* prof, cudaStream_t s, int* grid_out, const dag::DagIO* io,
+                     int mode) {
+  return dag::launch_dag_nb<64>(IB, items, nitems, next, done, nsm, prof, s, grid_out, io, mode);
 }
 int launch_update_pk_nb64(bool larfb, int IB, int batch, const double* const* Pk, double* const* C1,
                           double* const* C2, cudaStream_t s) {

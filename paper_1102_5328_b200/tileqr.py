@@ -54,8 +54,11 @@ _SIGS = {
     "tileqr_dist_init": ([_i, _i, _p, _i], _i),
     "tileqr_dist_unique_id": ([_p], _i),
     "tileqr_dist_local_cols": ([_i64, _i, _PI], _i),
-    "tileqr_dist_fill_uniform": ([_i64, _i, _p, _u64, _p], _i),
-    "tileqr_dist_factor": ([_i64, _p, _i, _i, _p, _p, _p], _i),
+    "tileqr_dist_fill_uniform": ([_i64, _i64, _i, _p, _u64, _p], _i),
+    "tileqr_dist_factor": ([_i64, _i64, _p, _i, _i, _p, _p, _p], _i),
+    "tileqr_dist_emulate": ([_i, _i64, _i64, _p, _i, _i, _p, _p, _p], _i),
+    "tileqr_dist_plan_items": ([_i64, _i64, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_i64), _i64,
+                                ctypes.POINTER(_i64)], _i),
     "tileqr_dist_plan_level": ([_i64, _i, _i, _i64, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)], _i),
     "tileqr_dist_finalize": ([], None),
     "tileqr_rng_uniform": ([_i64, _i64, _p, _i64, _u64, _u64, _p], _i),
@@ -356,16 +359,46 @@ def dist_local_cols(n: int, nb: int) -> int:
     return out.value
 
 
-def dist_fill_uniform(n: int, nb: int, A_local: torch.Tensor, seed: int, stream=None):
-    _check(_lib.tileqr_dist_fill_uniform(n, nb, A_local.data_ptr(), seed, _stream(stream)),
+def dist_fill_uniform(m: int, n: int, nb: int, A_local: torch.Tensor, seed: int, stream=None):
+    _check(_lib.tileqr_dist_fill_uniform(m, n, nb, A_local.data_ptr(), seed, _stream(stream)),
            "tileqr_dist_fill_uniform")
 
 
-def dist_factor(n: int, A_local: torch.Tensor, nb: int, ib: int, T_local: torch.Tensor,
+def dist_factor(m: int, n: int, A_local: torch.Tensor, nb: int, ib: int, T_local: torch.Tensor,
                 info: torch.Tensor | None = None, stream=None):
-    _check(_lib.tileqr_dist_factor(n, A_local.data_ptr(), nb, ib, T_local.data_ptr(),
+    _check(_lib.tileqr_dist_factor(m, n, A_local.data_ptr(), nb, ib, T_local.data_ptr(),
                                    info.data_ptr() if info is not None else None, _stream(stream)),
            "tileqr_dist_factor")
+
+
+def dist_emulate(nranks: int, m: int, n: int, A_locals, nb: int, ib: int, T_locals,
+                 info: torch.Tensor | None = None, stream=None):
+    """Multi-rank dataflow factorization with `nranks` emulated ranks on this GPU."""
+    pa = (ctypes.c_void_p * nranks)(*[a.data_ptr() if a is not None else None for a in A_locals])
+    pt = (ctypes.c_void_p * nranks)(*[t.data_ptr() if t is not None else None for t in T_locals])
+    _check(_lib.tileqr_dist_emulate(nranks, m, n, ctypes.cast(pa, ctypes.c_void_p), nb, ib,
+                                    ctypes.cast(pt, ctypes.c_void_p),
+                                    info.data_ptr() if info is not None else None, _stream(stream)),
+           "tileqr_dist_emulate")
+
+
+def dist_plan_items(m: int, n: int, nb: int, ib: int, nranks: int, rank: int, workers: int, sub_cols: int):
+    """Host-only dataflow work list of one rank: list of
+    (kind, k, m, n, s, task, deps) in claim order (KINDS_DIST names)."""
+    cnt = _i64()
+    _check(_lib.tileqr_dist_plan_items(m, n, nb, ib, nranks, rank, workers, sub_cols, None, 0,
+                                       ctypes.byref(cnt)), "tileqr_dist_plan_items")
+    out = (_i64 * (10 * max(1, cnt.value)))()
+    _check(_lib.tileqr_dist_plan_items(m, n, nb, ib, nranks, rank, workers, sub_cols, out, 10 * cnt.value,
+                                       ctypes.byref(cnt)), "tileqr_dist_plan_items")
+    rows = []
+    for i in range(cnt.value):
+        r = list(out[10 * i: 10 * i + 10])
+        rows.append((r[0], r[1], r[2], r[3], r[4], r[5], tuple(d for d in r[7:7 + r[6]])))
+    return rows
+
+
+KINDS_DIST = {0: "geqrt", 1: "tsqrt", 2: "larfb", 3: "ssrfb", 6: "arrive", 7: "copy"}
 
 
 def dist_finalize():
