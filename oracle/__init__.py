@@ -5,11 +5,13 @@ and ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import
 this package.  The product package ``paper_1102_5328_b200`` never imports,
 links or executes it; the two share no code (only ``synth_inputs`` seeds both).
 
-Two parts:
+Three parts:
   * ``tileqr_oracle.c`` (plain C loops, fp64) -- the tile kernels GEQRT,
     TSQRT, LARFB, SSRFB, the whole tile factorization and the Q application
     (P:147-187 of /root/reference/PAPER.md; S:58-106 of SPEC.md).  Wrapped
     here with ctypes; built by :func:`build` (gcc -O2 -fopenmp).
+  * the tall-skinny / communication-avoiding variant:
+    TTQRT / TTMQRT and the tree tile QR of DESIGN.md R20 (same C file);
   * ``oracle.tuner`` -- the paper's pruning rules (Properties 1-3,
     Heuristics 0/1/2, nearest-point lookup) and the DAG level schedule by an
     explicit dependency DP, in plain Python.
@@ -57,6 +59,12 @@ def _load():
         lib.oracle_tileqr_factor.restype = i
         lib.oracle_tileqr_apply.argtypes = [c, i64, i64, i64, _dp, i64, _dp, i, i, _dp, i64, i]
         lib.oracle_tileqr_apply.restype = i
+        lib.oracle_ttqrt.argtypes = [i, i, _dp, i, _dp, i, _dp, i]
+        lib.oracle_ttmqrt.argtypes = [c, i, i, _dp, i, _dp, i, _dp, i, _dp, i, i]
+        lib.oracle_tileqr_factor_tree.argtypes = [i64, i64, _dp, i64, i, i, i64, _dp, i]
+        lib.oracle_tileqr_factor_tree.restype = i
+        lib.oracle_tileqr_apply_tree.argtypes = [c, i64, i64, i64, _dp, i64, _dp, i, i, i64, _dp, i64, i]
+        lib.oracle_tileqr_apply_tree.restype = i
         _lib = lib
     return _lib
 
@@ -111,6 +119,58 @@ def ssrfb(v2, t, c1, c2, trans: str = "T"):
     _load().oracle_ssrfb(trans.encode(), nb, ib, _ptr(v2), nb, _ptr(t), ib, _ptr(c1), nb,
                          _ptr(c2), nb, c1.shape[1])
     return c1, c2
+
+
+def ttqrt(r1, r2, ib: int):
+    """TTQRT of [R1; R2] (both upper triangular; strict lower parts untouched).
+    Returns (R1 updated (upper part), R2 with V2 in its upper triangle, T)."""
+    r1, r2 = _f(r1), _f(r2)
+    nb = r1.shape[0]
+    t = np.zeros((ib, nb), order="F")
+    _load().oracle_ttqrt(nb, ib, _ptr(r1), nb, _ptr(r2), nb, _ptr(t), ib)
+    return r1, r2, t
+
+
+def ttmqrt(v2, t, c1, c2, trans: str = "T"):
+    """[C1; C2] <- Q^T [C1; C2] ('T') or Q [C1; C2] ('N') with TTQRT reflectors
+    (the upper triangle of v2)."""
+    v2, t, c1, c2 = _f(v2), _f(t), _f(c1), _f(c2)
+    nb, ib = v2.shape[0], t.shape[0]
+    _load().oracle_ttmqrt(trans.encode(), nb, ib, _ptr(v2), nb, _ptr(t), ib, _ptr(c1), nb,
+                          _ptr(c2), nb, c1.shape[1])
+    return c1, c2
+
+
+def tileqr_factor_tree(a, nb: int, ib: int, bs: int, nthreads: int = 0):
+    """Tile QR with the reduction tree of DESIGN.md R20 (domains of bs tile rows,
+    flat inside, binary tree over the heads).  Returns (A with R and V, T flat
+    array of 2 * t_size doubles: T then T2, info)."""
+    a = _f(a)
+    m, n = a.shape
+    t = np.zeros(max(1, 2 * t_size(m, n, nb, ib)), dtype=np.float64)
+    info = _load().oracle_tileqr_factor_tree(m, n, _ptr(a), max(1, m), nb, ib, bs, t.ctypes.data_as(_dp),
+                                             nthreads)
+    if info < 0:
+        raise MemoryError("oracle allocation failed")
+    return a, t, info
+
+
+def tileqr_apply_tree(trans: str, a, t, nb: int, ib: int, bs: int, b, nthreads: int = 0):
+    """B <- Q^T B ('T') or Q B ('N') for the Q of a tileqr_factor_tree output."""
+    a = _f(a)
+    b = _f(b)
+    m, k = a.shape
+    t = np.ascontiguousarray(t, dtype=np.float64)
+    rc = _load().oracle_tileqr_apply_tree(trans.encode(), m, b.shape[1], k, _ptr(a), max(1, m),
+                                          t.ctypes.data_as(_dp), nb, ib, bs, _ptr(b), max(1, m), nthreads)
+    if rc < 0:
+        raise MemoryError("oracle allocation failed")
+    return b
+
+
+def tree_heads(mt: int, k: int, bs: int):
+    """Domain heads of panel k (R20)."""
+    return [max(d * bs, k) for d in range(k // bs, -(-mt // bs))]
 
 
 def t_size(m: int, n: int, nb: int, ib: int) -> int:
