@@ -124,25 +124,39 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_sample(m, n, nb, ib, seed, target_gflop=150.0):
-    """Time the CPU oracle (as it stands) on the first kmax panels of the same
-    workload: useful flops = flops(m, n) - flops of the untouched trailing part."""
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_oracle_sample(m, n, nb, ib, seed, target_gflop=150.0, threads=None, full=False):
+    """Time the CPU oracle (as it stands) on the workload: the whole
+    factorization (full=True) or its first kmax panels (useful flops =
+    flops(m, n) - flops of the untouched trailing part)."""
     import numpy as np  # noqa: F401
     import oracle
     import synth_inputs as si
-    cores = len(os.sched_getaffinity(0))
-    kmax = max(1, int(target_gflop * 1e9 / (4.0 * m * n * nb)))
-    kmax = min(kmax, -(-min(m, n) // nb))
+    cores = threads or len(os.sched_getaffinity(0))
+    npan = -(-min(m, n) // nb)
+    kmax = npan if full else min(npan, max(1, int(target_gflop * 1e9 / (4.0 * m * n * nb))))
     a = si.uniform(m, n, seed)
     t0 = time.perf_counter()
-    oracle.tileqr_factor(a, nb, ib, nthreads=cores, kmax=kmax)
+    oracle.tileqr_factor(a, nb, ib, nthreads=cores, kmax=0 if kmax >= npan else kmax)
     dt = time.perf_counter() - t0
     done = kmax * nb
     fl = qr_flops(m, n) - (qr_flops(m - done, n - done) if done < min(m, n) else 0.0)
+    what = (f"the whole {m}x{n} NB={nb} IB={ib} factorization" if kmax >= npan else
+            f"first {kmax} of {npan} panels (k < {kmax}) of the {m}x{n} NB={nb} IB={ib} factorization")
     return {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {kmax} of {-(-min(m, n) // nb)} panels (k < {kmax}) of the {m}x{n} "
-                      f"NB={nb} IB={ib} factorization, oracle/tileqr_oracle.c with {cores} OpenMP "
-                      f"threads; {fl / 1e9:.1f} useful GFLOP in {dt:.2f} s"}
+            "cpu": _cpu_model(),
+            "sample": f"{what}, oracle/tileqr_oracle.c with {cores} OpenMP thread(s); "
+                      f"{fl / 1e9:.1f} useful GFLOP in {dt:.2f} s"}
 
 
 def run_reference(args, rank, world):
@@ -335,7 +349,7 @@ def run_tileqr(args, rank, world, local_rank):
         hA.copy_(A0)
         hR = torch.empty_like(hA, pin_memory=True)
         hT = torch.empty(T.numel(), dtype=torch.float64, pin_memory=True)
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = max(1, args.steps)
 
         def step_e2e():
             tq.factor_host(hA, m, n, nb, ib, hR=hR, hT=hT, info=info)
@@ -355,7 +369,11 @@ def run_tileqr(args, rank, world, local_rank):
 
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_oracle_sample(m, n, nb, ib, seed)
+        # the whole factorization on every host core (about 30 s at 10000^2 on 16 cores), plus a
+        # 1-thread sample of its first panel
+        cpu = cpu_oracle_sample(m, n, nb, ib, seed, full=True)
+        one = cpu_oracle_sample(m, n, nb, ib, seed, target_gflop=1.0, threads=1)
+        cpu["one_thread"] = {"value": one["value"], "unit": one["unit"], "sample": one["sample"]}
 
     line = {"metric": "tile-QR FP64 GFLOP/s", "value": round(value, 2), "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),

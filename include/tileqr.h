@@ -321,6 +321,46 @@ int tileqr_dist_emulate(int nranks, int64_t M, int64_t N, double* const* h_A_loc
                         double* const* h_T_local, int* d_info, tileqr_stream_t stream);
 
 /* ------------------------------------------------------------------------
+ * Tall-skinny / communication-avoiding variant (
+ * PAPER.md:840-850): the flat TSQRT chain of every panel is replaced by a
+ * reduction tree -- tile rows in domains of BS consecutive rows [d*BS,
+ * (d+1)*BS); per panel k each domain's first row >= k (its head) is factored
+ * by GEQRT and joined by the domain's other rows through the flat TSQRT
+ * chain; the heads are merged pairwise along a binary tree (distance 1, 2,
+ * 4, ...) by TTQRT ("triangle on triangle"), applied to the trailing tiles
+ * by TTMQRT (R20).  BS >= ceil(M/NB) is the flat tree.  Runs on the
+ * persistent dataflow kernel: (NB, IB) in its set (NB % 32 == 0, NB <= 256,
+ * IB in {8,16,24,32}).
+ *   tileqr_factor_tree: as tileqr_factor; output A holds R, the GEQRT V of
+ *     every head strictly below its diagonal, TSQRT V2 in full tiles, and the
+ *     TTQRT V2 of a merged head in the upper triangle (diagonal included) of
+ *     its tile; T holds tileqr_t_size_tree() = 2*MT*NT*IB*NB doubles: the
+ *     GEQRT / TSQRT factors (tileqr_factor layout), then the TTQRT factors
+ *     T2 (same offsets, tile (b,k) for the merged head b).
+ *     Errors: -1 M, -2 N, -3 A, -4 lda, -5 NB/IB, -6 (NB, IB) outside the
+ *     dataflow set, -7 BS < 1, -8 T.
+ *   tileqr_apply_qt_tree: B <- Q^T B / Q B for that factorization (same NB,
+ *     IB, BS): the operations replayed in order ('T') or backwards ('N').
+ *     Errors: -1 trans, -2 M, -3 NRHS, -4 K, -5 A, -6 lda, -7 T, -8 NB/IB,
+ *     -10 BS, -11 B, -12 ldb.
+ *   tileqr_ttqrt_batched: QR of [R[i]; A2[i]], both upper triangular (LAPACK
+ *     dtpqrt with L = NB): R's upper triangle updated, V2 in A2's upper
+ *     triangle, T[i] (IB x NB); the strict lower parts of R[i] and A2[i] are
+ *     neither read nor written.  Errors: -1 (NB, IB) unsupported, -3 batch,
+ *     -4..-6 NULL arrays.
+ * ------------------------------------------------------------------------ */
+int tileqr_factor_tree(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, int64_t BS, double* T,
+                       int* d_info, tileqr_stream_t stream);
+int tileqr_t_size_tree(int64_t M, int64_t N, int NB, int IB, size_t* n_doubles);
+int tileqr_apply_qt_tree(char trans, int64_t M, int64_t NRHS, int64_t K, const double* A, int64_t lda,
+                         const double* T, int NB, int IB, int64_t BS, double* B, int64_t ldb,
+                         tileqr_stream_t stream);
+int tileqr_ttqrt_batched(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
+                         tileqr_stream_t stream);
+/* Release the tree variant's cached workspaces. */
+void tileqr_tree_finalize(void);
+
+/* ------------------------------------------------------------------------
  * Utilities.
  * ------------------------------------------------------------------------ */
 /* Synthetic input generator (same counter-based

@@ -19,7 +19,7 @@ BUILD = os.path.join(HERE, "_build" + (f"_{VARIANT}" if VARIANT else ""))
 LIB = os.path.join(HERE, "libtileqr" + (f"_{VARIANT}" if VARIANT else "") + ".so")
 EXTRA = (["-DTILEQR_PANEL_PROF"] if VARIANT == "prof" else []) + os.environ.get("TILEQR_EXTRA_FLAGS", "").split()
 SOURCES = ["kernels_layout.cu", "kernels_panel.cu", "kernels_panel_fast.cu", "kernels_update.cu",
-           "api.cu", "tune.cu", "dist.cu", "table.cu", "dist_dag.cu"] + [f"update_nb{nb}.cu" for nb in (32, 64, 96, 128, 160, 192, 224, 256)]
+           "api.cu", "tune.cu", "dist.cu", "table.cu", "dist_dag.cu", "tree.cu"] + [f"update_nb{nb}.cu" for nb in (32, 64, 96, 128, 160, 192, 224, 256)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

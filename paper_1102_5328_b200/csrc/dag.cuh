@@ -294,7 +294,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         }
         if (prof) prof[3 * (size_t)cur + 1] = globaltimer();
         if constexpr (V2) {
-          if (it.kind == kLarfb || it.kind == kSsrfb) {
+          if (it.kind == kLarfb || it.kind == kSsrfb || (MODE == kModeTree && it.kind == kTtmqr)) {
             const int na = v2::active_warps<NB, MB, W>(it.col0, it.aux[0]);
             if (na > 0) v2::ring_start<NB, KW, S>(it.pk, smem, full, empty, na);
           }
@@ -323,10 +323,11 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       if (p == PF) {
         cp_async_wait<0>();
         const Item& n = s_desc[slot ^ 1];
-        if (n.kind == kSsrfb || n.kind == kLarfb) {
+        if (n.kind == kSsrfb || n.kind == kLarfb || (MODE == kModeTree && n.kind == kTtmqr)) {
           constexpr uint32_t tb = NB * NB * sizeof(double);
-          prefetch_l2(n.p[n.kind == kSsrfb ? 3 : 2], tb);
-          if (n.kind == kSsrfb) prefetch_l2(n.p[2], tb);
+          const bool two = n.kind != kLarfb;
+          prefetch_l2(n.p[two ? 3 : 2], tb);
+          if (two) prefetch_l2(n.p[2], tb);
           if constexpr (V2) prefetch_l2(n.pk, (uint32_t)v2::Pk<NB, (NB % KW == 0 ? KW : 8)>::TOTAL * 8);
         }
       }
@@ -359,6 +360,19 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         break;
       case kCopy:
         if constexpr (MODE == kModeDist) copy_body(it.p[0], it.p[1], it.aux[0]);
+        break;
+      case kTtqrt:  // tree variant: merge R_b (upper triangle of tile p[1]) into R_a
+        if constexpr (MODE == kModeTree)
+          pf::panel_fast_body<true, NB, W, KW, true>(it.p[0], it.p[1], it.p[2],
+                                                     reinterpret_cast<unsigned char*>(smem), V2 ? it.pk : nullptr,
+                                                     it.col0 & 0xffff, it.col0 >> 16);
+        break;
+      case kTtmqr:  // tree variant: TTMQRT column slab
+        if constexpr (MODE == kModeTree && V2) {
+          if (it.aux[0] <= it.col0) break;
+          v2::update_v2_body<NB, KW, MB, false, W, S, decltype(hook), true>(it.pk, smem, full, empty, it.p[2],
+                                                                            it.p[3], it.col0, hook, it.aux[0]);
+        }
         break;
       default:  // SSRFB: columns as LARFB
         if (it.aux[0] <= it.col0) break;
@@ -399,7 +413,8 @@ template <int NB, int KW>
 int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, int nsm,
                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io, int mode) {
   auto kern = mode == kModeIO ? dag_kernel<NB, KW, kModeIO>
-            : mode == kModeDist ? dag_kernel<NB, KW, kModeDist> : dag_kernel<NB, KW, kModePlain>;
+            : mode == kModeDist ? dag_kernel<NB, KW, kModeDist>
+            : mode == kModeTree ? dag_kernel<NB, KW, kModeTree> : dag_kernel<NB, KW, kModePlain>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));

@@ -19,12 +19,14 @@ __host__ __device__ constexpr int dag_ctas_per_sm(int NB) { return NB <= 128 ? 2
 
 enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3, kLoad = 4, kStore = 5,
             kArrive = 6,  // host-only pseudo task: completed by a copy engine / a peer, not by a CTA
-            kCopy = 7 };  // multi-rank dataflow: push a packed reflector tile to a peer rank
+            kCopy = 7,    // multi-rank dataflow: push a packed reflector tile to a peer rank
+            kTtqrt = 8,   // tree variant (f3): TTQRT sub-task (p: R_a, R_b, T2)
+            kTtmqr = 9 }; // tree variant: TTMQRT column slab (p: -, -, C1, C2)
 
 // Kernel instantiations of the dataflow kernel (dag.cuh): the device-only
 // factorization, the host-buffer pipeline (LOAD / STORE items) and the
 // multi-rank dataflow factorization (COPY items, system-scope signals).
-enum Mode { kModePlain = 0, kModeIO = 1, kModeDist = 2 };
+enum Mode { kModePlain = 0, kModeIO = 1, kModeDist = 2, kModeTree = 3 };
 
 // One work item: a whole panel task, or a column slab of an update task.
 struct Item {

@@ -14,18 +14,18 @@ __device__ unsigned long long g_panel_prof[16];  // phase cycles; filled only wi
 namespace {
 using pf::FastSmem;
 
-template <bool TS, int NB, int kWarps, int IB>
+template <bool TS, int NB, int kWarps, int IB, bool TT = false>
 __global__ void __launch_bounds__(kWarps * 32, 1)
 panel_fast_kernel(double* const* Rp, double* const* Bp, double* const* Tp, double* const* Pk) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  pf::panel_fast_body<TS, NB, kWarps, IB>(Rp[blockIdx.x], TS ? Bp[blockIdx.x] : nullptr, Tp[blockIdx.x],
-                                          smem_raw, Pk ? Pk[blockIdx.x] : nullptr);
+  pf::panel_fast_body<TS, NB, kWarps, IB, TT>(Rp[blockIdx.x], TS ? Bp[blockIdx.x] : nullptr, Tp[blockIdx.x],
+                                              smem_raw, Pk ? Pk[blockIdx.x] : nullptr);
 }
 
-template <bool TS, int NB, int NW, int IB>
+template <bool TS, int NB, int NW, int IB, bool TT = false>
 int launch_fast_i(int batch, double* const* R, double* const* B, double* const* T, cudaStream_t s,
                   double* const* Pk) {
-  auto kern = panel_fast_kernel<TS, NB, NW, IB>;
+  auto kern = panel_fast_kernel<TS, NB, NW, IB, TT>;
   const size_t bytes = sizeof(FastSmem<NB, NW>);
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   kern<<<batch, NW * 32, bytes, s>>>(R, B, T, Pk);
@@ -33,16 +33,16 @@ int launch_fast_i(int batch, double* const* R, double* const* B, double* const* 
   return 0;
 }
 
-template <bool TS, int NB, int NW>
+template <bool TS, int NB, int NW, bool TT = false>
 int launch_fast_w(int IB, int batch, double* const* R, double* const* B, double* const* T,
                   cudaStream_t s, double* const* Pk) {
   switch (IB) {
-    case 8: return launch_fast_i<TS, NB, NW, 8>(batch, R, B, T, s, Pk);
-    case 16: return launch_fast_i<TS, NB, NW, 16>(batch, R, B, T, s, Pk);
+    case 8: return launch_fast_i<TS, NB, NW, 8, TT>(batch, R, B, T, s, Pk);
+    case 16: return launch_fast_i<TS, NB, NW, 16, TT>(batch, R, B, T, s, Pk);
     case 24:
-      if constexpr (NB % 24 == 0) return launch_fast_i<TS, NB, NW, 24>(batch, R, B, T, s, Pk);
+      if constexpr (NB % 24 == 0) return launch_fast_i<TS, NB, NW, 24, TT>(batch, R, B, T, s, Pk);
       return -1;
-    case 32: return launch_fast_i<TS, NB, NW, 32>(batch, R, B, T, s, Pk);
+    case 32: return launch_fast_i<TS, NB, NW, 32, TT>(batch, R, B, T, s, Pk);
     default: return -1;
   }
 }
@@ -60,25 +60,25 @@ int panel_warps(int NB) {
   return v ? v : dag::dag_warps(NB);
 }
 
-template <bool TS, int NB>
+template <bool TS, int NB, bool TT = false>
 int launch_fast_t(int IB, int batch, double* const* R, double* const* B, double* const* T,
                   cudaStream_t s, double* const* Pk) {
-  return panel_warps(NB) == 8 ? launch_fast_w<TS, NB, 8>(IB, batch, R, B, T, s, Pk)
-                              : launch_fast_w<TS, NB, 4>(IB, batch, R, B, T, s, Pk);
+  return panel_warps(NB) == 8 ? launch_fast_w<TS, NB, 8, TT>(IB, batch, R, B, T, s, Pk)
+                              : launch_fast_w<TS, NB, 4, TT>(IB, batch, R, B, T, s, Pk);
 }
 
-template <bool TS>
+template <bool TS, bool TT = false>
 int launch_fast(int NB, int IB, int batch, double* const* R, double* const* B, double* const* T,
                 cudaStream_t s, double* const* Pk) {
   switch (NB) {
-    case 32: return launch_fast_t<TS, 32>(IB, batch, R, B, T, s, Pk);
-    case 64: return launch_fast_t<TS, 64>(IB, batch, R, B, T, s, Pk);
-    case 96: return launch_fast_t<TS, 96>(IB, batch, R, B, T, s, Pk);
-    case 128: return launch_fast_t<TS, 128>(IB, batch, R, B, T, s, Pk);
-    case 160: return launch_fast_t<TS, 160>(IB, batch, R, B, T, s, Pk);
-    case 192: return launch_fast_t<TS, 192>(IB, batch, R, B, T, s, Pk);
-    case 224: return launch_fast_t<TS, 224>(IB, batch, R, B, T, s, Pk);
-    case 256: return launch_fast_t<TS, 256>(IB, batch, R, B, T, s, Pk);
+    case 32: return launch_fast_t<TS, 32, TT>(IB, batch, R, B, T, s, Pk);
+    case 64: return launch_fast_t<TS, 64, TT>(IB, batch, R, B, T, s, Pk);
+    case 96: return launch_fast_t<TS, 96, TT>(IB, batch, R, B, T, s, Pk);
+    case 128: return launch_fast_t<TS, 128, TT>(IB, batch, R, B, T, s, Pk);
+    case 160: return launch_fast_t<TS, 160, TT>(IB, batch, R, B, T, s, Pk);
+    case 192: return launch_fast_t<TS, 192, TT>(IB, batch, R, B, T, s, Pk);
+    case 224: return launch_fast_t<TS, 224, TT>(IB, batch, R, B, T, s, Pk);
+    case 256: return launch_fast_t<TS, 256, TT>(IB, batch, R, B, T, s, Pk);
     default: return -1;
   }
 }
@@ -106,6 +106,12 @@ int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const
 int launch_tsqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
                       double* const* T, cudaStream_t s, double* const* Pk) {
   return launch_fast<true>(NB, IB, batch, R, A2, T, s, Pk);
+}
+
+// TTQRT (tree variant, f3): the TS body with B upper triangular
+int launch_ttqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
+                      double* const* T, cudaStream_t s, double* const* Pk) {
+  return launch_fast<true, true>(NB, IB, batch, R, A2, T, s, Pk);
 }
 
 }  // namespace tileqr

@@ -63,11 +63,19 @@ struct FastSmem {
 // Inner panels c0 = cbeg, cbeg+IB, ... < cend (the whole tile by default; the
 // DAG kernel runs a TSQRT / GEQRT as several sub-tasks of consecutive inner
 // panels, every state between them lives in global memory).
-template <bool TS, int NB, int kWarps, int IB>
+//
+// TT (with TS): the TTQRT of the tree variant -- B is upper
+// triangular: reflector j uses rows 0..j of column j of B, V2 is written to
+// B's upper triangle (diagonal included) only, and rows of B below a
+// column's diagonal are never read or written (they hold the GEQRT V of that
+// tile, read by other kernels).  Its zeros enter the register panel, so the
+// step loop, the Gram product and the packed copy are the TSQRT ones.
+template <bool TS, int NB, int kWarps, int IB, bool TT = false>
 __device__ __forceinline__ void panel_fast_body(double* const R, double* const Bx, double* const Tg,
                                                 unsigned char* smem_raw, double* const Vpk = nullptr,
                                                 int cbeg = 0, int cend = NB) {
   static_assert(IB % 8 == 0 && IB <= 32 && NB % IB == 0, "fast panel geometry");
+  static_assert(TS || !TT, "TT is a TS variant");
   constexpr int TR = IB / kWarps > 0 ? IB / kWarps : 1;  // GEQRT: top rows per warp
   constexpr int kThreads = kWarps * 32;
   constexpr int RW = NB / kWarps;  // rows per warp in the factorization
@@ -119,7 +127,8 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
           // concurrent TSQRT sub-task may be rewriting -- never read them (a
           // stale line could even land in the L1 another CTA of this SM reads
           // after its acquire); their operand entries are 0 anyway
-          v[u] = (idx < NB * IB && (TS || idx % NB >= c0)) ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+          v[u] = (idx < NB * IB && (TS || idx % NB >= c0) && (!TT || idx % NB <= c0 + idx / NB))
+                     ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
         }
         double rv[UR];
         if (TS && idx0 == tid) {
@@ -149,7 +158,8 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int idx = idx0 + u * kThreads;
-          v[u] = (idx < NB * IB && (TS || idx % NB >= c0)) ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+          v[u] = (idx < NB * IB && (TS || idx % NB >= c0) && (!TT || idx % NB <= c0 + idx / NB))
+                     ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -311,7 +321,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       double* p = &S.Vs[vsw(r, c, LDV)];
       const double v = *p;
       if (TS) {
-        B[r + (size_t)(c0 + c) * NB] = v;  // V2
+        if (!TT || r <= c0 + c) B[r + (size_t)(c0 + c) * NB] = v;  // V2 (TT: the upper triangle only)
       } else {
         // GEQRT: V strictly below the diagonal (registers), R on/above it (Rout)
         if (r > c0 + c) B[r + (size_t)(c0 + c) * NB] = v;
@@ -441,8 +451,11 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         // (a concurrent TSQRT sub-task of the DAG kernel may own them)
         double acc[RB][2];
 #pragma unroll
+        // TT: V2 of the applied panels is zero below row rhi: rows >= rhi are
+        // neither needed nor touched (below a column's diagonal they hold V)
+        const int rhi = TT ? cbeg + (j1 + 1) * IB : NB;
         for (int rb = 0; rb < RB; ++rb) {
-          if (!TS && 8 * rb + 7 < rlo) { acc[rb][0] = acc[rb][1] = 0.0; continue; }
+          if ((!TS && 8 * rb + 7 < rlo) || (TT && 8 * rb >= rhi)) { acc[rb][0] = acc[rb][1] = 0.0; continue; }
           const double2 v = __ldcg(reinterpret_cast<const double2*>(B + 8 * rb + 2 * a + (size_t)cc * NB));
           acc[rb][0] = v.x;
           acc[rb][1] = v.y;
@@ -466,6 +479,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
           for (int rb = 0; rb < RB; ++rb) {
             if (!TS && 8 * rb + 7 < pc0) continue;
+            if (TT && 8 * rb >= pc0 + IB) continue;
 #pragma unroll
             for (int nb = 0; nb < 4; ++nb)
               if (nb < nbi) {
@@ -525,6 +539,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
             for (int rb = 0; rb < RB; ++rb) {
               if (!TS && 8 * rb + 7 < pc0) continue;
+              if (TT && 8 * rb >= pc0 + IB) continue;
               dmma(acc[rb][0], acc[rb][1], af, S.Vs[vsw(8 * rb + g, voff + k4 + a, LDV)]);
             }
           }
@@ -532,7 +547,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         }
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
-          if (!TS && 8 * rb + 7 < rlo) continue;
+          if ((!TS && 8 * rb + 7 < rlo) || (TT && 8 * rb >= rhi)) continue;
           *reinterpret_cast<double2*>(B + 8 * rb + 2 * a + (size_t)cc * NB) = make_double2(acc[rb][0], acc[rb][1]);
         }
         __syncwarp();

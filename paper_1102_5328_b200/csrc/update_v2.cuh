@@ -191,7 +191,11 @@ struct NoHook {
 // claims its next work item there, overlapping the claim with the tail).
 // Ring of S stages (ring_start issued by thread 0 before the CTA barrier);
 // gpk = the packed tile in global memory (refills).
-template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook>
+//
+// TT: the TTMQRT of the tree variant: V2 of panel p is zero
+// below row c0 + IB (the packed tile of a TTQRT holds those zeros), so steps A
+// and C skip those row blocks -- half the flops of the SSRFB form.
+template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook, bool TT = false>
 __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, double* spk, uint64_t* full,
                                                uint64_t* empty, double* __restrict__ C1, double* __restrict__ C2,
                                                int col0, Hook hook = Hook(), int cend = NB) {
@@ -268,6 +272,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb) {
       if (rb < rb0) continue;
+      if (TT && 8 * rb >= c0 + IB) continue;
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -351,6 +356,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
 #pragma unroll
         for (int rb = 0; rb < RB; ++rb) {
           if (rb < rb0) continue;
+          if (TT && 8 * rb >= c0 + IB) continue;
           const double bf = pc[8 * rb * P::GW];
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], w[mb][nb][s], bf);

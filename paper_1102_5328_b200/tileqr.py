@@ -70,6 +70,11 @@ _SIGS = {
     "tileqr_kernel_trace": ([_i64, _i64, _i, _i, _i64, _PD, _PD, _PI, ctypes.POINTER(_i64),
                              ctypes.POINTER(_i64), ctypes.POINTER(_i64)], _i),
     "tileqr_finalize": ([], None),
+    "tileqr_factor_tree": ([_i64, _i64, _p, _i64, _i, _i, _i64, _p, _p, _p], _i),
+    "tileqr_t_size_tree": ([_i64, _i64, _i, _i, ctypes.POINTER(_sz)], _i),
+    "tileqr_apply_qt_tree": ([_c, _i64, _i64, _i64, _p, _i64, _p, _i, _i, _i64, _p, _i64, _p], _i),
+    "tileqr_ttqrt_batched": ([_i, _i, _i, _p, _p, _p, _p], _i),
+    "tileqr_tree_finalize": ([], None),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -337,6 +342,43 @@ def kernel_trace(m: int, n: int, nb: int, ib: int, max_recs: int = 1 << 16):
 
 def finalize():
     _lib.tileqr_finalize()
+    _lib.tileqr_tree_finalize()
+
+
+# ---------------------------------------------------------------------------
+# tall-skinny / communication-avoiding variant (reduction tree)
+# ---------------------------------------------------------------------------
+def t_size_tree(m: int, n: int, nb: int, ib: int) -> int:
+    out = _sz()
+    _check(_lib.tileqr_t_size_tree(m, n, nb, ib, ctypes.byref(out)), "tileqr_t_size_tree")
+    return out.value
+
+
+def factor_tree(A: torch.Tensor, m: int, n: int, nb: int, ib: int, bs: int, T: torch.Tensor | None = None,
+                info: torch.Tensor | None = None, lda: int | None = None, stream=None):
+    """tileqr_factor_tree on the column-major m x n matrix stored in A (in place);
+    bs = domain size in tile rows.  Returns (T (T then T2), info)."""
+    assert A.dtype == torch.float64 and A.is_cuda and A.is_contiguous()
+    if T is None:
+        T = torch.empty(max(1, t_size_tree(m, n, nb, ib)), dtype=torch.float64, device=A.device)
+    if info is None:
+        info = torch.zeros(1, dtype=torch.int32, device=A.device)
+    _check(_lib.tileqr_factor_tree(m, n, A.data_ptr(), lda if lda is not None else max(1, m), nb, ib, bs,
+                                   T.data_ptr(), info.data_ptr(), _stream(stream)), "tileqr_factor_tree")
+    return T, info
+
+
+def apply_qt_tree(trans: str, A: torch.Tensor, m: int, k: int, T: torch.Tensor, nb: int, ib: int, bs: int,
+                  B: torch.Tensor, nrhs: int, lda: int | None = None, ldb: int | None = None, stream=None):
+    _check(_lib.tileqr_apply_qt_tree(trans.encode(), m, nrhs, k, A.data_ptr(), lda if lda is not None else max(1, m),
+                                     T.data_ptr(), nb, ib, bs, B.data_ptr(), ldb if ldb is not None else max(1, m),
+                                     _stream(stream)), "tileqr_apply_qt_tree")
+    return B
+
+
+def ttqrt_batched(nb: int, ib: int, R_ptrs, A2_ptrs, T_ptrs, stream=None):
+    _check(_lib.tileqr_ttqrt_batched(nb, ib, R_ptrs.numel(), R_ptrs.data_ptr(), A2_ptrs.data_ptr(),
+                                     T_ptrs.data_ptr(), _stream(stream)), "tileqr_ttqrt_batched")
 
 
 # ---------------------------------------------------------------------------
