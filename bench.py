@@ -43,6 +43,9 @@ WORKLOADS = {
     2: dict(name="qr2048 (BASELINE configs[2])", M=2048, N=2048, seed=3),
     3: dict(name="qr10000_tuned (BASELINE configs[3])", M=10000, N=10000, seed=4),
     4: dict(name="qr40000_dist (BASELINE configs[4])", M=40000, N=40000, seed=5),
+    # not a BASELINE config: the tall-skinny case of SURVEY §8(f) f3 (reduction tree, BS tuned)
+    5: dict(name="tall_skinny_131072x256_tree (SURVEY f3; not a BASELINE config)", M=131072, N=256, seed=6,
+            nb=128, ib=16, tree=True),
 }
 TUNED = os.path.join(ROOT, "paper_1102_5328_b200", "tuned_table.json")
 
@@ -287,10 +290,14 @@ def run_tileqr(args, rank, world, local_rank):
     if args.nb:
         nb, ib, src = args.nb, args.ib, "command line"
     elif "nb" in wl:
-        nb, ib, src = wl["nb"], wl["ib"], "BASELINE configs[0]"
+        nb, ib, src = wl["nb"], wl["ib"], ("fixed for the f3 tall-skinny line" if wl.get("tree")
+                                           else "BASELINE configs[0]")
     else:
         nb, ib, src = tuned_pair(n, world)
     plan = tq.factor_plan(m, n, nb, ib)
+    tree_bs = None
+    if wl.get("tree"):  # domain size: tileqr_tune_tree ("p domains"), before any timing
+        tree_bs, _ = tq.tune_tree(m, n, nb, ib)
 
     A0 = torch.empty((n, m), dtype=torch.float64, device=dev)   # column-major m x n
     tq.rng_uniform(A0, m, n, seed=seed)
@@ -299,9 +306,18 @@ def run_tileqr(args, rank, world, local_rank):
     info = torch.zeros(1, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
+    if tree_bs:
+        T = torch.empty(max(1, tq.t_size_tree(m, n, nb, ib)), dtype=torch.float64, device=dev)
+
+    def factor_once(buf):
+        if tree_bs:
+            tq.factor_tree(buf, m, n, nb, ib, tree_bs, T=T, info=info)
+        else:
+            tq.factor(buf, m, n, nb, ib, T=T, info=info)
+
     def step():
         A.copy_(A0)
-        tq.factor(A, m, n, nb, ib, T=T, info=info)
+        factor_once(A)
 
     tq.set_kernel_timing(False)
     for _ in range(args.warmup):
@@ -323,7 +339,7 @@ def run_tileqr(args, rank, world, local_rank):
         e0.record(stream)
         for i in range(args.steps):
             if staged:
-                tq.factor(bufs[i], m, n, nb, ib, T=T, info=info)
+                factor_once(bufs[i])
             else:
                 step()
         e1.record(stream)
@@ -334,7 +350,16 @@ def run_tileqr(args, rank, world, local_rank):
     value = flops / (ms * 1e-3) / 1e9
 
     sched = tq.factor_schedule(nb, ib)
-    if sched == "dag":
+    if tree_bs:
+        sched = f"dag (reduction tree, BS={tree_bs})"
+        ach = qr_flops(m, n) / (ms * 1e-3) / 1e12
+        roofline = {"kernel": "dag_kernel (tree mode) + layout kernels: the whole step", "bound": "tensor",
+                    "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None, "peak_source": FP64_PEAK_SRC,
+                    "measured": "useful flops / the step's CUDA-event time (an upper bound on the kernel's "
+                                "duration)"}
+        kinds = None
+    elif sched == "dag":
         roofline, kinds = measure_dag(tq, m, n, nb, ib, step, ms)
     else:
         roofline, kinds = measure_levels(tq, m, n, nb, ib, step, ms)
@@ -344,7 +369,7 @@ def run_tileqr(args, rank, world, local_rank):
     # overlapped with the factorization inside the call; every step moves the
     # whole input in and the whole result out inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not tree_bs:
         hA = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         hA.copy_(A0)
         hR = torch.empty_like(hA, pin_memory=True)
@@ -368,7 +393,18 @@ def run_tileqr(args, rank, world, local_rank):
                "api": "tileqr_factor_host (copies overlapped with the dataflow kernel)"}
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and tree_bs:
+        import oracle
+        import synth_inputs as si
+        a_h = si.uniform(m, n, seed)
+        cores = len(os.sched_getaffinity(0))
+        t0 = time.perf_counter()
+        oracle.tileqr_factor_tree(a_h, nb, ib, tree_bs, nthreads=cores)
+        dt = time.perf_counter() - t0
+        cpu = {"value": qr_flops(m, n) / dt / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+               "cpu": _cpu_model(), "sample": f"the whole {m}x{n} tree factorization (BS={tree_bs}), "
+                                             f"oracle_tileqr_factor_tree with {cores} threads, {dt:.2f} s"}
+    elif not args.no_cpu_baseline:
         # the whole factorization on every host core (about 30 s at 10000^2 on 16 cores), plus a
         # 1-thread sample of its first panel
         cpu = cpu_oracle_sample(m, n, nb, ib, seed, full=True)
@@ -380,6 +416,7 @@ def run_tileqr(args, rank, world, local_rank):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic: i.i.d. uniform(-0.5,0.5), splitmix64 counter generator, seed {seed}",
             "config": {"workload": wl["name"], "M": m, "N": n, "NB": nb, "IB": ib, "nb_ib_source": src,
+                       "BS": tree_bs,
                        "parallelism": "single GPU", "levels": plan["levels"], "schedule": sched,
                        "l2": (f"input {m * n * 8 / 1e6:.0f} MB > 126 MB L2; " +
                               ("each timed step factors its own pristine copy of A, staged in HBM before "

@@ -357,6 +357,14 @@ int tileqr_apply_qt_tree(char trans, int64_t M, int64_t NRHS, int64_t K, const d
                          tileqr_stream_t stream);
 int tileqr_ttqrt_batched(int NB, int IB, int batch, double* const* R, double* const* A2, double* const* T,
                          tileqr_stream_t stream);
+/* The domain size BS as a tunable ("p domains"): times
+ * tileqr_factor_tree on a seeded M x N matrix for BS = 1, 2, 4, ... and the
+ * flat tree (BS = MT), 1 warm-up + 6 timed runs each, and returns the BS with
+ * the smallest median in *h_BS (its median ms in *h_ms, nullable); the
+ * report (nullable path) lists every median.  Synchronizes the device.
+ * Errors: -1 M, -2 N, -3 (NB, IB) outside the dataflow set, -5 h_BS NULL. */
+int tileqr_tune_tree(int64_t M, int64_t N, int NB, int IB, int64_t* h_BS, double* h_ms,
+                     const char* report_json_path);
 /* Release the tree variant's cached workspaces. */
 void tileqr_tree_finalize(void);
 

@@ -147,6 +147,8 @@ struct DagList {
   std::vector<unsigned char> item_kind;     // host copies for the diagnostics
   std::vector<int> item_info;               // per item: kind, k, m, n, sub-task / slab column
   std::vector<int> item_level;
+  std::vector<std::pair<int, int>> st_order;  // STORE groups (column, group) in claim order
+  int io_tiles = 8;
   ~DagList() {
     cudaFree(d_items);
     cudaFree(d_ctr);
@@ -288,7 +290,14 @@ static int build_dag(FactorWS* ws, bool io) {
   // engine lands the input column block by column block: contiguous copies
   // run at the link's rate, strided row blocks of NB doubles measured ~30 %
   // slower in total)
-  const int64_t ntask = ntask0 + (io ? 3 * NT : 0);
+  int kIoTiles = 8;  // tiles per LOAD / STORE item
+  if (const char* e = getenv("TILEQR_DAG_IOTILES")) kIoTiles = std::max(1, atoi(e));  // diagnostics
+  const int nld = (int)((MT + kIoTiles - 1) / kIoTiles), nst = nld;
+  // STORE tasks per (tile column n, group g of kIoTiles tile rows): a group
+  // is copied back as soon as ITS tiles are final -- the R rows of a column
+  // long before the column's own panel -- so the device-to-host traffic is
+  // spread over the factorization instead of bunching at its end
+  const int64_t ntask = ntask0 + (io ? (2 + nst) * NT : 0);
   if (ntask > (int64_t)1 << 30) {
     set_error("tileqr_factor: DAG too large for the dataflow kernel");
     return TILEQR_ERR_ALLOC;
@@ -300,8 +309,8 @@ static int build_dag(FactorWS* ws, bool io) {
     return nG + nL + nT + offS[k] + (m - k - 1) * (NT - k - 1) + (n - k - 1);
   };
   auto idLD = [&](int64_t n) { return ntask0 + n; };
-  auto idST = [&](int64_t n) { return ntask0 + NT + n; };
-  auto idAR = [&](int64_t n) { return ntask0 + 2 * NT + n; };
+  auto idST = [&](int64_t n, int g) { return ntask0 + NT + n * nst + g; };
+  auto idAR = [&](int64_t n) { return ntask0 + NT + NT * nst + n; };
   constexpr int kArrive = dag::kArrive;  // host-only pseudo kind: set by the copy stream
   using Task = sched::Task;
   std::vector<Task> tk(ntask);
@@ -344,25 +353,30 @@ static int build_dag(FactorWS* ws, bool io) {
       Task ld{dag::kLoad, 0, 0, (int)n, 0, 0, {0, 0, 0}, 0};
       ld.dep[ld.ndep++] = (int)idAR(n);
       tk[idLD(n)] = ld;
-      // the last task writing tile column n (its chain implies every earlier writer)
-      int64_t last;
-      if (n < KT) last = (MT > n + 1) ? idT(n, MT - 1, NS - 1) : idG(n, NS - 1);
-      else last = (MT > KT) ? idS(KT - 1, MT - 1, n) : idL(KT - 1, n);
-      Task st{dag::kStore, 0, 0, (int)n, last_level, 0, {0, 0, 0}, 0};
-      st.dep[st.ndep++] = (int)last;
-      tk[idST(n)] = st;
+      for (int g = 0; g < nst; ++g) {
+        // the last task writing tile rows [r0, r1) of column n (its chain
+        // implies every earlier writer): the column's panel when the group
+        // reaches the diagonal tile, else step r1-1's last update of the column
+        const int64_t r1 = std::min<int64_t>(MT, (int64_t)(g + 1) * kIoTiles);
+        int64_t last;
+        if (n < KT && r1 - 1 >= n) {
+          last = (MT > n + 1) ? idT(n, MT - 1, NS - 1) : idG(n, NS - 1);
+        } else {
+          const int64_t k = r1 - 1;
+          last = (MT > k + 1) ? idS(k, MT - 1, n) : idL(k, n);
+        }
+        Task st{dag::kStore, 0, 0, (int)n, last_level, 0, {0, 0, 0}, g};
+        st.dep[st.ndep++] = (int)last;
+        tk[idST(n, g)] = st;
+      }
     }
   }
   const int cols = dag::dag_cols(NB);
   const int nslab = (NB + cols - 1) / cols;
-  int kIoTiles = 8;  // tiles per LOAD / STORE item
-  if (const char* e = getenv("TILEQR_DAG_IOTILES")) kIoTiles = std::max(1, atoi(e));  // diagnostics
-  const int nld = (int)((MT + kIoTiles - 1) / kIoTiles), nst = nld;
   auto parts = [&](int kind) {
     if (kind == dag::kLarfb || kind == dag::kSsrfb) return nslab;
     if (kind == dag::kLoad) return nld;
-    if (kind == dag::kStore) return nst;
-    return 1;
+    return 1;  // GEQRT / TSQRT sub-tasks, STORE groups
   };
   // bottom levels (priority of ready items in the simulation below)
   // panel weight: twice the earlier 1200 ns per column (same-box sweep of
@@ -455,6 +469,7 @@ static int build_dag(FactorWS* ws, bool io) {
   L.item_kind.clear();
   L.item_level.clear();
   L.item_info.clear();
+  L.st_order.clear();
   for (const sched::Slot& sl : sched) {
     const int i = sl.task;
     const Task& t = tk[i];
@@ -477,12 +492,15 @@ static int build_dag(FactorWS* ws, bool io) {
         it.p[0] = tp(t.k, t.k); it.p[1] = tt(t.k, t.k); it.p[2] = tp(t.k, t.n); it.pk = pkp(t.k, t.k);
         break;
       case dag::kLoad:   // tiles (m, n), m in the item's row range
-      case dag::kStore:
+      case dag::kStore: {
+        const int g = t.kind == dag::kStore ? t.s : sl.slab;
         it.aux[0] = t.n;
         it.aux[1] = t.n + 1;
-        it.aux[2] = sl.slab * kIoTiles;
-        it.aux[3] = (int)std::min<int64_t>(MT, (int64_t)(sl.slab + 1) * kIoTiles);
+        it.aux[2] = g * kIoTiles;
+        it.aux[3] = (int)std::min<int64_t>(MT, (int64_t)(g + 1) * kIoTiles);
+        if (t.kind == dag::kStore) L.st_order.push_back({t.n, g});
         break;
+      }
       default:
         it.p[0] = tp(t.m, t.k); it.p[1] = tt(t.m, t.k); it.p[2] = tp(t.k, t.n); it.p[3] = tp(t.m, t.n);
         it.pk = pkp(t.m, t.k);
@@ -498,9 +516,10 @@ static int build_dag(FactorWS* ws, bool io) {
   L.nitems = (int)items.size();
   L.ntasks = (int)ntask;
   L.nio = nst;
+  L.io_tiles = kIoTiles;
   L.id_ld = ntask0;
   L.id_st = ntask0 + NT;
-  L.id_ar = ntask0 + 2 * NT;
+  L.id_ar = ntask0 + NT + NT * nst;
   int dev = 0;
   TQ_CUDA(cudaGetDevice(&dev));
   TQ_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -952,20 +971,31 @@ static int factor_host_dag(FactorWS* ws, const double* hA, int64_t lda, double* 
   if (!ws->d_io) TQ_CUDA(cudaMalloc(&ws->d_io, sizeof(dag::DagIO)));
   TQ_CUDA(cudaMemcpyAsync(ws->d_io, &io, sizeof io, cudaMemcpyHostToDevice, s));
   if (int rc = run_dag_list(ws, L, ws->d_io, s)) return rc;
-  // copy engine, device -> host: each tile column as soon as its STORE items
-  // are done (and with it that column of T)
-  for (int64_t n = 0; n < NT; ++n) {
+  // copy engine, device -> host: each STORE group (tile rows [r0, r1) of a
+  // column) as soon as its STORE item is done, in the simulated claim order;
+  // a column's T with the group holding its diagonal tile (final with the
+  // panel)
+  const int64_t KT = std::min(MT, NT);
+  for (const auto& sg : L.st_order) {
+    const int64_t n = sg.first, g = sg.second;
     const int64_t c0 = n * NB, nc = std::min<int64_t>(NB, N - c0);
-    TQ_CU(g_wait_value((CUstream)ws->s_d2h, counter(L.id_st + n), (cuuint32_t)L.nio, CU_STREAM_WAIT_VALUE_GEQ));
-    if (ldr == M)
-      TQ_CUDA(cudaMemcpyAsync(hR + c0 * ldr, ws->st_out + c0 * M, (size_t)M * nc * sizeof(double),
-                              cudaMemcpyDeviceToHost, ws->s_d2h));
-    else
-      TQ_CUDA(cudaMemcpy2DAsync(hR + c0 * ldr, ldr * sizeof(double), ws->st_out + c0 * M, M * sizeof(double),
-                                M * sizeof(double), nc, cudaMemcpyDeviceToHost, ws->s_d2h));
-    const size_t tcol = (size_t)MT * IB * NB;
-    TQ_CUDA(cudaMemcpyAsync(hT + n * tcol, ws->Tws + n * tcol, tcol * sizeof(double), cudaMemcpyDeviceToHost,
-                            ws->s_d2h));
+    const int64_t r0 = g * L.io_tiles * NB, r1 = std::min<int64_t>(M, (g + 1) * L.io_tiles * NB);
+    TQ_CU(g_wait_value((CUstream)ws->s_d2h, counter(L.id_st + n * L.nio + g), 1, CU_STREAM_WAIT_VALUE_GEQ));
+    if (r1 > r0) {
+      if (r0 == 0 && r1 == M && ldr == M)
+        TQ_CUDA(cudaMemcpyAsync(hR + c0 * ldr, ws->st_out + c0 * M, (size_t)M * nc * sizeof(double),
+                                cudaMemcpyDeviceToHost, ws->s_d2h));
+      else
+        TQ_CUDA(cudaMemcpy2DAsync(hR + r0 + c0 * ldr, ldr * sizeof(double), ws->st_out + r0 + c0 * M,
+                                  M * sizeof(double), (r1 - r0) * sizeof(double), nc, cudaMemcpyDeviceToHost,
+                                  ws->s_d2h));
+    }
+    const int64_t gd = std::min<int64_t>(n < KT ? n : MT - 1, MT - 1) / L.io_tiles;
+    if (g == gd) {
+      const size_t tcol = (size_t)MT * IB * NB;
+      TQ_CUDA(cudaMemcpyAsync(hT + n * tcol, ws->Tws + n * tcol, tcol * sizeof(double), cudaMemcpyDeviceToHost,
+                              ws->s_d2h));
+    }
   }
   TQ_CUDA(cudaEventRecord(ws->io_ev[1], ws->s_h2d));
   TQ_CUDA(cudaEventRecord(ws->io_ev[2], ws->s_d2h));

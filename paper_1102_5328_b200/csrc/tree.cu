@@ -31,6 +31,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <tuple>
 #include <vector>
 
@@ -470,6 +471,87 @@ int tileqr_ttqrt_batched(int NB, int IB, int batch, double* const* R, double* co
   if (!A2) return -5;
   if (!T) return -6;
   return launch_ttqrt_fast(NB, IB, batch, R, A2, T, reinterpret_cast<cudaStream_t>(stream), nullptr);
+}
+
+// The domain size as a tunable ("p domains"): time
+// tileqr_factor_tree for BS = 1, 2, 4, ... (and the flat tree, BS >= MT) on a
+// seeded M x N matrix, 1 warm-up + 6 timed runs each, and
+// return the fastest BS (median).  Synchronizes the current device.
+int tileqr_tune_tree(int64_t M, int64_t N, int NB, int IB, int64_t* h_BS, double* h_ms,
+                     const char* report_json_path) {
+  if (M < 1) return -1;
+  if (N < 1) return -2;
+  if (!valid_nb_ib(NB, IB) || !dag_path_supported(NB, IB)) return -3;
+  if (!h_BS) return -5;
+  const int64_t MT = (M + NB - 1) / NB;
+  double *A0 = nullptr, *A = nullptr, *T = nullptr;
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  size_t tn = 0;
+  tileqr_t_size_tree(M, N, NB, IB, &tn);
+  auto cleanup = [&]() {
+    if (s) cudaStreamSynchronize(s);
+    cudaFree(A0); cudaFree(A); cudaFree(T);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (s) cudaStreamDestroy(s);
+  };
+  if (cudaMalloc(&A0, (size_t)M * N * 8) != cudaSuccess || cudaMalloc(&A, (size_t)M * N * 8) != cudaSuccess ||
+      cudaMalloc(&T, tn * 8) != cudaSuccess || cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    set_error("tileqr_tune_tree: allocation failed");
+    return TILEQR_ERR_ALLOC;
+  }
+  int rc = launch_rng_uniform(M, N, A0, M, 3, 0, s);
+  std::vector<int64_t> cand;
+  for (int64_t bs = 1; bs < MT; bs *= 2) cand.push_back(bs);
+  cand.push_back(MT);  // one domain: the flat tree
+  std::string rep = "[";
+  double best_ms = 1e300;
+  int64_t best = MT;
+  for (int64_t bs : cand) {
+    std::vector<float> t;
+    for (int r = 0; r < 7 && !rc; ++r) {
+      cudaMemcpyAsync(A, A0, (size_t)M * N * 8, cudaMemcpyDeviceToDevice, s);
+      cudaEventRecord(e0, s);
+      rc = tileqr_factor_tree(M, N, A, M, NB, IB, bs, T, nullptr, (tileqr_stream_t)s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r) t.push_back(ms);
+    }
+    if (rc) break;
+    std::sort(t.begin(), t.end());
+    const double med = 0.5 * (t[2] + t[3]);
+    char b[128];
+    snprintf(b, sizeof b, "%s{\"bs\": %lld, \"median_ms\": %.6f}", rep.size() > 1 ? ", " : "", (long long)bs, med);
+    rep += b;
+    if (med < best_ms) {
+      best_ms = med;
+      best = bs;
+    }
+    std::lock_guard<std::mutex> lock(g_tree_mu);  // this shape's workspace is not needed again
+    int dev = 0;
+    cudaGetDevice(&dev);
+    g_tree.erase(std::make_tuple(dev, M, N, NB, IB, bs));
+  }
+  rep += "]";
+  cleanup();
+  if (rc) return rc;
+  *h_BS = best;
+  if (h_ms) *h_ms = best_ms;
+  if (report_json_path) {
+    FILE* f = fopen(report_json_path, "w");
+    if (f) {
+      fprintf(f, "{\"M\": %lld, \"N\": %lld, \"NB\": %d, \"IB\": %d, \"runs\": %s, \"best_bs\": %lld}\n",
+              (long long)M, (long long)N, NB, IB, rep.c_str(), (long long)best);
+      fclose(f);
+    }
+  }
+  return 0;
 }
 
 void tileqr_tree_finalize(void) {

@@ -75,6 +75,7 @@ _SIGS = {
     "tileqr_apply_qt_tree": ([_c, _i64, _i64, _i64, _p, _i64, _p, _i, _i, _i64, _p, _i64, _p], _i),
     "tileqr_ttqrt_batched": ([_i, _i, _i, _p, _p, _p, _p], _i),
     "tileqr_tree_finalize": ([], None),
+    "tileqr_tune_tree": ([_i64, _i64, _i, _i, ctypes.POINTER(_i64), _PD, ctypes.c_char_p], _i),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -374,6 +375,14 @@ def apply_qt_tree(trans: str, A: torch.Tensor, m: int, k: int, T: torch.Tensor, 
                                      T.data_ptr(), nb, ib, bs, B.data_ptr(), ldb if ldb is not None else max(1, m),
                                      _stream(stream)), "tileqr_apply_qt_tree")
     return B
+
+
+def tune_tree(m: int, n: int, nb: int, ib: int, report_json_path: str | None = None):
+    """(best BS, its median ms) of tileqr_factor_tree over BS = 1, 2, 4, ..., MT."""
+    bs, ms = _i64(), _d()
+    _check(_lib.tileqr_tune_tree(m, n, nb, ib, ctypes.byref(bs), ctypes.byref(ms),
+                                 report_json_path.encode() if report_json_path else None), "tileqr_tune_tree")
+    return bs.value, ms.value
 
 
 def ttqrt_batched(nb: int, ib: int, R_ptrs, A2_ptrs, T_ptrs, stream=None):

@@ -124,3 +124,14 @@ def test_tree_deterministic(tq):
         outs.append((A, T))
     for A, T in outs[1:]:
         assert torch.equal(A, outs[0][0]) and torch.equal(T, outs[0][1])
+
+
+def test_tune_tree_picks_a_measured_bs(tq, tmp_path):
+    import json
+    m, n, nb, ib = 8192, 256, 128, 16
+    path = tmp_path / "tt.json"
+    bs, ms = tq.tune_tree(m, n, nb, ib, str(path))
+    rep = json.load(open(path))
+    runs = {r["bs"]: r["median_ms"] for r in rep["runs"]}
+    assert set(runs) == {1, 2, 4, 8, 16, 32, 64}            # powers of two below MT = 64, and MT
+    assert bs == min(runs, key=runs.get) and abs(ms - runs[bs]) < 1e-5 and rep["best_bs"] == bs
