@@ -28,6 +28,15 @@
  *     GPU counts in tileqr_dist_factor) for the same (NB, IB).
  *   - No CPU fallback exists: without a CUDA device every compute call returns
  *     TILEQR_ERR_CUDA.
+ *   - Supported input range: the reflectors form plain sums of squares with no
+ *     LAPACK-style safmin/safmax rescaling (R1), so entries must
+ *     satisfy 2^-450 <= |a_ij| <= 2^450 (or be 0) for every sum to stay in
+ *     the normal FP64 range; scaling A by a power of two inside that range
+ *     scales R exactly and leaves V and T unchanged (tests).
+ *   - Concurrency: calls of the same shape share one cached workspace; each
+ *     call's stream waits for the previous call's last operation on it (an
+ *     event), so same-shape calls on different streams or host threads are
+ *     serialised on the device, not corrupted.
  */
 #ifndef TILEQR_H_
 #define TILEQR_H_

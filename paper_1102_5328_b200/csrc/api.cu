@@ -67,6 +67,27 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   return TILEQR_ERR_CUDA;
 }
 
+int stream_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  TQ_CUDA(cudaGetDevice(&dev));
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), dev) == done.end()) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+      done.push_back(dev);
+    }
+  }
+  TQ_CUDA(cudaMallocAsync(p, bytes, s));
+  return 0;
+}
+
 static int arg_error(int i, const char* fn, const char* what) {
   char buf[256];
   snprintf(buf, sizeof buf, "%s: illegal argument %d (%s)", fn, i, what);
@@ -1179,9 +1200,9 @@ int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double
   // per launch: LARFB tasks (k, n) n < BT; SSRFB tasks (k, m, n) n < BT
   const int64_t nlaunch_s = KT * MT;  // upper bound
   const size_t nptr = (size_t)KT * BT * 3 + (size_t)nlaunch_s * BT * 4;
-  TQ_CUDA(cudaMallocAsync(&Vt, tile * MT * KT * sizeof(double), s));
-  TQ_CUDA(cudaMallocAsync(&Bt, tile * MT * BT * sizeof(double), s));
-  TQ_CUDA(cudaMallocAsync(&dp, nptr * sizeof(void*), s));
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&Vt), tile * MT * KT * sizeof(double), s)) return rc_;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&Bt), tile * MT * BT * sizeof(double), s)) return rc_;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&dp), nptr * sizeof(void*), s)) return rc_;
   int rc = launch_v_to_tiles(M, K, A, lda, NB, MT, KT, Vt, s);
   if (!rc) rc = launch_layout_to_tiles(M, NRHS, B, ldb, NB, MT, BT, Bt, nullptr, s);
   std::vector<void*> hp(nptr);
@@ -1245,8 +1266,8 @@ static int packed_update(bool larfb, int NB, int IB, int batch, const double* co
   const size_t pd = v2_pk_doubles(NB, IB);
   double* buf = nullptr;
   double** ptr = nullptr;
-  TQ_CUDA(cudaMallocAsync(&buf, pd * batch * sizeof(double), s));
-  TQ_CUDA(cudaMallocAsync(&ptr, (size_t)batch * sizeof(double*), s));
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&buf), pd * batch * sizeof(double), s)) return rc_;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&ptr), (size_t)batch * sizeof(double*), s)) return rc_;
   int rc = launch_fill_ptrs(ptr, buf, pd, batch, s);
   if (!rc) rc = launch_pack(larfb, NB, IB, batch, V, T, ptr, s);
   if (!rc) rc = launch_update_pk(larfb, NB, IB, batch, ptr, C1, C2, s);

@@ -85,6 +85,12 @@ bool dag_path_supported(int NB, int IB);  // the dataflow kernel with packed ref
 // ---- multi-GPU helpers (dist.cu) for tileqr_tune with ngpus > 1 -----------------
 int dist_ranks(int* nranks, int* rank);
 int dist_host_collective(double* h, int n, int op);  // op 0: broadcast from rank 0, 1: max over ranks
+// Stream-ordered scratch (cudaMallocAsync) from the device's default pool,
+// which is told once per device to keep freed memory (release threshold =
+// max): the batched / apply entry points allocate per call, and a pool that
+// returns memory to the driver at every synchronisation made each such call
+// pay a fresh allocation (~0.3-2 ms, measured on the wide-panel launches).
+int stream_alloc(void** p, size_t bytes, cudaStream_t s);
 // Free the cached tileqr_factor workspace of one shape (api.cu; waits for its last use).
 void release_ws(int dev, int64_t M, int64_t N, int NB, int IB);
 

@@ -293,6 +293,66 @@ int launch_panel(int NB, int IB, int batch, double* const* R, double* const* B, 
   return 0;
 }
 
+// ---- wide panels (IB > 32, IB % 8 == 0, IB <= 64): T assembly ------------------
+// The GEQRT / TSQRT of a wide inner panel runs the register-resident panel
+// kernel with inner blocking IBi (the largest of 32, 24, 16, 8 dividing IB):
+// its reflectors, R and V are those of the IB-blocked algorithm (applying the
+// IBi-blocks of a panel in order IS applying the panel's reflectors in order;
+// DESIGN.md R22), only the compact-WY factor differs.  This kernel assembles
+// T_p of every IB-panel from the reflectors (the
+// oracle's recurrence): T[i,i] = tau_i (the diagonal of the IBi-blocked T),
+// T[0:i, i] = -tau_i T[0:i, 0:i] z with z_l = v_l^T v_i -- GEQRT: v_i = e_i +
+// strictly-lower column of the tile; TSQRT: v_i = [e_i; V2(:, i)].
+constexpr int kWideIB = 64;
+
+template <bool TS>
+__global__ void __launch_bounds__(kThreads)
+wide_t_kernel(int NB, int IB, int IBi, const double* const* Vp, const double* const* Tin, double* const* Tout) {
+  extern __shared__ double sm[];
+  double* Vs = sm;                        // NB x IB, column-major (ld NB + 1)
+  double* G = Vs + (size_t)(NB + 1) * IB; // IB x IB
+  double* Tp = G + (size_t)IB * IB;       // IB x IB
+  const double* V = Vp[blockIdx.x];
+  const double* Ti = Tin[blockIdx.x];
+  double* To = Tout[blockIdx.x];
+  const int tid = threadIdx.x, ldv = NB + 1;
+  for (int c0 = 0; c0 < NB; c0 += IB) {
+    for (int e = tid; e < NB * IB; e += kThreads) {
+      const int c = e / NB, r = e - c * NB, j = c0 + c;
+      double v = __ldcg(V + r + (size_t)j * NB);
+      if (!TS) v = r == j ? 1.0 : (r > j ? v : 0.0);   // GEQRT: unit lower trapezoid
+      Vs[r + c * ldv] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < IB * IB; e += kThreads) {   // z: G[l, i] = v_l^T v_i, l < i
+      const int i = e / IB, l = e - i * IB;
+      double acc = 0.0;
+      if (l < i)  // TSQRT: the top parts e_l, e_i are orthogonal, only V2 contributes
+        for (int r = 0; r < NB; ++r) acc = fma(Vs[r + l * ldv], Vs[r + i * ldv], acc);
+      G[l + i * IB] = acc;
+      Tp[l + i * IB] = 0.0;
+    }
+    __syncthreads();
+    for (int i = 0; i < IB; ++i) {                    // forward recurrence, one column at a time
+      const int j = c0 + i;
+      const double tau = __ldcg(Ti + (j % IBi) + (size_t)j * IBi);
+      if (tid < i) {
+        double acc = 0.0;
+        for (int l = tid; l < i; ++l) acc = fma(Tp[tid + l * IB], G[l + i * IB], acc);
+        Tp[tid + i * IB] = -tau * acc;
+      } else if (tid == i) {
+        Tp[i + i * IB] = tau;
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < IB * IB; e += kThreads) {
+      const int i = e / IB, l = e - i * IB;
+      To[l + (size_t)(c0 + i) * IB] = l <= i ? Tp[l + i * IB] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 bool panel_fast_supported(int NB, int IB);
@@ -300,6 +360,44 @@ int launch_geqrt_fast(int NB, int IB, int batch, double* const* A, double* const
                       double* const* Pk);
 int launch_tsqrt_fast(int NB, int IB, int batch, double* const* R, double* const* A2,
                       double* const* T, cudaStream_t s, double* const* Pk);
+
+static int wide_inner(int IB) {
+  for (int c : {32, 24, 16, 8})
+    if (IB % c == 0) return c;
+  return 0;
+}
+
+bool panel_wide_supported(int NB, int IB) {
+  return NB % 32 == 0 && NB >= 32 && NB <= 256 && IB > 32 && IB <= kWideIB && IB % 8 == 0 && NB % IB == 0 &&
+         panel_fast_supported(NB, wide_inner(IB));
+}
+
+// wide panel: the fast kernel at IBi into scratch T, T assembled at IB, then the packed copy
+template <bool TS>
+static int launch_wide(int NB, int IB, int batch, double* const* R, double* const* B, double* const* T,
+                       cudaStream_t s, double* const* Pk) {
+  const int IBi = wide_inner(IB);
+  double* ti = nullptr;
+  double** tp = nullptr;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&ti), (size_t)batch * IBi * NB * sizeof(double), s)) return rc_;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&tp), (size_t)batch * sizeof(double*), s)) return rc_;
+  int rc = launch_fill_ptrs(tp, ti, (size_t)IBi * NB, batch, s);
+  if (!rc) rc = TS ? launch_tsqrt_fast(NB, IBi, batch, R, B, tp, s, nullptr) : launch_geqrt_fast(NB, IBi, batch, R, tp, s, nullptr);
+  if (!rc) {
+    const size_t bytes = ((size_t)(NB + 1) * IB + 2 * (size_t)IB * IB) * sizeof(double);
+    auto kern = wide_t_kernel<TS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) {
+      kern<<<batch, kThreads, bytes, s>>>(NB, IB, IBi, TS ? B : R, tp, T);
+      e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) rc = cuda_fail(e, "wide_t_kernel", __FILE__, __LINE__);
+  }
+  if (!rc && Pk) rc = launch_pack(!TS, NB, IB, batch, TS ? B : R, T, Pk, s);
+  cudaFreeAsync(ti, s);
+  cudaFreeAsync(tp, s);
+  return rc;
+}
 
 static bool generic_panel_forced() {
   static int v = -1;
@@ -315,6 +413,8 @@ int launch_geqrt(int NB, int IB, int batch, double* const* A, double* const* T, 
   if (batch <= 0) return 0;
   if (panel_fast_supported(NB, IB) && !generic_panel_forced())
     return launch_geqrt_fast(NB, IB, batch, A, T, s, Pk);
+  if (panel_wide_supported(NB, IB) && !generic_panel_forced())
+    return launch_wide<false>(NB, IB, batch, A, nullptr, T, s, Pk);
   int rc = launch_panel<false>(NB, IB, batch, A, nullptr, T, s);
   if (!rc && Pk) rc = launch_pack(true, NB, IB, batch, A, T, Pk, s);
   return rc;
@@ -325,6 +425,8 @@ int launch_tsqrt(int NB, int IB, int batch, double* const* R, double* const* A2,
   if (batch <= 0) return 0;
   if (panel_fast_supported(NB, IB) && !generic_panel_forced())
     return launch_tsqrt_fast(NB, IB, batch, R, A2, T, s, Pk);
+  if (panel_wide_supported(NB, IB) && !generic_panel_forced())
+    return launch_wide<true>(NB, IB, batch, R, A2, T, s, Pk);
   int rc = launch_panel<true>(NB, IB, batch, R, A2, T, s);
   if (!rc && Pk) rc = launch_pack(false, NB, IB, batch, A2, T, Pk, s);
   return rc;

@@ -217,13 +217,17 @@ bool v2_supported(int NB, int IB) {
   if (force_simt()) return false;
   const char* e = getenv("TILEQR_NO_V2");
   if (e && e[0] == '1') return false;
-  return NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB >= 8 && IB <= 32 && NB % IB == 0;
+  if (!(NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB >= 8 && IB <= 64 && NB % IB == 0)) return false;
+  if (IB <= 32) return true;
+  // wide panels (update_v2.cuh pk_fits): two ring stages of one group + T_p within 220 KB
+  const size_t gw = (IB + 15) / 16 * 16;
+  return 2 * ((size_t)NB * gw + (size_t)IB * 66) * sizeof(double) <= 220 * 1024;
 }
 
 size_t v2_pk_doubles(int NB, int IB) {
-  if (IB % 8 || IB < 8 || IB > 32 || NB % IB) return 0;
-  const int GW = IB <= 16 ? 16 : 32, PW = IB == 8 ? 8 : GW, PPG = GW / PW, NP = NB / IB;
-  const int NG = (NP + PPG - 1) / PPG, LDT2 = IB <= 16 ? 18 : 34;
+  if (IB % 8 || IB < 8 || IB > 64 || NB % IB) return 0;
+  const int GW = IB <= 16 ? 16 : IB <= 32 ? 32 : (IB + 15) / 16 * 16, PW = IB == 8 ? 8 : GW, PPG = GW / PW;
+  const int NP = NB / IB, NG = (NP + PPG - 1) / PPG, LDT2 = IB <= 16 ? 18 : IB <= 32 ? 34 : 66;
   return (size_t)NG * NB * GW + (size_t)NP * IB * LDT2;
 }
 

@@ -272,15 +272,19 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       }
       const double w = fma(scal, d, rjl);
       const double tw = col < IB ? tau * w : 0.0;
-      // select-free rank-1 update of the reflector rows, x += coef * vj:
-      //   lane == jj: coef = scal - 1 (vj == x there: x becomes v2 = x2 * scal);
-      //   lane >  jj: coef = -tw * scal;   lane < jj: coef = 0.
-      const double coef = (col == jj) ? scal - 1.0 : (col > jj ? -tw * scal : 0.0);
+      // select-free rank-1 update of the reflector rows, x = x * m + coef * vj:
+      //   lane == jj: m = scal, coef = 0 (x becomes v2 = x2 * scal, one rounding);
+      //   lane >  jj: m = 1,  coef = -tw * scal;   lane < jj: m = 1, coef = 0.
+      // (Round 1 folded the pivot lane into one fma with coef = scal - 1; the
+      // rounding of scal - 1 costs |scal|^-1 ulps, i.e. all of v2 once the
+      // column norm reaches ~2^50 -- tests/test_gpu_parity.py scaled inputs.)
+      const double coef = (col > jj) ? -tw * scal : 0.0;
+      const double mlt = (col == jj) ? scal : 1.0;
 #pragma unroll
-      for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q]);
+      for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q] * mlt);
       if (!TS) {
 #pragma unroll
-        for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t]);
+        for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t] * mlt);
       }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
       if (warp == 0 && hg == 0 && col >= jj && col < IB) S.Rout[jj * LDR + col] = (col == jj) ? beta : rjl - tw;

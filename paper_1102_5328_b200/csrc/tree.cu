@@ -387,9 +387,9 @@ int tileqr_apply_qt_tree(char trans, int64_t M, int64_t NRHS, int64_t K, const d
   const int64_t KT = std::min(MT, KTt);
   const size_t tile = (size_t)NB * NB, ttile = (size_t)IB * NB, tsz = (size_t)MT * KTt * ttile;
   double *Vt = nullptr, *Ut = nullptr, *Bt = nullptr;
-  TQ_CUDA(cudaMallocAsync(&Vt, tile * MT * KT * sizeof(double), s));
-  TQ_CUDA(cudaMallocAsync(&Ut, tile * MT * KT * sizeof(double), s));
-  TQ_CUDA(cudaMallocAsync(&Bt, tile * MT * BT * sizeof(double), s));
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&Vt), tile * MT * KT * sizeof(double), s)) return rc_;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&Ut), tile * MT * KT * sizeof(double), s)) return rc_;
+  if (int rc_ = stream_alloc(reinterpret_cast<void**>(&Bt), tile * MT * BT * sizeof(double), s)) return rc_;
   int rc = launch_v_to_tiles(M, K, A, lda, NB, MT, KT, Vt, s);
   if (!rc) {
     triu_tiles_kernel<<<(unsigned)(MT * KT), 256, 0, s>>>(Vt, Ut, NB);  // TTQRT V2 (upper triangles)
@@ -422,8 +422,7 @@ int tileqr_apply_qt_tree(char trans, int64_t M, int64_t NRHS, int64_t K, const d
   void** dp = nullptr;
   const size_t per = 4 * (size_t)BT;
   if (!rc) {
-    cudaError_t e = cudaMallocAsync(&dp, std::max<size_t>(1, ops.size() * per) * sizeof(void*), s);
-    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocAsync", __FILE__, __LINE__);
+    rc = stream_alloc(reinterpret_cast<void**>(&dp), std::max<size_t>(1, ops.size() * per) * sizeof(void*), s);
   }
   std::vector<void*> hp(ops.size() * per);
   for (size_t o = 0; o < ops.size(); ++o)

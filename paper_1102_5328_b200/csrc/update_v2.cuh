@@ -43,30 +43,45 @@
 namespace tileqr {
 namespace v2 {
 
+// Wide panels (IB in {40, 48, 56, 64}): one panel per group of GW = IB rounded
+// up to 16 columns (the XOR swizzle flips column bits 0-3 only, so it stays
+// inside the group), T_p with ld 66 (== 2 mod 16), one warp column block
+// (MB = 1) per warp; only where two ring stages fit in shared memory.
 template <int NB, int IB>
 struct Pk {
-  static constexpr int GW = IB <= 16 ? 16 : 32;           // group width
+  static constexpr int GW = IB <= 16 ? 16 : IB <= 32 ? 32 : (IB + 15) / 16 * 16;  // group width
   static constexpr int PW = IB == 8 ? 8 : GW;             // packed panel width
   static constexpr int PPG = GW / PW;                     // panels per group
   static constexpr int NP = NB / IB;                      // panels
   static constexpr int NG = (NP + PPG - 1) / PPG;         // groups
-  static constexpr int LDT2 = IB <= 16 ? 18 : 34;
+  static constexpr int LDT2 = IB <= 16 ? 18 : IB <= 32 ? 34 : 66;
   static constexpr int GDBL = NB * GW;                    // doubles per V group
   static constexpr int TOFF = NG * GDBL;
   static constexpr int TP = IB * LDT2;                    // doubles per T_p
   static constexpr int TOTAL = TOFF + NP * TP;            // doubles per packed tile
   static constexpr int NBK = IB / 8;
-  static_assert(IB % 8 == 0 && IB <= 32 && NB % IB == 0, "packed tile geometry");
+  static_assert(IB % 8 == 0 && IB <= 64 && NB % IB == 0, "packed tile geometry");
 };
 
 __host__ __device__ constexpr int pk_f(int r) { return (r & 1) | ((r & 2) << 2) | (r & 4); }
 
 // packed-tile size in doubles for a runtime (NB, IB) (0 if unsupported)
 inline size_t pk_doubles(int NB, int IB) {
-  if (IB % 8 || IB > 32 || NB % IB) return 0;
-  const int GW = IB <= 16 ? 16 : 32, PW = IB == 8 ? 8 : GW, PPG = GW / PW, NP = NB / IB;
-  const int NG = (NP + PPG - 1) / PPG, LDT2 = IB <= 16 ? 18 : 34;
+  if (IB % 8 || IB > 64 || NB % IB) return 0;
+  const int GW = IB <= 16 ? 16 : IB <= 32 ? 32 : (IB + 15) / 16 * 16, PW = IB == 8 ? 8 : GW, PPG = GW / PW;
+  const int NP = NB / IB, NG = (NP + PPG - 1) / PPG, LDT2 = IB <= 16 ? 18 : IB <= 32 ? 34 : 66;
   return (size_t)NG * NB * GW + (size_t)NP * IB * LDT2;
+}
+
+// a wide-panel geometry is built only where two ring stages fit (<= 220 KB)
+template <int NB, int IB>
+constexpr bool pk_fits() {
+  if constexpr (IB % 8 != 0 || IB > 64 || NB % IB != 0) {
+    return false;
+  } else {
+    using P = Pk<NB, IB>;
+    return IB <= 32 || 2 * (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double) <= 220 * 1024;
+  }
 }
 
 // ---- mbarrier / bulk-copy helpers -------------------------------------------
@@ -392,6 +407,8 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
 constexpr int kWarpsB = 8;  // warps per CTA of the batched v2 kernels (same geometry as the DAG kernel)
 
 __host__ __device__ constexpr int v2_mb(int NB) { return (NB == 96 || NB == 128) ? 2 : 1; }
+// batched kernel: wide panels keep one 8-column block per warp (registers)
+__host__ __device__ constexpr int v2_mb(int NB, int IB) { return IB > 32 ? 1 : v2_mb(NB); }
 
 // ring stages of the batched kernel: the whole packed tile when it fits
 // (NB <= 128), else as many column groups as fit in ~200 KB (refilled by TMA
@@ -418,7 +435,7 @@ __device__ __forceinline__ int active_warps(int col0, int cend = NB) {
 template <int NB, int IB, bool LARFB>
 __global__ void __launch_bounds__(kWarpsB * 32, 1)
 update_v2_kernel(const double* const* Pkp, double* const* C1p, double* const* C2p) {
-  constexpr int MB = v2_mb(NB);
+  constexpr int MB = v2_mb(NB, IB);
   constexpr int S = v2_stages<NB, IB>();  // whole tile resident for NB <= 128
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[S], empty[S];
@@ -459,7 +476,7 @@ int launch_update_v2_t(int batch, const double* const* Pk_, double* const* C1, d
   const size_t bytes = v2_smem_bytes<NB, IB>();
   static_assert(v2_smem_bytes<NB, IB>() <= 227 * 1024, "packed tile exceeds shared memory");
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  constexpr int cols = kWarpsB * 8 * v2_mb(NB);
+  constexpr int cols = kWarpsB * 8 * v2_mb(NB, IB);
   dim3 grid((NB + cols - 1) / cols, batch);
   kern<<<grid, kWarpsB * 32, bytes, s>>>(Pk_, C1, C2);
   TQ_LAUNCH_CHECK();
@@ -474,18 +491,22 @@ int launch_update_v2(bool larfb, int IB, int batch, const double* const* Pk_, do
   case ib:                                                                                     \
     return larfb ? launch_update_v2_t<NB, ib, true>(batch, Pk_, C1, C2, s)                     \
                  : launch_update_v2_t<NB, ib, false>(batch, Pk_, C1, C2, s);
+#define TQ_V2W(ib)                                                                             \
+  case ib:                                                                                     \
+    if constexpr (pk_fits<NB, ib>())                                                           \
+      return larfb ? launch_update_v2_t<NB, ib, true>(batch, Pk_, C1, C2, s)                   \
+                   : launch_update_v2_t<NB, ib, false>(batch, Pk_, C1, C2, s);                 \
+    break;
   switch (IB) {
     TQ_V2(8) TQ_V2(16) TQ_V2(32)
-    case 24:
-      if constexpr (NB % 24 == 0)
-        return larfb ? launch_update_v2_t<NB, 24, true>(batch, Pk_, C1, C2, s)
-                     : launch_update_v2_t<NB, 24, false>(batch, Pk_, C1, C2, s);
-      [[fallthrough]];
+    TQ_V2W(24) TQ_V2W(40) TQ_V2W(48) TQ_V2W(56) TQ_V2W(64)
     default:
-      set_error("update_v2: unsupported IB");
-      return TILEQR_ERR_CUDA;
+      break;
   }
+  set_error("update_v2: unsupported IB");
+  return TILEQR_ERR_CUDA;
 #undef TQ_V2
+#undef TQ_V2W
 }
 
 template <int NB>
@@ -497,20 +518,24 @@ int launch_pack(bool larfb, int IB, int batch, const double* const* V, const dou
     if (larfb) pack_kernel<NB, ib, true><<<batch, 256, 0, s>>>(V, T, Pk_);                    \
     else pack_kernel<NB, ib, false><<<batch, 256, 0, s>>>(V, T, Pk_);                         \
     break;
+#define TQ_PKW(ib)                                                                            \
+  case ib:                                                                                    \
+    if constexpr (pk_fits<NB, ib>()) {                                                        \
+      if (larfb) pack_kernel<NB, ib, true><<<batch, 256, 0, s>>>(V, T, Pk_);                  \
+      else pack_kernel<NB, ib, false><<<batch, 256, 0, s>>>(V, T, Pk_);                       \
+      break;                                                                                  \
+    }                                                                                         \
+    set_error("pack: unsupported IB");                                                        \
+    return TILEQR_ERR_CUDA;
   switch (IB) {
     TQ_PK(8) TQ_PK(16) TQ_PK(32)
-    case 24:
-      if constexpr (NB % 24 == 0) {
-        if (larfb) pack_kernel<NB, 24, true><<<batch, 256, 0, s>>>(V, T, Pk_);
-        else pack_kernel<NB, 24, false><<<batch, 256, 0, s>>>(V, T, Pk_);
-        break;
-      }
-      [[fallthrough]];
+    TQ_PKW(24) TQ_PKW(40) TQ_PKW(48) TQ_PKW(56) TQ_PKW(64)
     default:
       set_error("pack: unsupported IB");
       return TILEQR_ERR_CUDA;
   }
 #undef TQ_PK
+#undef TQ_PKW
   TQ_LAUNCH_CHECK();
   return 0;
 }

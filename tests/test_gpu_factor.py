@@ -77,6 +77,9 @@ CASES = [
     (512, 512, 160, 40, 19),
     (384, 384, 192, 64, 20),
     (600, 600, 256, 16, 22),   # NB > 128 on the packed update (dataflow kernel)
+    (500, 500, 128, 64, 25),   # wide panel: generic panel kernel + packed update (levels)
+    (400, 400, 96, 48, 26),
+    (500, 500, 192, 48, 27),
     (500, 500, 160, 32, 23),
     (200, 200, 48, 6, 21),     # SIMT path (NB % 32 != 0)
     (64, 64, 64, 16, 22),      # single tile

@@ -153,6 +153,8 @@ def test_rng_matches_synth_inputs(tq):
 
 
 PACKED = [(nb, ib) for nb in (32, 64, 96, 128, 160, 192, 224, 256) for ib in (8, 16, 24, 32) if nb % ib == 0]
+# wide panels (IB > 32, one group per panel) where two ring stages fit in shared memory
+PACKED += [(64, 64), (96, 48), (128, 64), (160, 40), (192, 48)]
 
 
 @pytest.mark.parametrize("nb,ib", PACKED)
@@ -210,3 +212,12 @@ def test_packed_layout_is_a_permutation_of_v_and_t(tq):
     want_nonzero = np.sort(np.concatenate([vu[vu != 0]] + [b[b != 0] for b in tt]))
     assert not np.any(got == 12345.0)                       # every slot written
     assert np.array_equal(got[got != 0], want_nonzero)
+
+
+def test_packed_geometry_coverage(tq):
+    """The packed update covers IB in {8, 16, 24, 32} and the wide panels whose
+    two ring stages fit; the others report no packed form."""
+    for nb, ib in PACKED:
+        assert tq.packed_size(nb, ib) > 0, (nb, ib)
+    for nb, ib in [(192, 64), (256, 64), (224, 56), (128, 128), (96, 12)]:
+        assert tq.packed_size(nb, ib) == 0, (nb, ib)

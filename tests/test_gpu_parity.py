@@ -255,3 +255,46 @@ def test_negative_zero_pivots(tq):
     fb = tq.from_colmajor(B)
     assert fb[0, 0] == 0.0 and np.signbit(fb[0, 0])
     assert not np.any(TB.cpu().numpy())
+
+
+@pytest.mark.parametrize("scale_exp", [-300, -100, 100, 300])
+def test_scaled_inputs_within_the_supported_range(tq, scale_exp):
+    """No safmin / safmax rescaling (R1, include/tileqr.h): inputs
+    with |a| in [2^-450, 2^450] keep every sum of squares in the normal range.
+    Scaling A by a power of two scales R exactly and leaves V, T unchanged."""
+    m, n, nb, ib = 600, 500, 128, 16
+    a = si.uniform(m, n, 650)
+    s = 2.0 ** scale_exp
+    A1, A2 = tq.to_colmajor(a), tq.to_colmajor(a * s)
+    T1, _ = tq.factor(A1, m, n, nb, ib)
+    T2, info = tq.factor(A2, m, n, nb, ib)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    f1, f2 = tq.from_colmajor(A1), tq.from_colmajor(A2)
+    assert nrel(np.triu(f2) / s, np.triu(f1)) < 1e-13
+    assert nrel(np.tril(f2, -1), np.tril(f1, -1)) < 1e-13
+    assert nrel(T2.cpu().numpy(), T1.cpu().numpy()) < 1e-13
+
+
+def test_concurrent_same_shape_calls_on_two_streams(tq):
+    """Two factorizations of the same shape (one cached workspace) issued on
+    two streams without synchronisation: the workspace's last-use event
+    orders them, and both results are exact."""
+    m = n = 1024
+    nb, ib = 128, 16
+    a, b = si.uniform(m, n, 660), si.uniform(m, n, 661)
+    ref_a, ref_b = tq.to_colmajor(a), tq.to_colmajor(b)
+    Ta, _ = tq.factor(ref_a, m, n, nb, ib)
+    Tb, _ = tq.factor(ref_b, m, n, nb, ib)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        A, B = tq.to_colmajor(a), tq.to_colmajor(b)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            T1, _ = tq.factor(A, m, n, nb, ib, stream=s1)
+        with torch.cuda.stream(s2):
+            T2, _ = tq.factor(B, m, n, nb, ib, stream=s2)
+        torch.cuda.synchronize()
+        assert torch.equal(A, ref_a) and torch.equal(T1, Ta)
+        assert torch.equal(B, ref_b) and torch.equal(T2, Tb)
