@@ -183,8 +183,10 @@ int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* co
                          int ncols, tileqr_stream_t stream);
 
 /* Packed reflector tiles -- the operand format of the factorization's
- * trailing-update kernel for NB in {32, 64, 96, 128}, IB in {8, 16, 24, 32}
- * (IB | NB): the V_p / T_p of a tile in the shared-memory image the
+ * trailing-update kernel for NB % 32 == 0, NB <= 256, and IB | NB with
+ * IB in {8, 16, 24, 32} or a wide IB in {40, 48, 56, 64} whose column group
+ * plus T_p fits one shared-memory ring stage (every such pair of the tuning
+ * grid): the V_p / T_p of a tile in the shared-memory image the
  * barrier-free DMMA update loads with TMA bulk copies (layout: DESIGN.md §5,
  * csrc/update_v2.cuh).  tileqr_factor writes them itself from its GEQRT /
  * TSQRT kernels; these entry points expose the same kernels for tests and

@@ -219,9 +219,9 @@ bool v2_supported(int NB, int IB) {
   if (e && e[0] == '1') return false;
   if (!(NB % 32 == 0 && NB >= 32 && NB <= 256 && IB % 8 == 0 && IB >= 8 && IB <= 64 && NB % IB == 0)) return false;
   if (IB <= 32) return true;
-  // wide panels (update_v2.cuh pk_fits): two ring stages of one group + T_p within 220 KB
+  // wide panels (update_v2.cuh pk_fits): one ring stage (a group + T_p) within 220 KB
   const size_t gw = (IB + 15) / 16 * 16;
-  return 2 * ((size_t)NB * gw + (size_t)IB * 66) * sizeof(double) <= 220 * 1024;
+  return ((size_t)NB * gw + (size_t)IB * 66) * sizeof(double) <= 220 * 1024;
 }
 
 size_t v2_pk_doubles(int NB, int IB) {

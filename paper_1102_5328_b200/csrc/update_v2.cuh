@@ -46,7 +46,7 @@ namespace v2 {
 // Wide panels (IB in {40, 48, 56, 64}): one panel per group of GW = IB rounded
 // up to 16 columns (the XOR swizzle flips column bits 0-3 only, so it stays
 // inside the group), T_p with ld 66 (== 2 mod 16), one warp column block
-// (MB = 1) per warp; only where two ring stages fit in shared memory.
+// (MB = 1) per warp; a one-stage ring where two stages do not fit.
 template <int NB, int IB>
 struct Pk {
   static constexpr int GW = IB <= 16 ? 16 : IB <= 32 ? 32 : (IB + 15) / 16 * 16;  // group width
@@ -80,7 +80,7 @@ constexpr bool pk_fits() {
     return false;
   } else {
     using P = Pk<NB, IB>;
-    return IB <= 32 || 2 * (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double) <= 220 * 1024;
+    return IB <= 32 || (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double) <= 220 * 1024;
   }
 }
 
@@ -418,7 +418,10 @@ constexpr int v2_stages() {
   using P = Pk<NB, IB>;
   constexpr size_t stage = (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double);
   constexpr int s = (int)((200 * 1024) / stage);
-  return s >= P::NG ? P::NG : (s < 2 ? 2 : s);
+  // wide panels whose group + T_p exceed 100 KB keep ONE stage (refilled when
+  // every warp has released it: the TMA of the next group is then exposed)
+  constexpr int lo = (IB > 32 && 2 * stage > 220 * 1024) ? 1 : 2;
+  return s >= P::NG ? P::NG : (s < lo ? lo : s);
 }
 
 template <int NB, int IB>

@@ -153,8 +153,8 @@ def test_rng_matches_synth_inputs(tq):
 
 
 PACKED = [(nb, ib) for nb in (32, 64, 96, 128, 160, 192, 224, 256) for ib in (8, 16, 24, 32) if nb % ib == 0]
-# wide panels (IB > 32, one group per panel) where two ring stages fit in shared memory
-PACKED += [(64, 64), (96, 48), (128, 64), (160, 40), (192, 48)]
+# wide panels (IB > 32, one group per panel; one ring stage where two do not fit)
+PACKED += [(64, 64), (96, 48), (128, 64), (160, 40), (192, 48), (192, 64), (224, 56), (256, 64)]
 
 
 @pytest.mark.parametrize("nb,ib", PACKED)
@@ -219,5 +219,5 @@ def test_packed_geometry_coverage(tq):
     two ring stages fit; the others report no packed form."""
     for nb, ib in PACKED:
         assert tq.packed_size(nb, ib) > 0, (nb, ib)
-    for nb, ib in [(192, 64), (256, 64), (224, 56), (128, 128), (96, 12)]:
+    for nb, ib in [(128, 128), (256, 128), (160, 80), (96, 12), (160, 10)]:
         assert tq.packed_size(nb, ib) == 0, (nb, ib)
