@@ -77,14 +77,46 @@ constexpr bool dag_v2() {
 #endif
 }
 
+// C2 prefetch (2 CTAs per SM, NB <= 128): during the last inner panel of an
+// update item, thread 0 checks the next claimed item's dependencies without
+// blocking and, if they hold and it is an update, copies that item's C2
+// column slab (NB x W*8*MB doubles, contiguous in the tile) into a shared
+// staging buffer with one TMA bulk copy; the next item then fills its
+// accumulator registers from shared memory instead of from L2 at its start.
+// Enabled where a ring of two stages plus the staging buffer fits the 2-CTA
+// budget (110 KB) and the items are long enough (NB >= 96) for the check in
+// the last panel to pay: same-box A/B at 10000^2, (128, 16) -1.4 %, while NB
+// = 64 items (~5 us) lost 10-17 % to the extra latency on warp 0 and a
+// one-stage budget (128, 32) halved the resident CTAs (+38 %).
+template <int NB, int KW>
+constexpr bool dag_c2pf() {
+#ifdef TILEQR_NO_C2PF
+  return false;
+#else
+  if constexpr (dag_v2<NB>() && dag_ctas_per_sm(NB) == 2 && NB >= 96 && NB % KW == 0) {
+    using P = v2::Pk<NB, KW>;
+    constexpr size_t stage = (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double);
+    constexpr size_t c2 = (size_t)NB * dag_warps(NB) * 8 * dag_mb(NB) * sizeof(double);
+    return 2 * stage + c2 <= 110 * 1024;
+  } else {
+    return false;
+  }
+#endif
+}
+template <int NB, int KW>
+constexpr size_t dag_c2_bytes() {
+  return dag_c2pf<NB, KW>() ? (size_t)NB * dag_warps(NB) * 8 * dag_mb(NB) * sizeof(double) : 0;
+}
+
 // Ring stages of the packed reflector tile per CTA: as many as fit in ~110 KB
-// (2 CTAs per SM, NB <= 128) or ~200 KB (1 CTA), at least 2, at most 8.
+// (2 CTAs per SM, NB <= 128; less the C2 staging buffer) or ~200 KB (1 CTA),
+// at least 2, at most 8.
 template <int NB, int KW>
 constexpr int dag_stages() {
   if constexpr (dag_v2<NB>() && NB % KW == 0) {
     using P = v2::Pk<NB, KW>;
     constexpr size_t stage = (size_t)(P::GDBL + P::PPG * P::TP) * sizeof(double);
-    constexpr size_t budget = dag_ctas_per_sm(NB) == 2 ? 110 * 1024 : 200 * 1024;
+    constexpr size_t budget = (dag_ctas_per_sm(NB) == 2 ? 110 * 1024 : 200 * 1024) - dag_c2_bytes<NB, KW>();
 #ifdef TILEQR_FULL_RING
     constexpr int s = P::NG;
 #else
@@ -106,7 +138,8 @@ struct DagSmem {
       (2 * (size_t)LS::STAGE + (size_t)W * 8 * MB * (KW + 4)) * sizeof(double);
   static constexpr size_t v2_bytes =
       (NB % KW == 0) ? v2::Ring<NB, (NB % KW == 0 ? KW : 8), dag_stages<NB, KW>()>::bytes : 0;
-  static constexpr size_t upd_bytes = dag_v2<NB>() ? v2_bytes : old_bytes;
+  static constexpr size_t upd_bytes = dag_v2<NB>() ? v2_bytes + dag_c2_bytes<NB, KW>() : old_bytes;
+  static constexpr size_t c2_off = v2_bytes;  // C2 staging buffer after the ring
   static constexpr size_t pan_bytes = sizeof(pf::FastSmem<NB, W>);
 #ifdef TILEQR_ONE_CTA  // diagnostics: force one CTA per SM
   static constexpr size_t bytes0 = upd_bytes > pan_bytes ? upd_bytes : pan_bytes;
@@ -242,6 +275,20 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
   __shared__ int s_cur;
   __shared__ __align__(8) uint64_t full[8], empty[8];
   constexpr bool V2 = dag_v2<NB>();
+  constexpr bool C2PF = dag_c2pf<NB, KW>();
+  __shared__ __align__(8) uint64_t c2bar, c2free;  // C2 staging: data landed / every warp done reading
+  __shared__ int s_c2item;                          // item whose C2 slab is staged (-1: none)
+  uint32_t c2par = 0;   // all threads: phase of c2bar for the next staged slab
+  uint32_t c2fpar = 0;  // thread 0: phase of c2free for the running update item
+  if constexpr (C2PF) {
+    if (threadIdx.x == 0) {
+      v2::mbar_init(&c2bar, 1);
+      v2::mbar_init(&c2free, W);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      s_c2item = -1;
+    }
+    __syncthreads();
+  }
   int nxt = -1;   // thread 0: item claimed ahead (-1: none)
   int slot = 0;   // descriptor slot of the running item (all threads)
   auto fetch_desc = [&](int i, int sl) {
@@ -326,12 +373,47 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         if (n.kind == kSsrfb || n.kind == kLarfb || (MODE == kModeTree && n.kind == kTtmqr)) {
           constexpr uint32_t tb = NB * NB * sizeof(double);
           const bool two = n.kind != kLarfb;
-          prefetch_l2(n.p[two ? 3 : 2], tb);
+          bool staged = false;
+          if constexpr (C2PF) {
+            // the next item's inputs already final? (no spin: else it loads C2 from L2 itself)
+            int got[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d)  // all three in flight at once
+              got[d] = d >= n.ndep ? 0 : n.need[d] < 0 ? ld_acquire_sys(done + n.dep[d]) : ld_acquire(done + n.dep[d]);
+            bool ready = n.aux[0] > n.col0;
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+              ready = ready && (d >= n.ndep || got[d] >= (n.need[d] < 0 ? -n.need[d] : n.need[d]));
+            if (ready) {
+              // every warp of THIS item has read its slab from the staging buffer
+              v2::mbar_wait(&c2free, c2fpar);
+              const int ncol = min(dag_warps(NB) * 8 * dag_mb(NB), NB - n.col0);
+              const uint32_t bytes = (uint32_t)(ncol * NB * sizeof(double));
+              v2::fence_proxy_async();  // generic-proxy acquire before the async-proxy read
+              v2::mbar_expect_tx(&c2bar, bytes);
+              v2::bulk_g2s(smem + DagSmem<NB, KW>::c2_off / sizeof(double),
+                           n.p[two ? 3 : 2] + (size_t)n.col0 * NB, bytes, &c2bar);
+              staged = true;
+            }
+            s_c2item = staged ? nxt : -1;
+          }
+          if (!staged) prefetch_l2(n.p[two ? 3 : 2], tb);
           if (two) prefetch_l2(n.p[2], tb);
           if constexpr (V2) prefetch_l2(n.pk, (uint32_t)v2::Pk<NB, (NB % KW == 0 ? KW : 8)>::TOTAL * 8);
         }
       }
 #endif
+    };
+    // C2 staging of this item (if the previous item's last panel staged it)
+    const bool c2_here = C2PF && s_c2item == i;
+    auto c2_src = [&]() -> const double* {
+      return c2_here ? smem + DagSmem<NB, KW>::c2_off / sizeof(double) : nullptr;
+    };
+    auto c2_done = [&]() {  // after an update item: phases of the two staging barriers
+      if constexpr (C2PF) {
+        if (c2_here) c2par ^= 1u;
+        if (threadIdx.x == 0) c2fpar ^= 1u;
+      }
     };
     switch (it.kind) {
       case kGeqrt:  // inner panels [col0 & 0xffff, col0 >> 16)
@@ -346,11 +428,14 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         break;
       case kLarfb:  // columns [col0, min(col0 + slab, aux[0])): the rest of the tile is padding
         if (it.aux[0] <= it.col0) break;
-        if constexpr (V2)
+        if constexpr (V2) {
           v2::update_v2_body<NB, KW, MB, true, W, S>(it.pk, smem, full, empty, nullptr, it.p[2], it.col0, hook,
-                                                     it.aux[0]);
-        else upd::update_body<NB, MB, KW, true, true, false, W>(IB, KW, it.aux[0], it.p[0], it.p[1], nullptr,
-                                                                     it.p[2], 1, it.col0, smem);
+                                                     it.aux[0], c2_src(), &c2bar, c2par, C2PF ? &c2free : nullptr);
+          c2_done();
+        } else {
+          upd::update_body<NB, MB, KW, true, true, false, W>(IB, KW, it.aux[0], it.p[0], it.p[1], nullptr,
+                                                             it.p[2], 1, it.col0, smem);
+        }
         break;
       case kLoad:
         if constexpr (MODE == kModeIO) load_body<NB>(io, it.aux[0], it.aux[1], it.aux[2], it.aux[3]);
@@ -370,17 +455,23 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       case kTtmqr:  // tree variant: TTMQRT column slab
         if constexpr (MODE == kModeTree && V2) {
           if (it.aux[0] <= it.col0) break;
-          v2::update_v2_body<NB, KW, MB, false, W, S, decltype(hook), true>(it.pk, smem, full, empty, it.p[2],
-                                                                            it.p[3], it.col0, hook, it.aux[0]);
+          v2::update_v2_body<NB, KW, MB, false, W, S, decltype(hook), true>(
+              it.pk, smem, full, empty, it.p[2], it.p[3], it.col0, hook, it.aux[0], c2_src(), &c2bar, c2par,
+              C2PF ? &c2free : nullptr);
+          c2_done();
         }
         break;
       default:  // SSRFB: columns as LARFB
         if (it.aux[0] <= it.col0) break;
-        if constexpr (V2)
+        if constexpr (V2) {
           v2::update_v2_body<NB, KW, MB, false, W, S>(it.pk, smem, full, empty, it.p[2], it.p[3], it.col0,
-                                                      hook, it.aux[0]);
-        else upd::update_body<NB, MB, KW, true, false, false, W>(IB, KW, it.aux[0], it.p[0], it.p[1], it.p[2],
-                                                                      it.p[3], 1, it.col0, smem);
+                                                      hook, it.aux[0], c2_src(), &c2bar, c2par,
+                                                      C2PF ? &c2free : nullptr);
+          c2_done();
+        } else {
+          upd::update_body<NB, MB, KW, true, false, false, W>(IB, KW, it.aux[0], it.p[0], it.p[1], it.p[2],
+                                                              it.p[3], 1, it.col0, smem);
+        }
         break;
     }
     // every thread orders its generic-proxy shared-memory accesses of this

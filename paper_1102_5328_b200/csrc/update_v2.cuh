@@ -210,10 +210,17 @@ struct NoHook {
 // TT: the TTMQRT of the tree variant: V2 of panel p is zero
 // below row c0 + IB (the packed tile of a TTQRT holds those zeros), so steps A
 // and C skip those row blocks -- half the flops of the SSRFB form.
+//
+// c2s (DAG kernel, nullable): the item's C2 column slab already staged in
+// shared memory by a TMA bulk copy (column-major, ld NB, from column col0),
+// complete when c2bar reaches phase c2par; c2free (nullable) gets one arrival
+// per warp once the warp no longer reads the staging buffer.
 template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook, bool TT = false>
 __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, double* spk, uint64_t* full,
                                                uint64_t* empty, double* __restrict__ C1, double* __restrict__ C2,
-                                               int col0, Hook hook = Hook(), int cend = NB) {
+                                               int col0, Hook hook = Hook(), int cend = NB,
+                                               const double* c2s = nullptr, uint64_t* c2bar = nullptr,
+                                               uint32_t c2par = 0, uint64_t* c2free = nullptr) {
   using P = Pk<NB, IB>;
   using RG = Ring<NB, IB, S>;
   constexpr int RB = NB / 8;
@@ -225,21 +232,41 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
   // idle warp (8*MB*W > NB, or every column from wc0 on is padding: cend,
   // the item's column limit): no CTA barrier follows
   if (wc0 >= cend) {
+    if (c2free && lane == 0) mbar_arrive(c2free);
     for (int p = 0; p < P::NP; ++p) hook(p);
     return;
   }
 
   // ---- C2 slab -> registers: acc[mb][rb][j] = C2(8rb+2t+j, wc0+8mb+g) --------
   double acc[MB][RB][2];
+  if (c2s) {  // staged by the previous item's last panel
+    mbar_wait(c2bar, c2par);
 #pragma unroll
-  for (int mb = 0; mb < MB; ++mb) {
-    const double* src = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
+    for (int mb = 0; mb < MB; ++mb) {
+      const double* src = c2s + 2 * t + (size_t)(wc0 - col0 + 8 * mb + g) * NB;
 #pragma unroll
-    for (int rb = 0; rb < RB; ++rb) {
-      const double2 v = __ldcg(reinterpret_cast<const double2*>(src + 8 * rb));  // streaming: L2 only
-      acc[mb][rb][0] = v.x;
-      acc[mb][rb][1] = v.y;
+      for (int rb = 0; rb < RB; ++rb) {
+        const double2 v = *reinterpret_cast<const double2*>(src + 8 * rb);
+        acc[mb][rb][0] = v.x;
+        acc[mb][rb][1] = v.y;
+      }
     }
+  } else {
+#pragma unroll
+    for (int mb = 0; mb < MB; ++mb) {
+      const double* src = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
+#pragma unroll
+      for (int rb = 0; rb < RB; ++rb) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(src + 8 * rb));  // streaming: L2 only
+        acc[mb][rb][0] = v.x;
+        acc[mb][rb][1] = v.y;
+      }
+    }
+  }
+  if (c2free) {  // done with the staging buffer: the next slab's TMA may overwrite it
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(c2free);
   }
   // C1 rows of panel 0 (SSRFB): c1n[mb][nb][j] = C1(c0 + 8nb+2t+j, col)
   double c1n[MB][NBK][2];
