@@ -491,9 +491,22 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         __threadfence_system();
         atomicAdd_system(reinterpret_cast<int*>(it.p[2]), 1);
       } else {
+#ifdef TILEQR_FENCE_ATOMIC
         __threadfence();
+#endif
       }
+#ifdef TILEQR_FENCE_ATOMIC
       atomicAdd(done + it.task, 1);
+#else
+      if (MODE == kModeIO && it.kind == kStore) {
+        atomicAdd(done + it.task, 1);
+      } else {
+        // release reduction: the item's writes (every thread's, ordered before
+        // this point by the CTA barrier) become visible before the count does;
+        // consumers acquire the counter (ld.acquire.gpu)
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(done + it.task) : "memory");
+      }
+#endif
       if (prof) prof[3 * (size_t)i + 2] = globaltimer();
     }
     slot ^= 1;
