@@ -376,6 +376,17 @@ int tileqr_ttqrt_batched(int NB, int IB, int batch, double* const* R, double* co
  * Errors: -1 M, -2 N, -3 (NB, IB) outside the dataflow set, -5 h_BS NULL. */
 int tileqr_tune_tree(int64_t M, int64_t N, int NB, int IB, int64_t* h_BS, double* h_ms,
                      const char* report_json_path);
+/* Host-only work list of the tree variant's dataflow kernel (its claim
+ * order), for CPU tests of the derived task graph: per item 11 int64 (kind,
+ * a, b, k, n, s, task, ndep, dep0, dep1, dep2) with kind 0 GEQRT(tile a; panel
+ * k), 1 TSQRT(a <- b), 8 TTQRT(a <- b), 2 LARFB(a; column n), 3 SSRFB(a, b;
+ * column n), 9 TTMQRT(a, b; column n); s = panel sub-task (inner panels of
+ * columns [s*sub_cols, (s+1)*sub_cols)) or update slab.  workers: resident
+ * CTAs in the schedule simulation.  *h_count = item count; h_out may be
+ * NULL.  Errors: -1 M, -2 N, -3 NB/IB, -5 BS, -6 workers, -7 sub_cols,
+ * -9 capacity, -10 h_count NULL. */
+int tileqr_tree_plan_items(int64_t M, int64_t N, int NB, int IB, int64_t BS, int workers, int sub_cols,
+                           int64_t* h_out, int64_t cap, int64_t* h_count);
 /* Release the tree variant's cached workspaces. */
 void tileqr_tree_finalize(void);
 

@@ -28,6 +28,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -85,13 +86,24 @@ struct TTask {
   int s;
 };
 
-int build_tree(TreeWS* ws) {
-  const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT), BS = ws->BS;
-  const int NB = ws->NB, IB = ws->IB;
-  const int SC = panel_sub_cols(NB, IB), NS = NB / SC;
-  const int cols = dag::dag_cols(NB), nslab = (NB + cols - 1) / cols;
+// The tree variant's task graph (dependencies by last-writer tracking) and
+// its claim order (list-schedule simulation over `workers` CTAs); host only.
+struct TreePlan {
   std::vector<sched::Task> tk;
   std::vector<TTask> info;
+  std::vector<sched::Slot> order;
+  int SC = 0, NS = 1, cols = 0, nslab = 1;
+  std::function<int(int)> parts;
+};
+
+int build_tree_plan(int64_t MT, int64_t NT, int NB, int IB, int64_t BS, int SC, int workers, TreePlan* out) {
+  const int64_t KT = std::min(MT, NT);
+  const int NS = NB / SC;
+  const int cols = dag::dag_cols(NB), nslab = (NB + cols - 1) / cols;
+  std::vector<sched::Task>& tk = out->tk;
+  std::vector<TTask>& info = out->info;
+  tk.clear();
+  info.clear();
   auto add = [&](int kind, int64_t a, int64_t b, int64_t k, int64_t n, int s, int level,
                  std::initializer_list<int64_t> deps) {
     sched::Task t{kind, (int)k, (int)b, (int)n, level, 0, {0, 0, 0}, s};
@@ -170,9 +182,6 @@ int build_tree(TreeWS* ws) {
     return TILEQR_ERR_ALLOC;
   }
   // claim order: the flat tree's simulation model (api.cu build_dag)
-  int dev = 0;
-  TQ_CUDA(cudaGetDevice(&dev));
-  TQ_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, dev));
   const int cps = dag::dag_ctas_per_sm(NB);
   const double cta_gflops = 220.0 / cps, hand = 5000.0, sPan = cps == 1 ? 1500.0 : 3000.0;
   const double dS = 4.0 * NB * NB * cols / cta_gflops;
@@ -189,12 +198,34 @@ int build_tree(TreeWS* ws) {
       default: return sPan * SC + hand;
     }
   };
-  prm.workers = ws->nsm * cps;
-  std::vector<sched::Slot> order;
-  if (sched::simulate(tk, prm, &order)) {
+  prm.workers = std::max(1, workers);
+  if (sched::simulate(tk, prm, &out->order)) {
     set_error("tileqr_factor_tree: internal error in the DAG schedule simulation");
     return TILEQR_ERR_INTERNAL;
   }
+  out->SC = SC;
+  out->NS = NS;
+  out->cols = cols;
+  out->nslab = nslab;
+  out->parts = prm.parts;
+  return 0;
+}
+
+int build_tree(TreeWS* ws) {
+  const int64_t MT = ws->MT, NT = ws->NT;
+  const int NB = ws->NB, IB = ws->IB;
+  int dev = 0;
+  TQ_CUDA(cudaGetDevice(&dev));
+  TQ_CUDA(cudaDeviceGetAttribute(&ws->nsm, cudaDevAttrMultiProcessorCount, dev));
+  TreePlan pl;
+  int rc = build_tree_plan(MT, NT, NB, IB, ws->BS, panel_sub_cols(NB, IB), ws->nsm * dag::dag_ctas_per_sm(NB), &pl);
+  if (rc) return rc;
+  const std::vector<sched::Task>& tk = pl.tk;
+  const std::vector<TTask>& info = pl.info;
+  const std::vector<sched::Slot>& order = pl.order;
+  const int SC = pl.SC, cols = pl.cols;
+  const int64_t ntask = (int64_t)tk.size();
+  auto parts = pl.parts;
   const size_t tile = (size_t)NB * NB, ttile = (size_t)IB * NB, tsz = (size_t)MT * NT * ttile;
   auto tp = [&](int64_t m, int64_t n) { return ws->tiles + (size_t)(m + n * MT) * tile; };
   auto T1 = [&](int64_t m, int64_t k) { return ws->Tws + (size_t)(m + k * MT) * ttile; };
@@ -211,7 +242,7 @@ int build_tree(TreeWS* ws) {
     it.ndep = t.ndep;
     for (int d = 0; d < t.ndep; ++d) {
       it.dep[d] = t.dep[d];
-      it.need[d] = prm.parts(tk[t.dep[d]].kind);
+      it.need[d] = parts(tk[t.dep[d]].kind);
     }
     const int64_t k = x.k;
     switch (t.kind) {
@@ -549,6 +580,42 @@ int tileqr_tune_tree(int64_t M, int64_t N, int NB, int IB, int64_t* h_BS, double
               (long long)M, (long long)N, NB, IB, rep.c_str(), (long long)best);
       fclose(f);
     }
+  }
+  return 0;
+}
+
+// Host-only work list of the tree variant (claim order), for CPU tests of the
+// task graph: per item 11 int64 (kind, a, b, k, n, s, task, ndep, dep0, dep1,
+// dep2): kind 0 GEQRT(a; k), 1 TSQRT(a <- b; k), 8 TTQRT(a <- b; k), 2 LARFB(a;
+// k, n), 3 SSRFB(a, b; k, n), 9 TTMQRT(a, b; k, n); s = panel sub-task
+// (columns [s*sub_cols, (s+1)*sub_cols)) or update slab; task / deps = task
+// ids.  Errors: -1 M, -2 N, -3 NB/IB, -5 BS, -6 workers, -7 sub_cols, -9
+// capacity, -10 h_count NULL.
+int tileqr_tree_plan_items(int64_t M, int64_t N, int NB, int IB, int64_t BS, int workers, int sub_cols,
+                           int64_t* h_out, int64_t cap, int64_t* h_count) {
+  if (M < 1) return -1;
+  if (N < 1) return -2;
+  if (!valid_nb_ib(NB, IB)) return -3;
+  if (BS < 1) return -5;
+  if (workers < 1) return -6;
+  if (sub_cols < IB || NB % sub_cols || sub_cols % IB) return -7;
+  if (!h_count) return -10;
+  TreePlan pl;
+  int rc = build_tree_plan((M + NB - 1) / NB, (N + NB - 1) / NB, NB, IB, BS, sub_cols, workers, &pl);
+  if (rc) return rc;
+  const int64_t n = (int64_t)pl.order.size();
+  *h_count = n;
+  if (!h_out) return 0;
+  if (cap < 11 * n) return -9;
+  for (int64_t i = 0; i < n; ++i) {
+    const sched::Slot& sl = pl.order[i];
+    const sched::Task& t = pl.tk[sl.task];
+    const TTask& x = pl.info[sl.task];
+    int64_t* o = h_out + 11 * i;
+    o[0] = t.kind; o[1] = x.a; o[2] = x.b; o[3] = x.k; o[4] = x.n;
+    o[5] = (t.kind == dag::kLarfb || t.kind == dag::kSsrfb || t.kind == dag::kTtmqr) ? sl.slab : x.s;
+    o[6] = sl.task; o[7] = t.ndep;
+    for (int d = 0; d < 3; ++d) o[8 + d] = d < t.ndep ? t.dep[d] : -1;
   }
   return 0;
 }

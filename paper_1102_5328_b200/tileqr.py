@@ -76,6 +76,8 @@ _SIGS = {
     "tileqr_ttqrt_batched": ([_i, _i, _i, _p, _p, _p, _p], _i),
     "tileqr_tree_finalize": ([], None),
     "tileqr_tune_tree": ([_i64, _i64, _i, _i, ctypes.POINTER(_i64), _PD, ctypes.c_char_p], _i),
+    "tileqr_tree_plan_items": ([_i64, _i64, _i, _i, _i64, _i, _i, ctypes.POINTER(_i64), _i64,
+                                ctypes.POINTER(_i64)], _i),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -383,6 +385,21 @@ def tune_tree(m: int, n: int, nb: int, ib: int, report_json_path: str | None = N
     _check(_lib.tileqr_tune_tree(m, n, nb, ib, ctypes.byref(bs), ctypes.byref(ms),
                                  report_json_path.encode() if report_json_path else None), "tileqr_tune_tree")
     return bs.value, ms.value
+
+
+def tree_plan_items(m: int, n: int, nb: int, ib: int, bs: int, workers: int, sub_cols: int):
+    """Host-only claim-ordered work list of the tree variant: (kind, a, b, k, n, s, task, deps)."""
+    cnt = _i64()
+    _check(_lib.tileqr_tree_plan_items(m, n, nb, ib, bs, workers, sub_cols, None, 0, ctypes.byref(cnt)),
+           "tileqr_tree_plan_items")
+    out = (_i64 * (11 * max(1, cnt.value)))()
+    _check(_lib.tileqr_tree_plan_items(m, n, nb, ib, bs, workers, sub_cols, out, 11 * cnt.value, ctypes.byref(cnt)),
+           "tileqr_tree_plan_items")
+    rows = []
+    for i in range(cnt.value):
+        r = list(out[11 * i: 11 * i + 11])
+        rows.append((r[0], r[1], r[2], r[3], r[4], r[5], r[6], tuple(r[8:8 + r[7]])))
+    return rows
 
 
 def ttqrt_batched(nb: int, ib: int, R_ptrs, A2_ptrs, T_ptrs, stream=None):
