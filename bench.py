@@ -552,9 +552,25 @@ def verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nlo
         dist.send(T, dst=0)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, src=0)
+    # residual without the single GPU: every rank applies Q^T (its packed reflector slots) to its
+    # pristine columns; ||Q^T A - R||^2 and ||A||^2 summed over ranks (all-reduce)
+    B = torch.empty(max(1, nloc * mt * nb * nb), dtype=torch.float64, device=dev)
+    tq.dist_fill_uniform(n, n, nb, B, seed)
+    a2 = torch.sum(B ** 2) if nloc else torch.zeros((), dtype=torch.float64, device=dev)
+    if nloc:
+        tq.dist_apply_qt_local(n, n, B, nb, ib)
+        r2 = tq.dist_residual_terms(n, n, nb, A, B, rank, world)
+    else:
+        r2 = torch.zeros((), dtype=torch.float64, device=dev)
+    tot = torch.stack([r2, a2]).reshape(2)
+    dist.all_reduce(tot)
+    npad = sum(1 for j in range(n, mt * nb) if j < mt * nb)
+    res = float(torch.sqrt(tot[0]) / (torch.sqrt(tot[1] - npad) * n * 2.0 ** -52))
     return {"bitwise_equal_to_single_gpu": bool(flag.item()),
+            "residual_ratio": res, "residual_ok": res < 10,
             "how": "all ranks' tile columns and T gathered on rank 0 and compared with tileqr_factor of the same "
-                   "matrix on rank 0's GPU"}
+                   "matrix on rank 0's GPU; residual ||Q^T A - R||_F / (||A||_F N eps) from every rank's own "
+                   "reflector slots (tileqr_dist_apply_qt_local), sums of squares all-reduced"}
 
 
 def main():

@@ -320,6 +320,15 @@ int tileqr_dist_plan_items(int64_t M, int64_t N, int NB, int IB, int nranks, int
 int tileqr_dist_factor(int64_t M, int64_t N, double* A_local, int NB, int IB, double* T_local, int* d_info,
                        tileqr_stream_t stream);
 void tileqr_dist_finalize(void);
+/* B <- Q^T B on this rank's local tile columns (layout of A_local, padded as
+ * tileqr_dist_fill_uniform pads) with the Q of the most recent DATAFLOW
+ * tileqr_dist_factor of this (M, N, NB, IB) on this rank: panels k <= n on
+ * local column n, from the packed reflector tiles the rank's slots hold (its
+ * own panels, the pushed ones).  For the P > 1 residual check: Q^T A = R on
+ * every rank's columns, ||Q^T A - R||_F = ||A - QR||_F, sums of squares
+ * all-reduced (bench.py --verify).  Not collective.  Errors: -1 M, -2 N,
+ * -3 B_local NULL, TILEQR_ERR_NOT_INIT without such a factorization. */
+int tileqr_dist_apply_qt_local(int64_t M, int64_t N, double* B_local, int NB, int IB, tileqr_stream_t stream);
 /* The dataflow multi-rank factorization with nranks EMULATED ranks on the
  * current GPU (one process, no NCCL): rank r's local columns in
  * h_A_local[r] / h_T_local[r] (device pointers, layout as above), the

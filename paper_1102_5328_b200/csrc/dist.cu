@@ -596,6 +596,70 @@ int tileqr_dist_factor(int64_t M, int64_t N, double* A_local, int NB, int IB, do
   return 0;
 }
 
+// B <- Q^T B for this rank's local tile columns of an M x N matrix (same
+// layout as A_local), with the Q of the most recent dataflow
+// tileqr_dist_factor of that shape: panels k <= n applied to local column n
+// (LARFB(k, n), then SSRFB(k, m, n) for m ascending), reading the packed
+// reflector tiles this rank's slots hold after the factorization (its own
+// panels and the pushed ones).  Panels k > n act on rows where Q^T a_n is
+// zero and are not applied.  Used for the P > 1 residual check
+// ||Q^T A - R||_F (= ||A - QR||_F): every rank applies Q^T to its pristine
+// columns and compares with its R tiles; the sum of squares is all-reduced.
+int tileqr_dist_apply_qt_local(int64_t M, int64_t N, double* B_local, int NB, int IB, tileqr_stream_t stream) {
+  if (M < 1) return -1;
+  if (N < 1) return -2;
+  if (!g_d.init) {
+    set_error("tileqr_dist_apply_qt_local: tileqr_dist_init not called");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  if (!g_dd.plan || g_dd.M != M || g_dd.N != N || g_dd.NB != NB || g_dd.IB != IB) {
+    set_error("tileqr_dist_apply_qt_local: no dataflow factorization of this shape on this rank");
+    return TILEQR_ERR_NOT_INIT;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const dd::Plan& p = *g_dd.plan;
+  const int P = g_d.nranks, me = g_d.rank;
+  const int64_t MT = p.MT, NT = p.NT, KT = p.KT;
+  const size_t tile = (size_t)NB * NB, pkd = v2_pk_doubles(NB, IB);
+  if (dd::local_cols(NT, P, me) == 0) return 0;
+  if (!B_local) return -3;
+  auto bt = [&](int64_t m, int64_t n) { return (void*)(B_local + (size_t)(m + (n / P) * MT) * tile); };
+  auto sl = [&](int64_t k, int64_t m) { return (void*)(g_dd.slots + (size_t)p.slot(k, m) * pkd); };
+  struct L { bool larfb; size_t off; int cnt; };
+  std::vector<L> seq;
+  std::vector<void*> hp;
+  for (int64_t k = 0; k < KT; ++k) {
+    std::vector<int64_t> cols;
+    for (int64_t n = k; n < NT; ++n)
+      if (p.owner(n) == me) cols.push_back(n);
+    if (cols.empty()) continue;
+    const int c = (int)cols.size();
+    seq.push_back({true, hp.size(), c});  // [Pk | C1 (unused) | C2]
+    for (int64_t n : cols) hp.push_back(sl(k, k));
+    for (int64_t n : cols) hp.push_back(nullptr), (void)n;
+    for (int64_t n : cols) hp.push_back(bt(k, n));
+    for (int64_t m = k + 1; m < MT; ++m) {
+      seq.push_back({false, hp.size(), c});
+      for (int64_t n : cols) hp.push_back(sl(k, m)), (void)n;
+      for (int64_t n : cols) hp.push_back(bt(k, n));
+      for (int64_t n : cols) hp.push_back(bt(m, n));
+    }
+  }
+  void** dp = nullptr;
+  if (int rc = stream_alloc(reinterpret_cast<void**>(&dp), std::max<size_t>(1, hp.size()) * sizeof(void*), s)) return rc;
+  TQ_CUDA(cudaMemcpyAsync(dp, hp.data(), hp.size() * sizeof(void*), cudaMemcpyHostToDevice, s));
+  TQ_CUDA(cudaStreamSynchronize(s));  // hp is a host temporary
+  int rc = 0;
+  double** d = reinterpret_cast<double**>(dp);
+  for (const L& l : seq) {
+    rc = launch_update_pk(l.larfb, NB, IB, l.cnt, (const double* const*)(d + l.off), d + l.off + l.cnt,
+                          d + l.off + 2 * l.cnt, s);
+    if (rc) break;
+  }
+  cudaFreeAsync(dp, s);
+  return rc;
+}
+
 void tileqr_dist_finalize(void) {
   if (!g_d.init) return;
   cudaDeviceSynchronize();

@@ -57,6 +57,7 @@ _SIGS = {
     "tileqr_dist_fill_uniform": ([_i64, _i64, _i, _p, _u64, _p], _i),
     "tileqr_dist_factor": ([_i64, _i64, _p, _i, _i, _p, _p, _p], _i),
     "tileqr_dist_emulate": ([_i, _i64, _i64, _p, _i, _i, _p, _p, _p], _i),
+    "tileqr_dist_apply_qt_local": ([_i64, _i64, _p, _i, _i, _p], _i),
     "tileqr_dist_plan_items": ([_i64, _i64, _i, _i, _i, _i, _i, _i, ctypes.POINTER(_i64), _i64,
                                 ctypes.POINTER(_i64)], _i),
     "tileqr_dist_plan_level": ([_i64, _i, _i, _i64, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)], _i),
@@ -437,6 +438,32 @@ def dist_factor(m: int, n: int, A_local: torch.Tensor, nb: int, ib: int, T_local
     _check(_lib.tileqr_dist_factor(m, n, A_local.data_ptr(), nb, ib, T_local.data_ptr(),
                                    info.data_ptr() if info is not None else None, _stream(stream)),
            "tileqr_dist_factor")
+
+
+def dist_apply_qt_local(m: int, n: int, B_local: torch.Tensor, nb: int, ib: int, stream=None):
+    """B <- Q^T B on this rank's local tile columns (after a dataflow dist_factor of the shape)."""
+    _check(_lib.tileqr_dist_apply_qt_local(m, n, B_local.data_ptr(), nb, ib, _stream(stream)),
+           "tileqr_dist_apply_qt_local")
+
+
+def dist_residual_terms(m: int, n: int, nb: int, A_fact: torch.Tensor, QtA: torch.Tensor, rank: int,
+                        nranks: int):
+    """(||Q^T A - R||^2, ||A||^2-part) on this rank's local columns: R tile (i, j) is the whole tile
+    above the diagonal tile, its upper triangle on it, zero below (the V tiles)."""
+    mt = -(-m // nb)
+    a = A_fact.view(-1, mt, nb, nb)      # [local col][tile row][jl][il]
+    q = QtA.view(-1, mt, nb, nb)
+    tot = torch.zeros((), dtype=torch.float64, device=A_fact.device)
+    for j in range(a.shape[0]):
+        c = rank + j * nranks
+        for i in range(mt):
+            r = a[j, i].t()
+            if i == c:
+                r = torch.triu(r)
+            elif i > c:
+                r = torch.zeros_like(r)
+            tot += torch.sum((q[j, i].t() - r) ** 2)
+    return tot
 
 
 def dist_emulate(nranks: int, m: int, n: int, A_locals, nb: int, ib: int, T_locals,

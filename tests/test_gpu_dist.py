@@ -174,3 +174,25 @@ def test_tune_step2_through_dist_factor(tq, tmp_path, monkeypatch):
     report = json.load(open(path))
     assert report["ngpus"] == 1
     replay(report, 2, True, nb, ib)
+
+
+@pytest.mark.parametrize("m,n,nb,ib", [(640, 640, 128, 16), (900, 500, 64, 16), (500, 800, 96, 32)])
+def test_dist_residual_via_apply_qt_local(tq, m, n, nb, ib):
+    """The P > 1 residual check (bench.py --verify) at world size 1: Q^T A from
+    the rank's own packed reflector slots equals the factor's R tiles, and
+    ||Q^T A - R||_F / (||A||_F N eps) < 10 (north_star)."""
+    import math
+    mt = -(-m // nb)
+    nloc = tq.dist_local_cols(n, nb)
+    A = torch.empty(nloc * mt * nb * nb, dtype=torch.float64, device="cuda")
+    tq.dist_fill_uniform(m, n, nb, A, seed=9)
+    A0 = A.clone()
+    T = torch.empty(nloc * mt * ib * nb, dtype=torch.float64, device="cuda")
+    tq.dist_factor(m, n, A, nb, ib, T)
+    B = A0.clone()
+    tq.dist_apply_qt_local(m, n, B, nb, ib)
+    torch.cuda.synchronize()
+    res2 = float(tq.dist_residual_terms(m, n, nb, A, B, 0, 1))
+    npad = sum(1 for j in range(n, nloc * nb) if m <= j < mt * nb)   # identity entries of the padding
+    a2 = float(torch.sum(A0 ** 2)) - npad
+    assert math.sqrt(res2) / (math.sqrt(a2) * max(m, n) * 2.0 ** -52) < 10
