@@ -18,7 +18,9 @@
  *     library never synchronizes the stream except where stated (tune).
  *   - The caller owns A, T, B and every batched operand; the library owns a
  *     workspace (padded tile buffer, task lists, CUDA graphs, NCCL comm)
- *     cached per (device, shape) and released by tileqr_finalize().
+ *     cached per (device, shape) -- at most TILEQR_WS_CACHE shapes (default
+ *     4; the least recently used is freed after its last use) -- and released
+ *     by tileqr_finalize().
  *   - Return value: 0 = success; -i = the i-th argument is illegal (LAPACK
  *     xerbla style, nothing is launched); > 0 = TILEQR_ERR_* (message from
  *     tileqr_last_error()).  NB must satisfy 1 <= NB <= 512 (the paper bounds

@@ -223,6 +223,7 @@ struct FactorWS {
   // touching it, whatever stream or host thread that call came from.
   cudaEvent_t last_use = nullptr;
   bool used = false;
+  uint64_t stamp = 0;  // LRU
   // kernel timing (tileqr_set_kernel_timing): one event pair per launch
   struct Rec { int kind; int64_t tasks; int64_t level; cudaEvent_t a, b; };
   int64_t cur_level = 0;
@@ -252,6 +253,23 @@ struct FactorWS {
 
 static std::mutex g_mu;
 static std::map<std::tuple<int, int64_t, int64_t, int, int>, std::unique_ptr<FactorWS>> g_ws;
+static uint64_t g_ws_clock = 0;  // LRU stamps of the cached workspaces
+
+// Cap on cached factorization workspaces (each is the padded tile buffer, T,
+// the packed reflector tiles and the DAG lists: ~3.4 GB at 10000^2): the
+// least recently used one is freed (after its last use completes) when a new
+// shape would exceed TILEQR_WS_CACHE (default 4).  Call with g_mu held.
+static void evict_workspaces() {
+  size_t cap = 4;
+  if (const char* e = getenv("TILEQR_WS_CACHE")) cap = std::max(1, atoi(e));
+  while (g_ws.size() >= cap) {
+    auto lru = g_ws.begin();
+    for (auto it = g_ws.begin(); it != g_ws.end(); ++it)
+      if (it->second->stamp < lru->second->stamp) lru = it;
+    if (lru->second->used) cudaEventSynchronize(lru->second->last_use);
+    g_ws.erase(lru);
+  }
+}
 
 static int g_timing = 0;  // bit k: time launches of kernel kind k
 
@@ -716,6 +734,7 @@ static int create_ws(int dev, int64_t M, int64_t N, int NB, int IB, FactorWS** o
     if (rc) return rc;
   }
   *out = ws.get();
+  evict_workspaces();
   g_ws[std::make_tuple(dev, M, N, NB, IB)] = std::move(ws);
   return 0;
 }
@@ -1094,6 +1113,7 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
     if (rc) return rc;
   }
   if (ws->used) TQ_CUDA(cudaStreamWaitEvent(s, ws->last_use, 0));  // previous user of the workspace
+  ws->stamp = ++g_ws_clock;
   int rc = launch_layout_to_tiles(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, d_info, s);
   if (rc) return rc;
   if ((rc = run_levels(ws, s))) return rc;
@@ -1139,6 +1159,7 @@ int tileqr_factor_host(int64_t M, int64_t N, const double* h_A, int64_t lda, int
     if (rc) return rc;
   }
   if (ws->used) TQ_CUDA(cudaStreamWaitEvent(s, ws->last_use, 0));  // previous user of the workspace
+  ws->stamp = ++g_ws_clock;
   if (ws->use_dag) {
     const int rc = factor_host_dag(ws, h_A, lda, h_R, ldr, h_T, d_info, s);
     if (rc) return rc;

@@ -315,6 +315,13 @@ int get_ws(int64_t M, int64_t N, int NB, int IB, int64_t BS, TreeWS** out) {
   int rc = build_tree(ws.get());
   if (rc) return rc;
   *out = ws.get();
+  size_t cap = 4;  // cached shapes, as tileqr_factor (TILEQR_WS_CACHE)
+  if (const char* e = getenv("TILEQR_WS_CACHE")) cap = std::max(1, atoi(e));
+  while (g_tree.size() >= cap) {  // drop the oldest entry after its last use
+    auto it = g_tree.begin();
+    if (it->second->used) cudaEventSynchronize(it->second->last_use);
+    g_tree.erase(it);
+  }
   g_tree[key] = std::move(ws);
   return 0;
 }

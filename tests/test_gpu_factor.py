@@ -272,3 +272,21 @@ def test_factor_host_flags_nonfinite(tq):
     _, _, info = tq.factor_host(hA, 512, 512, 128, 16)
     torch.cuda.synchronize()
     assert int(info.item()) == 1
+
+
+def test_workspace_cache_is_bounded(tq, monkeypatch):
+    """At most TILEQR_WS_CACHE shapes stay cached (LRU); an evicted shape is
+    rebuilt on its next call and still gives the same bits."""
+    monkeypatch.setenv("TILEQR_WS_CACHE", "2")
+    tq.finalize()
+    shapes = [(256, 256), (320, 320), (384, 384)]
+    first = {}
+    for _ in range(2):
+        for m, n in shapes:
+            a = si.uniform(m, n, 90 + m)
+            A, T, _ = gpu_factor(tq, a, 64, 16)
+            if (m, n) in first:
+                assert torch.equal(A, first[(m, n)][0]) and torch.equal(T, first[(m, n)][1])
+            else:
+                first[(m, n)] = (A, T)
+    tq.finalize()

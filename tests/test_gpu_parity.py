@@ -298,3 +298,43 @@ def test_concurrent_same_shape_calls_on_two_streams(tq):
         torch.cuda.synchronize()
         assert torch.equal(A, ref_a) and torch.equal(T1, Ta)
         assert torch.equal(B, ref_b) and torch.equal(T2, Tb)
+
+
+@pytest.mark.slow
+def test_config4_size_on_one_gpu(tq):
+    """BASELINE.json configs[4]'s matrix (40000^2, 12.8 GB) on ONE B200 -- the
+    maximum size: the first block row of R and panel 0 (V, T) against the
+    oracle (kmax=1, ~0.8 TFLOP on the host cores), residual and orthogonality
+    on random vectors (properties that hold at any size)."""
+    n = 40000
+    nb, ib, _ = tq.lookup(n, n, 1)
+    A = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    tq.rng_uniform(A, n, n, seed=5)
+    A0 = A.clone()
+    T, info = tq.factor(A, n, n, nb, ib)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    # the oracle's first panel on the same matrix (column-major storage -> numpy matrix)
+    a = A0.cpu().numpy().T
+    fo, to, _ = oracle.tileqr_factor(a, nb, ib, kmax=1)
+    f_row = A[:, :nb].cpu().numpy().T
+    assert nrel(f_row, fo[:nb, :]) < 1e-10
+    f_col = A[:nb, :].cpu().numpy().T
+    assert nrel(f_col, fo[:, :nb]) < 1e-10
+    mt = -(-n // nb)
+    assert nrel(T[: mt * ib * nb].cpu().numpy(), to[: mt * ib * nb]) < 1e-10
+    del a, fo, to, f_row, f_col
+    x = torch.from_numpy(si.uniform(n, 4, 42)).cuda()
+    Rx = torch.triu(A.t()) @ x
+    QRx = Rx.t().contiguous()
+    tq.apply_qt("N", A, n, n, T, nb, ib, QRx, 4)
+    Ax = A0.t() @ x
+    torch.cuda.synchronize()
+    res = torch.linalg.norm(Ax - QRx.t()) / (torch.linalg.norm(A0) * torch.linalg.norm(x) * n * EPS)
+    assert float(res) < 10
+    y = tq.to_colmajor(si.uniform(n, 4, 43))
+    y0 = y.clone()
+    tq.apply_qt("N", A, n, n, T, nb, ib, y, 4)
+    tq.apply_qt("T", A, n, n, T, nb, ib, y, 4)
+    torch.cuda.synchronize()
+    assert float(torch.linalg.norm(y - y0) / (torch.linalg.norm(y0) * n * EPS)) < 10
