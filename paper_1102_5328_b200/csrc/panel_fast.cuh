@@ -85,7 +85,14 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
   // issues RW/HL instead of RW shuffles and FMAs per warp; their partial dots
   // are combined with shfl_xor (symmetric: every lane of a column gets the
   // same bits).  GEQRT keeps one column per lane (its top-row slots).
+#ifdef TILEQR_GEQRT_HL1  // diagnostic: GEQRT with one column per lane (round 1)
   constexpr int HL = (TS && IB <= 16 && 32 % IB == 0) ? 32 / IB : 1;
+#else
+  // GEQRT too (round 2): at 2048^2 GEQRT sub-tasks were 62 % of the critical
+  // path (tools/critical_path.py) with half the lanes idle at IB = 16; the
+  // top-row slots (rows leaving the reflector) live in lane group 0 only
+  constexpr int HL = (IB <= 16 && 32 % IB == 0) ? 32 / IB : 1;
+#endif
   constexpr int RL = RW / HL;      // rows per lane
   FastSmem<NB, kWarps>& S = *reinterpret_cast<FastSmem<NB, kWarps>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -284,7 +291,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q] * mlt);
       if (!TS) {
 #pragma unroll
-        for (int t = 0; t < TR; ++t) top[t] = fma(coef, vt[t], top[t] * mlt);
+        for (int t = 0; t < TR; ++t) top[t] = hg == 0 ? fma(coef, vt[t], top[t] * mlt) : 0.0;
       }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
       if (warp == 0 && hg == 0 && col >= jj && col < IB) S.Rout[jj * LDR + col] = (col == jj) ? beta : rjl - tw;
