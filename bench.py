@@ -283,7 +283,7 @@ def run_tileqr(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    if world > 1 or args.force_dist:
         return run_tileqr_dist(args, rank, world, local_rank)
     wl = WORKLOADS[args.workload if args.workload is not None else 3]
     m, n, seed = wl["M"], wl["N"], wl["seed"]
@@ -438,6 +438,11 @@ def run_tileqr_dist(args, rank, world, local_rank):
     from paper_1102_5328_b200 import tileqr as tq
 
     dev = torch.device("cuda", local_rank)
+    if world == 1:  # --force-dist without torchrun
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
     dist.init_process_group("nccl", device_id=dev)
     wl = WORKLOADS[args.workload if args.workload is not None else 4]
     n, seed = wl["N"], wl["seed"]
@@ -487,7 +492,8 @@ def run_tileqr_dist(args, rank, world, local_rank):
         for t in range(3 * mt - 2):
             panel, _, upd = tq.dist_plan_level(mt, world, rank, t)
             launches += len({q[0] for q in panel}) + len({q[0] for q in upd})
-    verify = verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nloc) if args.verify else None
+    verify = verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nloc, dataflow) \
+        if args.verify else None
     if rank == 0:
         line = {"metric": "tile-QR FP64 GFLOP/s", "value": round(value, 2), "unit": "GFLOP/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -509,7 +515,7 @@ def run_tileqr_dist(args, rank, world, local_rank):
     dist.destroy_process_group()
 
 
-def verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nloc):
+def verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nloc, dataflow=True):
     """P>1 verification: every rank's factored tile columns and T tiles are
     sent to rank 0, which factors the same matrix on its own GPU with
     tileqr_factor and compares BITWISE (the distributed result must be
@@ -552,6 +558,10 @@ def verify_dist(tq, dist, args, rank, world, dev, n, nb, ib, seed, A, T, mt, nlo
         dist.send(T, dst=0)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, src=0)
+    if not dataflow:  # the level-synchronous baseline keeps no reflector slots to apply Q^T from
+        return {"bitwise_equal_to_single_gpu": bool(flag.item()), "residual_ratio": None,
+                "how": "all ranks' tile columns and T gathered on rank 0 and compared with tileqr_factor of the "
+                       "same matrix on rank 0's GPU"}
     # residual without the single GPU: every rank applies Q^T (its packed reflector slots) to its
     # pristine columns; ||Q^T A - R||^2 and ||A||^2 summed over ranks (all-reduce)
     B = torch.empty(max(1, nloc * mt * nb * nb), dtype=torch.float64, device=dev)
@@ -585,6 +595,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--verify", action="store_true", help="N>1: bitwise check against a 1-GPU tileqr_factor")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU path even at world size 1 (exercises its code on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "tileqr":
         ap.error("--warmup must be >= 3")
