@@ -80,11 +80,11 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
   constexpr int kThreads = kWarps * 32;
   constexpr int RW = NB / kWarps;  // rows per warp in the factorization
   constexpr int RB = NB / 8;       // 8-row blocks in the trailing update
-  // TSQRT with IB <= 16: HL lane groups of IB lanes share a column (group h
-  // holds rows [w*RW + h*RL, w*RW + (h+1)*RL)), so no lane idles and the step
-  // issues RW/HL instead of RW shuffles and FMAs per warp; their partial dots
-  // are combined with shfl_xor (symmetric: every lane of a column gets the
-  // same bits).  GEQRT keeps one column per lane (its top-row slots).
+  // IB <= 16: HL lane groups of IB lanes share a column (group h holds rows
+  // [w*RW + h*RL, w*RW + (h+1)*RL)), so no lane idles and the step issues
+  // RW/HL instead of RW shuffles and FMAs per warp; their partial dots are
+  // combined with shfl_xor (symmetric: every lane of a column gets the same
+  // bits).  GEQRT's top-row slots live in group 0.
 #ifdef TILEQR_GEQRT_HL1  // diagnostic: GEQRT with one column per lane (round 1)
   constexpr int HL = (TS && IB <= 16 && 32 % IB == 0) ? 32 / IB : 1;
 #else
