@@ -258,24 +258,33 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         // reciprocal: with s = alpha^2 + sigma, rs = 1/sqrt(s), nrm = s*rs,
         //   beta = -sgn(alpha) nrm,  tau = (beta - alpha)/beta = 1 + |alpha| rs,
         //   scal = 1/(alpha - beta) = sgn(alpha) / (|alpha| + nrm).
-        // Branch-free Newton refinement (s > 0 and O(1) data: no special cases).
+        // Branch-free refinement (s > 0 and O(1) data: no special cases).
         const double s2 = fma(alpha, alpha, sigma);
-        double rs;
-        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(s2));
-        const double hs = -0.5 * s2;
-        rs = rs * fma(hs, rs * rs, 1.5);
-        rs = rs * fma(hs, rs * rs, 1.5);
-        const double nrm = s2 * rs;
         const double aa = fabs(alpha);
         const double sg = (alpha >= 0.0) ? 1.0 : -1.0;
+        // One higher-order step each (round 1: two Newton steps each; the
+        // shorter dependent chain gives -2.5 % at 2048^2, same-box A/B in
+        // profiles/r02y_panel_step_ab.log): with y ~ 1/sqrt(s), r = 1 - s y^2,
+        //   1/sqrt(s) = y (1 - r)^(-1/2) = y (1 + q),  q = r/2 + 3r^2/8,
+        // and sqrt(s) = (s y)(1 + q) from the same q; with c ~ 1/den,
+        // e = 1 - den c: 1/den = c (1 + e + e^2).  The approximations' measured
+        // relative error is 2^-20 on sm_100a (tools/approx_err.cu, 2^26
+        // log-uniform inputs), so |r| <~ 2^-19 and the truncation errors
+        // 5 r^3 / 16 and e^3 stay below 2^-58, under the rounding of the
+        // steps themselves.
+        double y, c;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s2));
+        const double n0 = s2 * y;
+        const double r = fma(-s2, y * y, 1.0);
+        const double q = r * fma(0.375, r, 0.5);
+        const double rs = fma(y, q, y);
+        const double nrm = fma(n0, q, n0);
         beta = -sg * nrm;
         tau = fma(aa, rs, 1.0);
         const double den = aa + nrm;
-        double rc;
-        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rc) : "d"(den));
-        rc = fma(rc, fma(-den, rc, 1.0), rc);
-        rc = fma(rc, fma(-den, rc, 1.0), rc);
-        scal = sg * rc;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(c) : "d"(den));
+        const double e = fma(-den, c, 1.0), sc = sg * c;
+        scal = fma(sc, fma(e, e, e), sc);
       }
       const double w = fma(scal, d, rjl);
       const double tw = col < IB ? tau * w : 0.0;
@@ -285,7 +294,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       // (Round 1 folded the pivot lane into one fma with coef = scal - 1; the
       // rounding of scal - 1 costs |scal|^-1 ulps, i.e. all of v2 once the
       // column norm reaches ~2^50 -- tests/test_gpu_parity.py scaled inputs.)
-      const double coef = (col > jj) ? -tw * scal : 0.0;
+      const double coef = (col > jj && col < IB) ? -(tau * scal) * w : 0.0;  // tau*scal beside w
       const double mlt = (col == jj) ? scal : 1.0;
 #pragma unroll
       for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q] * mlt);

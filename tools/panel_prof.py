@@ -13,12 +13,13 @@ f = tq._lib.tileqr_debug_panel_prof
 f.argtypes = [ctypes.c_void_p, ctypes.c_int]
 out = (ctypes.c_ulonglong * 16)()
 names = {0: "stage", 1: "factor", 2: "writeV", 5: "gram", 6: "Tdiag", 7: "Tmerge", 3: "Twrite+pack", 4: "trailing"}
-for nb, ib in [(128, 16), (128, 32), (64, 16)]:
+for nb, ib in [(128, 16), (64, 16), (64, 32)]:
     for kind in ("tsqrt", "geqrt"):
         f(out, 1)
         r = time_panel(nb, ib, reps=20, kind=kind)
         f(out, 1)
         reps = 21
-        ph = {v: round(out[k] / reps) for k, v in names.items()}
+        off = 0 if kind == "tsqrt" else 8  # GEQRT phases are counted at index 8 + k
+        ph = {v: round(out[off + k] / reps) for k, v in names.items()}
         ph["total"] = sum(ph.values())
         print(r, ph, flush=True)
