@@ -111,6 +111,18 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #define TQ_PHASE(k) do { } while (0)
 #endif
   const bool fuse = cend - cbeg > IB && cend - cbeg <= 32 && 32 % IB == 0;  // see step 3
+  // Panel element idx (of NB * IB) in the order the stage and write-out loops
+  // use: each warp instruction covers an 8-row x 4-column block, every 4 lanes
+  // one 32-byte sector of a column (coalesced in global memory), every half
+  // warp 16 distinct bank pairs of the swizzled Vs.  (Column-major order, 32
+  // rows of one column per instruction, hit 4 bank pairs: 8-way conflicts.)
+  // GEQRT only: for TSQRT the column-major order measured faster (batched
+  // TSQRT +0.3-1.4 %, 10000^2 at IB = 32 +1.8 %; GEQRT -2 to -7 %,
+  // profiles/r02z_panel_order_ab.log, r02z2_panel_order_geqrt_only_ab.log)
+  auto prow = [](int idx) {
+    return TS ? idx % NB : 8 * ((idx >> 5) % (NB / 8)) + (idx & 3) + ((idx >> 4) & 1) * 4;
+  };
+  auto pcol = [](int idx) { return TS ? idx / NB : 4 * ((idx >> 5) / (NB / 8)) + ((idx >> 2) & 3); };
   for (int c0 = cbeg; c0 < cend; c0 += IB) {
     // ---- stage the panel (coalesced) and, for TSQRT, the R block -------------
     // trailing columns of this inner panel -> L2 while the panel is factored
@@ -134,8 +146,9 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
           // concurrent TSQRT sub-task may be rewriting -- never read them (a
           // stale line could even land in the L1 another CTA of this SM reads
           // after its acquire); their operand entries are 0 anyway
-          v[u] = (idx < NB * IB && (TS || idx % NB >= c0) && (!TT || idx % NB <= c0 + idx / NB))
-                     ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+          const int r = prow(idx), c = pcol(idx);
+          v[u] = (idx < NB * IB && (TS || r >= c0) && (!TT || r <= c0 + c))
+                     ? __ldcg(&B[r + (size_t)(c0 + c) * NB]) : 0.0;
         }
         double rv[UR];
         if (TS && idx0 == tid) {
@@ -148,7 +161,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
         for (int u = 0; u < UV; ++u) {
           const int idx = idx0 + u * kThreads;
-          if (idx < NB * IB) S.Vs[vsw(idx % NB, idx / NB, LDV)] = v[u];
+          if (idx < NB * IB) S.Vs[vsw(prow(idx), pcol(idx), LDV)] = v[u];
         }
         if (TS && idx0 == tid) {
 #pragma unroll
@@ -165,13 +178,14 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int idx = idx0 + u * kThreads;
-          v[u] = (idx < NB * IB && (TS || idx % NB >= c0) && (!TT || idx % NB <= c0 + idx / NB))
-                     ? __ldcg(&B[(idx % NB) + (size_t)(c0 + idx / NB) * NB]) : 0.0;
+          const int r = prow(idx), c = pcol(idx);
+          v[u] = (idx < NB * IB && (TS || r >= c0) && (!TT || r <= c0 + c))
+                     ? __ldcg(&B[r + (size_t)(c0 + c) * NB]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int idx = idx0 + u * kThreads;
-          if (idx < NB * IB) S.Vs[vsw(idx % NB, idx / NB, LDV)] = v[u];
+          if (idx < NB * IB) S.Vs[vsw(prow(idx), pcol(idx), LDV)] = v[u];
         }
       }
       if (TS) {
@@ -336,8 +350,11 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       if ((col < IB || 32 % IB != 0) && (TS || rbase + q >= c0 + IB))
         S.Vs[vsw(rbase + q, col, LDV)] = col < IB ? x[q] : 0.0;
     __syncthreads();  // GEQRT: the top rows were stored as they left the reflector
-    for (int idx = tid; idx < NB * IB; idx += kThreads) {
-      const int c = idx / NB, r = idx - c * NB;
+    // (GEQRT: rows from c0 only -- above it Vs holds the stage's zeros, and
+    // the R rows of earlier inner panels are not this panel's to write)
+    for (int idx = TS ? tid : (c0 / 8) * IB * 8 + tid; idx < NB * IB; idx += kThreads) {
+      const int c = TS ? idx / NB : 4 * ((idx >> 5) % (IB / 4)) + ((idx >> 2) & 3);
+      const int r = TS ? idx % NB : 8 * ((idx >> 5) / (IB / 4)) + (idx & 3) + ((idx >> 4) & 1) * 4;
       double* p = &S.Vs[vsw(r, c, LDV)];
       const double v = *p;
       if (TS) {
