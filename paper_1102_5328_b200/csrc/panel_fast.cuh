@@ -213,6 +213,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       top[t] = (!TS && lane < IB && i < IB) ? S.Vs[vsw(c0 + i, lane, LDV)] : 0.0;
     }
 
+    double myscal = 1.0;  // 1 / (alpha - beta) of the lane's own column, once its step ran
     TQ_PHASE(0);
     // ---- 1. factor the panel column by column --------------------------------
     auto step = [&](const int jj) {
@@ -225,7 +226,9 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         S.rowj[buf][lane] = top[0];
         // columns >= IB: kept panels (step 3), or for IB = 24 the zero padding
         // the packed copy takes
-        if (lane < IB || 32 % IB != 0) S.Vs[vsw(c0 + jj, lane, LDV)] = lane < IB ? top[0] : 0.0;
+        // (lanes < j: V entries, scaled by their column's deferred scal; the
+        // entries from lane j on are R, written from Rout)
+        if (lane < IB || 32 % IB != 0) S.Vs[vsw(c0 + jj, lane, LDV)] = lane < IB ? top[0] * myscal : 0.0;
 #pragma unroll
         for (int t = 0; t + 1 < TR; ++t) top[t] = top[t + 1];
         top[TR - 1] = 0.0;
@@ -302,19 +305,21 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       }
       const double w = fma(scal, d, rjl);
       const double tw = col < IB ? tau * w : 0.0;
-      // select-free rank-1 update of the reflector rows, x = x * m + coef * vj:
-      //   lane == jj: m = scal, coef = 0 (x becomes v2 = x2 * scal, one rounding);
-      //   lane >  jj: m = 1,  coef = -tw * scal;   lane < jj: m = 1, coef = 0.
-      // (Round 1 folded the pivot lane into one fma with coef = scal - 1; the
-      // rounding of scal - 1 costs |scal|^-1 ulps, i.e. all of v2 once the
-      // column norm reaches ~2^50 -- tests/test_gpu_parity.py scaled inputs.)
+      // rank-1 update of the reflector rows, x = x + coef * vj (coef = 0 for
+      // lanes <= jj).  The pivot lane's column becomes v2 = x2 * scal: it is
+      // never read again in this panel, so the scaling is deferred to the
+      // write-out (myscal, one rounding as before: bitwise the same values)
+      // instead of a multiply of every lane's rows in every step.  (Round 1
+      // folded the pivot lane into one fma with coef = scal - 1; the rounding
+      // of scal - 1 costs |scal|^-1 ulps, i.e. all of v2 once the column norm
+      // reaches ~2^50 -- tests/test_gpu_parity.py scaled inputs.)
       const double coef = (col > jj && col < IB) ? -(tau * scal) * w : 0.0;  // tau*scal beside w
-      const double mlt = (col == jj) ? scal : 1.0;
+      myscal = (col == jj) ? scal : myscal;
 #pragma unroll
-      for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q] * mlt);
+      for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q]);
       if (!TS) {
 #pragma unroll
-        for (int t = 0; t < TR; ++t) top[t] = hg == 0 ? fma(coef, vt[t], top[t] * mlt) : 0.0;
+        for (int t = 0; t < TR; ++t) top[t] = hg == 0 ? fma(coef, vt[t], top[t]) : 0.0;
       }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
       if (warp == 0 && hg == 0 && col >= jj && col < IB) S.Rout[jj * LDR + col] = (col == jj) ? beta : rjl - tw;
@@ -348,7 +353,7 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
     for (int q = 0; q < RL; ++q)  // GEQRT: the top rows were stored by the step loop
       if ((col < IB || 32 % IB != 0) && (TS || rbase + q >= c0 + IB))
-        S.Vs[vsw(rbase + q, col, LDV)] = col < IB ? x[q] : 0.0;
+        S.Vs[vsw(rbase + q, col, LDV)] = col < IB ? x[q] * myscal : 0.0;
     __syncthreads();  // GEQRT: the top rows were stored as they left the reflector
     // (GEQRT: rows from c0 only -- above it Vs holds the stage's zeros, and
     // the R rows of earlier inner panels are not this panel's to write)
