@@ -218,6 +218,15 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
     // ---- 1. factor the panel column by column --------------------------------
     auto step = [&](const int jj) {
       const int buf = jj & 1;
+      double vj[RL];
+      double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
+#pragma unroll
+      for (int q = 0; q < RL; ++q) {
+        vj[q] = __shfl_sync(0xffffffffu, x[q], jj + hg * IB);
+        pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
+      }
+      // (after the x rows' shuffles, which do not depend on it: the owner's
+      // stores overlap their latency)
       if (!TS && warp == jj % kWarps) {
         // row j leaves the reflector: its owner publishes it (alpha, R(j, c))
         // and stores its final V entries (lanes < j; the rest is R, written
@@ -232,13 +241,6 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
         for (int t = 0; t + 1 < TR; ++t) top[t] = top[t + 1];
         top[TR - 1] = 0.0;
-      }
-      double vj[RL];
-      double pp[4] = {0.0, 0.0, 0.0, 0.0};  // 4 independent chains
-#pragma unroll
-      for (int q = 0; q < RL; ++q) {
-        vj[q] = __shfl_sync(0xffffffffu, x[q], jj + hg * IB);
-        pp[q & 3] = fma(vj[q], x[q], pp[q & 3]);
       }
       double vt[TR];
       if (!TS) {  // top rows below row j (warp-uniform predicate per slot)
@@ -269,13 +271,12 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
       const double sigma = ps[0], d = pd[0];
       const double alpha = TS ? S.Rin[jj * LDR + jj] : S.rowj[buf][jj];
       const double rjl = TS ? S.Rin[jj * LDR + col] : S.rowj[buf][col];
-      double tau = 0.0, scal = 0.0, beta = alpha;
-      if (sigma != 0.0) {
+      double tau, scal, beta;
+      {  // branch-free: sigma == 0 (R1: tau = 0, v = 0, beta = alpha) is selected at the end
         // Reflector rule (R1) from one reciprocal square root and one
         // reciprocal: with s = alpha^2 + sigma, rs = 1/sqrt(s), nrm = s*rs,
         //   beta = -sgn(alpha) nrm,  tau = (beta - alpha)/beta = 1 + |alpha| rs,
         //   scal = 1/(alpha - beta) = sgn(alpha) / (|alpha| + nrm).
-        // Branch-free refinement (s > 0 and O(1) data: no special cases).
         const double s2 = fma(alpha, alpha, sigma);
         const double aa = fabs(alpha);
         const double sg = (alpha >= 0.0) ? 1.0 : -1.0;
@@ -296,12 +297,13 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
         const double q = r * fma(0.375, r, 0.5);
         const double rs = fma(y, q, y);
         const double nrm = fma(n0, q, n0);
-        beta = -sg * nrm;
-        tau = fma(aa, rs, 1.0);
         const double den = aa + nrm;
         asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(c) : "d"(den));
         const double e = fma(-den, c, 1.0), sc = sg * c;
-        scal = fma(sc, fma(e, e, e), sc);
+        const bool refl = sigma != 0.0;  // (s2 = 0 makes the values above inf / nan: not selected)
+        beta = refl ? -sg * nrm : alpha;
+        tau = refl ? fma(aa, rs, 1.0) : 0.0;
+        scal = refl ? fma(sc, fma(e, e, e), sc) : 0.0;
       }
       const double w = fma(scal, d, rjl);
       const double tw = col < IB ? tau * w : 0.0;
@@ -318,8 +320,9 @@ __device__ __forceinline__ void panel_fast_body(double* const R, double* const B
 #pragma unroll
       for (int q = 0; q < RL; ++q) x[q] = fma(coef, vj[q], x[q]);
       if (!TS) {
+        const double coefT = hg == 0 ? coef : 0.0;
 #pragma unroll
-        for (int t = 0; t < TR; ++t) top[t] = hg == 0 ? fma(coef, vt[t], top[t]) : 0.0;
+        for (int t = 0; t < TR; ++t) top[t] = fma(coefT, vt[t], top[t]);  // (other groups' slots stay 0)
       }
       // row j of R: beta on the diagonal, R(j, c) - tau w_c to its right
       if (warp == 0 && hg == 0 && col >= jj && col < IB) S.Rout[jj * LDR + col] = (col == jj) ? beta : rjl - tw;

@@ -1,6 +1,6 @@
 #!/bin/bash
 # panel A/B: libtileqr.so (working tree) vs libtileqr_prev.so (HEAD)
-OUT=gpurun_out/r02ab
+OUT=gpurun_out/r02ac
 mkdir -p $OUT
 timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kernels.py tests/test_gpu_factor.py tests/test_gpu_tree.py -x -q -p no:cacheprovider -k "not config3 and not config4" > $OUT/t.log 2>&1; echo "rc=$?" >> $OUT/t.log
 for r in 1 2 3; do
