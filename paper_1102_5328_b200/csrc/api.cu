@@ -290,10 +290,13 @@ static bool dag_enabled(int NB, int IB) {
 
 bool dag_path_supported(int NB, int IB) { return dag::dag_supported(NB, IB) && v2_supported(NB, IB); }
 
-// Columns of one GEQRT / TSQRT sub-task (a multiple of IB).
+// Columns of one GEQRT / TSQRT sub-task (a multiple of IB): 16 for NB <= 64,
+// else 32 (same-box sweep of 16 / 32 / 64 / NB, profiles/r02ad_panel_sub_ab.log:
+// at NB = 64 16 columns give 2048^2 -7 %, 1024^2 -8 %, 4096^2 -2 %; at
+// NB = 128 16 columns are neutral at 2048^2 and slower at 4096^2 / 10000^2).
 int panel_sub_cols(int NB, int IB) {
   const char* e = getenv("TILEQR_PANEL_SUB");
-  int sc = e ? atoi(e) : 32;
+  int sc = e ? atoi(e) : (NB <= 64 ? 16 : 32);
   if (sc <= 0 || sc >= NB) sc = NB;
   sc = std::max(IB, sc / IB * IB);
   while (NB % sc) sc += IB;
