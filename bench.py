@@ -200,18 +200,21 @@ def _traffic(key, nb, ib):
     return None
 
 
-def measure_dag(tq, m, n, nb, ib, step, step_ms):
+def measure_dag(tq, m, n, nb, ib, step, step_ms, launch=None):
     """Roofline of the persistent dataflow kernel (the one launch that runs the
     whole DAG): algorithmic flops = the factorization's useful flops
-     per launch / the kernel's duration (CUDA events around
-    the launch on its stream), in one measurement step after the timed region.
-    Per-kind item busy times come from the device clock (globaltimer) in the
-    same step."""
+     per launch / the kernel's average duration over the
+    timed steps (`launch`: CUDA events around every launch, on its stream).
+    Per-kind item busy times come from the device clock (globaltimer) in one
+    traced step after the timed region."""
     tq.set_kernel_timing(True)
     step()
     import torch
     torch.cuda.synchronize()
     dag_ms, slots, _ = tq.kernel_times(m, n, nb, ib, "dag")   # slots = resident CTAs
+    traced_ms = dag_ms
+    if launch:
+        dag_ms = launch[0]
     kinds = {"note": "dataflow kernel: per kind, items, busy ms summed over CTAs (inputs ready -> done), "
                      "one step after the timed region"}
     busy = {}
@@ -225,7 +228,8 @@ def measure_dag(tq, m, n, nb, ib, step, step_ms):
     kinds["ssrfb"]["tflops_while_running"] = round(
         s_tasks * 4.0 * nb ** 3 / (busy["ssrfb"] * 1e-3 / slots) / 1e12, 3) if busy["ssrfb"] else None
     kinds["cta_slots"] = slots
-    kinds["slot_busy_frac"] = round(sum(busy.values()) / (slots * dag_ms), 4) if dag_ms else None
+    kinds["slot_busy_frac"] = round(sum(busy.values()) / (slots * traced_ms), 4) if traced_ms else None
+    kinds["traced_launch_ms"] = round(traced_ms, 4)
     flops = qr_flops(m, n)
     achieved = flops / (dag_ms * 1e-3) / 1e12 if dag_ms > 0 else 0.0
     roofline = {"kernel": "dag_kernel (persistent dataflow: GEQRT/TSQRT/LARFB/SSRFB items)",
@@ -233,8 +237,11 @@ def measure_dag(tq, m, n, nb, ib, step, step_ms):
                 "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": _traffic("dag", nb, ib),
                 "flops_per_launch": flops, "avg_launch_ms": round(dag_ms, 4),
                 "peak_source": FP64_PEAK_SRC, "share_of_step": round(dag_ms / step_ms, 4),
-                "measured": "CUDA events around the single dag_kernel launch (on the caller's stream) in the "
-                            "step right after the timed region; flops = useful 4/3 N^3 (2MN^2-2N^3/3); "
+                "launches_timed": launch[1] if launch else 1,
+                "measured": ("CUDA events around every dag_kernel launch of the timed steps (on the caller's "
+                             "stream), averaged" if launch else
+                             "CUDA events around the dag_kernel launch of one step after the timed region") +
+                            "; flops = useful 4/3 N^3 (2MN^2-2N^3/3); "
                             "traffic = ncu dram read+write bytes of one launch (profiles/ncu_traffic.json)"}
     return roofline, kinds
 
@@ -332,6 +339,11 @@ def run_tileqr(args, rank, world, local_rank):
     free, _ = torch.cuda.mem_get_info(dev)
     staged = args.steps * A0.numel() * 8 < 0.5 * free
     bufs = [A0.clone() for _ in range(args.steps)] if staged else []
+    sched = tq.factor_schedule(nb, ib)
+    live = sched == "dag" and not tree_bs
+    if live:  # CUDA events around every dataflow-kernel launch of the timed steps (no device-clock trace)
+        tq.set_kernel_timing(True, kinds=(), launch_events=True)
+        tq.kernel_times(m, n, nb, ib, "dag_launches")   # reset
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -345,11 +357,15 @@ def run_tileqr(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    launch = None
+    if live:
+        tot, cnt, _ = tq.kernel_times(m, n, nb, ib, "dag_launches")
+        launch = (tot / cnt, cnt) if cnt else None
+        tq.set_kernel_timing(False)
     del bufs
     flops = qr_flops(m, n)
     value = flops / (ms * 1e-3) / 1e9
 
-    sched = tq.factor_schedule(nb, ib)
     if tree_bs:
         sched = f"dag (reduction tree, BS={tree_bs})"
         ach = qr_flops(m, n) / (ms * 1e-3) / 1e12
@@ -360,7 +376,7 @@ def run_tileqr(args, rank, world, local_rank):
                                 "duration)"}
         kinds = None
     elif sched == "dag":
-        roofline, kinds = measure_dag(tq, m, n, nb, ib, step, ms)
+        roofline, kinds = measure_dag(tq, m, n, nb, ib, step, ms, launch)
     else:
         roofline, kinds = measure_levels(tq, m, n, nb, ib, step, ms)
 

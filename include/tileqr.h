@@ -428,7 +428,9 @@ int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out);
 /* Kernel timing for measurement (bench.py): bit k of `mask` (k = 0 GEQRT,
  * 1 TSQRT, 2 LARFB, 3 SSRFB) makes tileqr_factor bracket every batched launch
  * of that kind with CUDA events on the stream it is launched on (captured
- * into the CUDA graph as event-record nodes); 0 turns timing off. */
+ * into the CUDA graph as event-record nodes); 0 turns timing off.  Bit 4:
+ * CUDA events around every dataflow-kernel launch only (no device-clock
+ * trace), accumulated until read with kind 5 below. */
 void tileqr_set_kernel_timing(int mask);
 /* After the stream of a timed tileqr_factor(M, N, NB, IB) completed: sum of
  * the launch durations of kernel kind (0 GEQRT, 1 TSQRT, 2 LARFB, 3 SSRFB) in
@@ -437,7 +439,9 @@ void tileqr_set_kernel_timing(int mask);
  * that kind's work items summed over CTAs (inputs ready -> completion), the
  * number of items and of tasks; kind 4 gives the dataflow kernel's duration
  * (CUDA events around its launch), h_launches = its resident CTAs and
- * h_tasks = the DAG's task count. */
+ * h_tasks = the DAG's task count.  Kind 5 (timing bit 4): the summed
+ * durations and the number of dataflow-kernel launches recorded since the
+ * last kind-5 read (which resets them). */
 int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
                         int64_t* h_launches, int64_t* h_tasks);
 

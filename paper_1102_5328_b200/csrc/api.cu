@@ -20,6 +20,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <numeric>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -208,6 +209,8 @@ struct FactorWS {
   unsigned long long* d_prof = nullptr;  // per-item claim/start/end (tileqr_set_kernel_timing)
   size_t prof_cap = 0;
   cudaEvent_t dag_ev[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> acc_ev;  // timing bit 4: event pairs around every dataflow-kernel launch
+  size_t acc_n = 0;                 // launches recorded since the last read
   bool use_dag = false, dag_timed = false;
   int dag_grid = 0;  // resident CTAs of the last DAG launch
   // host pipeline (tileqr_factor_host): column-major staging, copy streams
@@ -244,6 +247,7 @@ struct FactorWS {
     cudaFree(st_out);
     cudaFree(d_io);
     for (auto e : dag_ev) if (e) cudaEventDestroy(e);
+    for (auto e : acc_ev) if (e) cudaEventDestroy(e);
     for (auto e : io_ev) if (e) cudaEventDestroy(e);
     if (last_use) cudaEventDestroy(last_use);
     if (s_h2d) cudaStreamDestroy(s_h2d);
@@ -317,7 +321,7 @@ int panel_sub_cols(int NB, int IB) {
 // since a task's bottom level exceeds each successor's -- ties by ASAP level,
 // then task id.
 static int build_dag(FactorWS* ws, bool io) {
-  const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT), N = ws->N;
+  const int64_t MT = ws->MT, NT = ws->NT, KT = std::min(MT, NT), N = ws->N, M = ws->M;
   const int NB = ws->NB, IB = ws->IB;
   const int SC = panel_sub_cols(NB, IB), NS = NB / SC;
   std::vector<int64_t> offL(KT + 1), offT(KT + 1), offS(KT + 1);
@@ -506,6 +510,7 @@ static int build_dag(FactorWS* ws, bool io) {
   auto tt = [&](int64_t m, int64_t k) { return Tw + (size_t)(m + k * MT) * IB * NB; };
   auto pkp = [&](int64_t m, int64_t k) { return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr; };
   DagList& L = io ? ws->dag_io : ws->dag_plain;
+  const bool rowlim = !getenv("TILEQR_DAG_NO_ROWLIM");  // diagnostics: SSRFB over the padding rows too
   std::vector<dag::Item> items;
   items.reserve(sched.size());
   L.item_kind.clear();
@@ -550,6 +555,7 @@ static int build_dag(FactorWS* ws, bool io) {
     }
     if (t.kind == dag::kLarfb || t.kind == dag::kSsrfb)  // padded columns (e_j or 0) are invariant
       it.aux[0] = (int)std::min<int64_t>(NB, std::max<int64_t>(0, N - (int64_t)t.n * NB));
+    if (t.kind == dag::kSsrfb && rowlim) it.aux[1] = dag::ssrfb_rows(M, t.m, NB);
     items.push_back(it);
     L.item_kind.push_back((unsigned char)t.kind);
     L.item_level.push_back(t.level);
@@ -579,7 +585,16 @@ static int build_dag(FactorWS* ws, bool io) {
 
 static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStream_t stream) {
   unsigned long long* prof = nullptr;
-  if (g_timing) {
+  const bool acc = (g_timing & 16) != 0;  // launch events only (no device-clock trace)
+  if (acc) {
+    while (ws->acc_ev.size() < 2 * (ws->acc_n + 1)) {
+      cudaEvent_t e;
+      TQ_CUDA(cudaEventCreate(&e));
+      ws->acc_ev.push_back(e);
+    }
+    TQ_CUDA(cudaEventRecord(ws->acc_ev[2 * ws->acc_n], stream));
+  }
+  if (g_timing & 15) {
     if (ws->prof_cap < (size_t)L.nitems) {
       cudaFree(ws->d_prof);
       ws->d_prof = nullptr;
@@ -597,8 +612,9 @@ static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStre
   int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, ws->nsm, prof, stream,
                       &ws->dag_grid, io, io ? dag::kModeIO : dag::kModePlain);
   if (rc) return rc;
-  if (g_timing) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
-  ws->dag_timed = g_timing != 0;
+  if (g_timing & 15) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
+  if (acc) TQ_CUDA(cudaEventRecord(ws->acc_ev[2 * ws->acc_n++ + 1], stream));
+  ws->dag_timed = (g_timing & 15) != 0;
   ws->dag_last = &L;
   return 0;
 }
@@ -1055,6 +1071,30 @@ int panel_prof_read_dag128(unsigned long long* out, int reset);
 }
 using namespace tileqr;
 
+namespace tileqr {
+bool panel_fast_supported(int NB, int IB);  // kernels_panel_fast.cu
+bool panel_wide_supported(int NB, int IB);  // kernels_panel.cu
+
+// Inner blocking the factorization runs at (R23): IB itself when
+// the register-resident panels and the packed DMMA update take it, else
+// lcm(IB, 8) when they take that (IB in {1, 2, 4} -> 8, 3, 6, 12 -> 24, 5,
+// 10, 20 -> 40, 7, 14, 28 -> 56, where it divides NB): the same reflectors
+// (applying the IBe-blocks of a panel in order is applying its IB-blocks in
+// order, R22), with T returned at IB as the diagonal blocks of T at IBe.
+// Else IB (the generic panels and update).  TILEQR_NO_IB_LCM=1: always IB.
+int effective_ib(int NB, int IB) {
+  auto fast = [&](int ib) {
+    return ib <= NB && NB % ib == 0 &&
+           (panel_fast_supported(NB, ib) || (panel_wide_supported(NB, ib) && v2_supported(NB, ib)));
+  };
+  if (fast(IB)) return IB;
+  const char* e = getenv("TILEQR_NO_IB_LCM");
+  if (e && e[0] == '1') return IB;
+  const int l = std::lcm(IB, 8);
+  return (l <= 64 && fast(l)) ? l : IB;
+}
+}  // namespace tileqr
+
 extern "C" {
 
 const char* tileqr_version(void) { return "tileqr 0.1 sm_100a (FP64 DMMA tile QR)"; }
@@ -1106,13 +1146,14 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
   if (M == 0 || N == 0) return 0;
   int dev;
   TQ_CUDA(cudaGetDevice(&dev));
+  const int IBe = effective_ib(NB, IB);
   std::lock_guard<std::mutex> lock(g_mu);
   FactorWS* ws = nullptr;
-  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IBe));
   if (it != g_ws.end()) {
     ws = it->second.get();
   } else {
-    int rc = create_ws(dev, M, N, NB, IB, &ws);
+    int rc = create_ws(dev, M, N, NB, IBe, &ws);
     if (rc) return rc;
   }
   if (ws->used) TQ_CUDA(cudaStreamWaitEvent(s, ws->last_use, 0));  // previous user of the workspace
@@ -1121,8 +1162,12 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
   if (rc) return rc;
   if ((rc = run_levels(ws, s))) return rc;
   if ((rc = launch_tiles_to_layout(M, N, A, lda, NB, ws->MT, ws->NT, ws->tiles, s))) return rc;
-  TQ_CUDA(cudaMemcpyAsync(T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
-                          cudaMemcpyDeviceToDevice, s));
+  if (IBe == IB) {
+    TQ_CUDA(cudaMemcpyAsync(T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
+                            cudaMemcpyDeviceToDevice, s));
+  } else if ((rc = launch_t_extract(ws->Tws, IBe, T, IB, NB, ws->MT * ws->NT, s))) {
+    return rc;
+  }
   TQ_CUDA(cudaEventRecord(ws->last_use, s));
   ws->used = true;
   return 0;
@@ -1287,6 +1332,19 @@ int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double
 // pack (V, T) into stream-ordered scratch, then run update_v2.
 static int packed_update(bool larfb, int NB, int IB, int batch, const double* const* V, const double* const* T,
                          double* const* C1, double* const* C2, cudaStream_t s) {
+  const int IBe = effective_ib(NB, IB);
+  if (IBe != IB) {  // R23: T at IBe from V and tau, then the IBe update
+    double* tb = nullptr;
+    double** tp = nullptr;
+    if (int rc_ = stream_alloc(reinterpret_cast<void**>(&tb), (size_t)batch * IBe * NB * sizeof(double), s)) return rc_;
+    if (int rc_ = stream_alloc(reinterpret_cast<void**>(&tp), (size_t)batch * sizeof(double*), s)) return rc_;
+    int rc = launch_fill_ptrs(tp, tb, (size_t)IBe * NB, batch, s);
+    if (!rc) rc = launch_t_assemble(!larfb, NB, IBe, IB, batch, V, T, tp, s);
+    if (!rc) rc = packed_update(larfb, NB, IBe, batch, V, tp, C1, C2, s);
+    cudaFreeAsync(tb, s);
+    cudaFreeAsync(tp, s);
+    return rc;
+  }
   const size_t pd = v2_pk_doubles(NB, IB);
   double* buf = nullptr;
   double** ptr = nullptr;
@@ -1344,7 +1402,7 @@ int tileqr_larfb_batched(char trans, int NB, int IB, int batch, const double* co
   if (ncols < 1 || ncols > NB) return arg_error(8, fn, "ncols not in [1, NB]");
   const bool tr = trans == 'T' || trans == 't';
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (tr && ncols == NB && v2_supported(NB, IB))  // the factorization's kernel: pack, then update
+  if (tr && ncols == NB && v2_supported(NB, effective_ib(NB, IB)))  // the factorization's kernel: pack, then update
     return packed_update(true, NB, IB, batch, V, T, nullptr, C, s);
   return launch_larfb(tr, NB, IB, batch, V, T, C, ncols, s);
 }
@@ -1366,7 +1424,7 @@ int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* co
   if (ncols < 1 || ncols > NB) return arg_error(9, fn, "ncols not in [1, NB]");
   const bool tr = trans == 'T' || trans == 't';
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (tr && ncols == NB && v2_supported(NB, IB))
+  if (tr && ncols == NB && v2_supported(NB, effective_ib(NB, IB)))
     return packed_update(false, NB, IB, batch, V2, T, C1, C2, s);
   return launch_ssrfb(tr, NB, IB, batch, V2, T, C1, C2, ncols, s);
 }
@@ -1419,7 +1477,7 @@ int tileqr_debug_dag_item(int64_t M, int64_t N, int NB, int IB, int64_t idx, int
   int dev;
   TQ_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_mu);
-  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, effective_ib(NB, IB)));
   if (it == g_ws.end() || !it->second->use_dag) return TILEQR_ERR_NOT_INIT;
   FactorWS* ws = it->second.get();
   const DagList& L = ws->dag_last ? *ws->dag_last : ws->dag_plain;
@@ -1474,18 +1532,18 @@ int tileqr_factor_plan(int64_t M, int64_t N, int NB, int IB, int64_t* h_out) {
 
 void tileqr_set_kernel_timing(int mask) {
   std::lock_guard<std::mutex> lock(g_mu);
-  g_timing = mask & 15;
+  g_timing = mask & 31;
 }
 
 int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* h_total_ms,
                         int64_t* h_launches, int64_t* h_tasks) {
   static const char* fn = "tileqr_kernel_times";
-  if (kind < 0 || kind > 4) return arg_error(5, fn, "kind not in 0..4");
+  if (kind < 0 || kind > 5) return arg_error(5, fn, "kind not in 0..5");
   if (!h_total_ms || !h_launches || !h_tasks) return arg_error(6, fn, "NULL output");
   int dev;
   TQ_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_mu);
-  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, effective_ib(NB, IB)));
   if (it == g_ws.end()) {
     set_error("tileqr_kernel_times: no factorization of this shape has run");
     return TILEQR_ERR_NOT_INIT;
@@ -1493,6 +1551,19 @@ int tileqr_kernel_times(int64_t M, int64_t N, int NB, int IB, int kind, double* 
   FactorWS* ws = it->second.get();
   double tot = 0.0;
   int64_t nl = 0, nt = 0;
+  if (kind == 5) {  // timing bit 4: dataflow-kernel launches since the last read (sum, count); resets
+    double t = 0.0;
+    for (size_t i = 0; i < ws->acc_n; ++i) {
+      float ms = 0.f;
+      TQ_CUDA(cudaEventElapsedTime(&ms, ws->acc_ev[2 * i], ws->acc_ev[2 * i + 1]));
+      t += ms;
+    }
+    *h_total_ms = t;
+    *h_launches = (int64_t)ws->acc_n;
+    *h_tasks = ws->dag_last ? ws->dag_last->ntasks : 0;
+    ws->acc_n = 0;
+    return 0;
+  }
   if (ws->use_dag) {
     // dataflow kernel: busy time of the items of this kind summed over CTAs
     // (inputs ready -> completion published); kind 4 = the whole DAG kernel
@@ -1548,7 +1619,7 @@ int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, 
   int dev;
   TQ_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(g_mu);
-  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, effective_ib(NB, IB)));
   if (it == g_ws.end()) {
     set_error("tileqr_kernel_trace: no factorization of this shape has run");
     return TILEQR_ERR_NOT_INIT;
@@ -1572,7 +1643,9 @@ int tileqr_kernel_trace(int64_t M, int64_t N, int NB, int IB, int64_t max_recs, 
       if (h_t1_ms) h_t1_ms[i] = (double)(pr[3 * i + 2] - t0) * 1e-6;
       if (h_kind) h_kind[i] = L.item_kind[i];
       if (h_level) h_level[i] = L.item_level[i];
-      if (h_tasks) h_tasks[i] = (int64_t)(pr[3 * i] - t0);  // DAG: claim time (ns from origin)
+      // DAG: claim time (ns from origin, 1024 ns resolution), the low 10 bits
+      // the item's tag (SM id | C2 staged << 9, dag.cuh)
+      if (h_tasks) h_tasks[i] = (int64_t)(((pr[3 * i] - t0) & ~0x3ffull) | (pr[3 * i] & 0x3ffull));
     }
     return 0;
   }
@@ -1601,7 +1674,7 @@ namespace tileqr {
 // keep one workspace per candidate resident).
 void release_ws(int dev, int64_t M, int64_t N, int NB, int IB) {
   std::lock_guard<std::mutex> lock(g_mu);
-  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, IB));
+  auto it = g_ws.find(std::make_tuple(dev, M, N, NB, effective_ib(NB, IB)));
   if (it == g_ws.end()) return;
   if (it->second->used) cudaEventSynchronize(it->second->last_use);
   g_ws.erase(it);

@@ -43,8 +43,17 @@ struct Item {
   int aux[4];    // COPY: aux[0] = doubles to push from p[0] to p[1], then +1 on the peer counter (int*)p[2];
                  // LOAD / STORE (host-buffer pipeline): tile column n, tile rows [aux[1], aux[2]);
                  // LARFB / SSRFB: aux[0] = column limit in the tile (N - n*NB, at most NB):
-                 // the columns past it are padding, which every update leaves exactly as is
+                 // the columns past it are padding, which every update leaves exactly as is;
+                 // SSRFB: aux[1] = rows of C2's tile above M when that tile holds padding
+                 // rows (V2 is zero there: those rows are skipped), else 0 (all NB rows)
 };
+
+// aux[1] of SSRFB(k, m, n): rows of tile row m that are inside the matrix, or
+// 0 when all NB are
+inline int ssrfb_rows(long long M, long long m, int NB) {
+  const long long r = M - m * NB;
+  return (r > 0 && r < NB) ? (int)r : 0;
+}
 
 // Host-buffer pipeline of tileqr_factor_host: LOAD items convert a tile
 // column that the copy engine has landed in a column-major staging buffer

@@ -244,6 +244,7 @@ int emit_items(const Plan& p, int rank, const std::vector<RankBufs>& bufs, bool 
       case dag::kSsrfb:
         it.p[2] = A(t.k, t.n); it.p[3] = A(t.m, t.n); it.pk = slot(r, t.k, t.m);
         it.aux[0] = (int)std::min<int64_t>(NB, std::max<int64_t>(0, p.N - (int64_t)t.n * NB));
+        it.aux[1] = dag::ssrfb_rows(p.M, t.m, NB);
         break;
       case dag::kCopy: {
         const int d = t.s;

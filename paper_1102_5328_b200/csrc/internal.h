@@ -36,6 +36,10 @@ inline bool valid_nb_ib(int NB, int IB) {
 // (m + n*MT)*NB*NB); sets *d_info = 1 when A holds a non-finite value.
 int launch_layout_to_tiles(int64_t M, int64_t N, const double* A, int64_t lda, int NB, int64_t MT,
                            int64_t NT, double* tiles, int* d_info, cudaStream_t s);
+int launch_t_assemble(bool ts, int NB, int IBe, int IB, int batch, const double* const* V,
+                      const double* const* Tin, double* const* Tout, cudaStream_t s);
+int effective_ib(int NB, int IB);
+int launch_t_extract(const double* Te, int IBe, double* T, int IB, int NB, int64_t ntiles, cudaStream_t s);
 int launch_tiles_to_layout(int64_t M, int64_t N, double* A, int64_t lda, int NB, int64_t MT,
                            int64_t NT, const double* tiles, cudaStream_t s);
 // Copy the V part of A (M x K) into a tile buffer (rows >= M zero, columns >= K zero).

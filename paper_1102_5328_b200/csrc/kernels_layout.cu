@@ -291,6 +291,32 @@ int launch_fill_ptrs(double** out, double* base, size_t stride, int n, cudaStrea
   return 0;
 }
 
+// T of inner blocking IB from the T of a factorization run at IBe (a multiple
+// of IB): the diagonal IB x IB blocks of each IBe x IBe block (R23 --
+// the compact-WY recurrence T[0:i, i] = -tau_i T[0:i, 0:i] V[:, 0:i]^T v_i
+// restricted to the reflectors of one IB block involves only that block).
+__global__ void t_extract_kernel(const double* __restrict__ Te, int IBe, double* __restrict__ T, int IB, int NB,
+                                 long long total) {
+  const long long per = (long long)IB * NB;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long tile = e / per;
+    const int r = (int)(e - tile * per);
+    const int j = r / IB, l = r - j * IB;
+    const int jb = j % IB;               // column j within its IB block
+    const int off = (j - jb) % IBe;      // first row of that IB block within the IBe block
+    T[e] = l <= jb ? __ldg(Te + tile * (long long)IBe * NB + off + l + (long long)j * IBe) : 0.0;
+  }
+}
+
+int launch_t_extract(const double* Te, int IBe, double* T, int IB, int NB, int64_t ntiles, cudaStream_t s) {
+  const long long total = (long long)ntiles * IB * NB;
+  if (total <= 0) return 0;
+  t_extract_kernel<<<grid_for(total), kThreads, 0, s>>>(Te, IBe, T, IB, NB, total);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
 int launch_zero_int(int* p, cudaStream_t s) {
   zero_int_kernel<<<1, 1, 0, s>>>(p);
   TQ_LAUNCH_CHECK();

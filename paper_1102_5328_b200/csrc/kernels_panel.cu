@@ -399,6 +399,26 @@ static int launch_wide(int NB, int IB, int batch, double* const* R, double* cons
   return rc;
 }
 
+// T at inner blocking IBe (<= 64, a multiple of IB) from the reflectors V and
+// tau = the diagonal of T at IB (R23): the batched update entry
+// points run an IB that the packed update does not take at IBe.
+int launch_t_assemble(bool ts, int NB, int IBe, int IB, int batch, const double* const* V,
+                      const double* const* Tin, double* const* Tout, cudaStream_t s) {
+  if (batch <= 0) return 0;
+  if (IBe > kWideIB || IBe % IB || NB % IBe) {
+    set_error("launch_t_assemble: IBe must be a multiple of IB dividing NB, at most 64");
+    return TILEQR_ERR_CUDA;
+  }
+  const size_t bytes = ((size_t)(NB + 1) * IBe + 2 * (size_t)IBe * IBe) * sizeof(double);
+  auto kern = ts ? wide_t_kernel<true> : wide_t_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    kern<<<batch, kThreads, bytes, s>>>(NB, IBe, IB, V, Tin, Tout);
+    e = cudaGetLastError();
+  }
+  return e == cudaSuccess ? 0 : cuda_fail(e, "wide_t_kernel", __FILE__, __LINE__);
+}
+
 static bool generic_panel_forced() {
   static int v = -1;
   if (v < 0) {

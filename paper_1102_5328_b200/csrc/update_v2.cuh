@@ -215,12 +215,17 @@ struct NoHook {
 // shared memory by a TMA bulk copy (column-major, ld NB, from column col0),
 // complete when c2bar reaches phase c2par; c2free (nullable) gets one arrival
 // per warp once the warp no longer reads the staging buffer.
-template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook, bool TT = false>
+//
+// RL (runtime row limit, SSRFB of a tile row holding the padding rows >= M):
+// only the first rbe row blocks of C2 are read, updated and written.  V2 is
+// exactly zero in the rows past M (TSQRT of zero rows), so those rows add
+// nothing to W in step A and step C leaves them as they are.
+template <int NB, int IB, int MB, bool LARFB, int W, int S, class Hook = NoHook, bool TT = false, bool RL = false>
 __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, double* spk, uint64_t* full,
                                                uint64_t* empty, double* __restrict__ C1, double* __restrict__ C2,
                                                int col0, Hook hook = Hook(), int cend = NB,
                                                const double* c2s = nullptr, uint64_t* c2bar = nullptr,
-                                               uint32_t c2par = 0, uint64_t* c2free = nullptr) {
+                                               uint32_t c2par = 0, uint64_t* c2free = nullptr, int rbe = NB / 8) {
   using P = Pk<NB, IB>;
   using RG = Ring<NB, IB, S>;
   constexpr int RB = NB / 8;
@@ -246,6 +251,10 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
       const double* src = c2s + 2 * t + (size_t)(wc0 - col0 + 8 * mb + g) * NB;
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
+        if (RL && rb >= rbe) {
+          acc[mb][rb][0] = acc[mb][rb][1] = 0.0;
+          continue;
+        }
         const double2 v = *reinterpret_cast<const double2*>(src + 8 * rb);
         acc[mb][rb][0] = v.x;
         acc[mb][rb][1] = v.y;
@@ -257,6 +266,10 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
       const double* src = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
 #pragma unroll
       for (int rb = 0; rb < RB; ++rb) {
+        if (RL && rb >= rbe) {
+          acc[mb][rb][0] = acc[mb][rb][1] = 0.0;
+          continue;
+        }
         const double2 v = __ldcg(reinterpret_cast<const double2*>(src + 8 * rb));  // streaming: L2 only
         acc[mb][rb][0] = v.x;
         acc[mb][rb][1] = v.y;
@@ -315,6 +328,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
     for (int rb = 0; rb < RB; ++rb) {
       if (rb < rb0) continue;
       if (TT && 8 * rb >= c0 + IB) continue;
+      if (RL && rb >= rbe) continue;
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -399,6 +413,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
         for (int rb = 0; rb < RB; ++rb) {
           if (rb < rb0) continue;
           if (TT && 8 * rb >= c0 + IB) continue;
+          if (RL && rb >= rbe) continue;
           const double bf = pc[8 * rb * P::GW];
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], w[mb][nb][s], bf);
@@ -426,7 +441,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
     double* dst = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb)
-      *reinterpret_cast<double2*>(dst + 8 * rb) = make_double2(acc[mb][rb][0], acc[mb][rb][1]);
+      if (!RL || rb < rbe) *reinterpret_cast<double2*>(dst + 8 * rb) = make_double2(acc[mb][rb][0], acc[mb][rb][1]);
   }
 }
 

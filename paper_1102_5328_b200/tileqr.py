@@ -313,12 +313,16 @@ def factor_schedule(nb: int, ib: int) -> str:
     return _lib.tileqr_factor_schedule(nb, ib).decode()
 
 
-KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3, "dag": 4}
+KINDS = {"geqrt": 0, "tsqrt": 1, "larfb": 2, "ssrfb": 3, "dag": 4, "dag_launches": 5}
 
 
-def set_kernel_timing(on, kinds=("geqrt", "tsqrt", "larfb", "ssrfb")):
-    """Enable CUDA-event timing of the given kernel kinds (False/0: off)."""
+def set_kernel_timing(on, kinds=("geqrt", "tsqrt", "larfb", "ssrfb"), launch_events=False):
+    """Enable CUDA-event timing of the given kernel kinds (False/0: off).
+    launch_events: only CUDA events around every dataflow-kernel launch (no
+    device-clock trace), read back with kernel_times(..., "dag_launches")."""
     mask = 0 if not on else sum(1 << KINDS[k] for k in kinds)
+    if launch_events:
+        mask |= 16
     _lib.tileqr_set_kernel_timing(mask)
 
 
