@@ -1081,7 +1081,11 @@ bool panel_wide_supported(int NB, int IB);  // kernels_panel.cu
 // 10, 20 -> 40, 7, 14, 28 -> 56, where it divides NB): the same reflectors
 // (applying the IBe-blocks of a panel in order is applying its IB-blocks in
 // order, R22), with T returned at IB as the diagonal blocks of T at IBe.
-// Else IB (the generic panels and update).  TILEQR_NO_IB_LCM=1: always IB.
+// IB > 64 (whole-tile blockings such as IB = NB/2, NB): the largest of 32,
+// 24, 16, 8 dividing IB (the dataflow kernel's inner blockings), with T at IB
+// assembled afterwards from the factored tiles (its diagonal IBs-blocks are T
+// at IBs).  Else IB (the generic panels and update).  TILEQR_NO_IB_LCM=1:
+// always IB.
 int effective_ib(int NB, int IB) {
   auto fast = [&](int ib) {
     return ib <= NB && NB % ib == 0 &&
@@ -1090,6 +1094,11 @@ int effective_ib(int NB, int IB) {
   if (fast(IB)) return IB;
   const char* e = getenv("TILEQR_NO_IB_LCM");
   if (e && e[0] == '1') return IB;
+  if (IB > 64) {
+    for (int d : {32, 24, 16, 8})
+      if (IB % d == 0 && fast(d)) return d;
+    return IB;
+  }
   const int l = std::lcm(IB, 8);
   return (l <= 64 && fast(l)) ? l : IB;
 }
@@ -1165,8 +1174,14 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
   if (IBe == IB) {
     TQ_CUDA(cudaMemcpyAsync(T, ws->Tws, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double),
                             cudaMemcpyDeviceToDevice, s));
-  } else if ((rc = launch_t_extract(ws->Tws, IBe, T, IB, NB, ws->MT * ws->NT, s))) {
-    return rc;
+  } else if (IBe > IB) {
+    if ((rc = launch_t_extract(ws->Tws, IBe, T, IB, NB, ws->MT * ws->NT, s))) return rc;
+  } else {
+    TQ_CUDA(cudaMemsetAsync(T, 0, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double), s));
+    int nsm = 148;
+    TQ_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if ((rc = launch_t_assemble_big(ws->tiles, ws->Tws, T, NB, IB, IBe, ws->MT, std::min(ws->MT, ws->NT), nsm, s)))
+      return rc;
   }
   TQ_CUDA(cudaEventRecord(ws->last_use, s));
   ws->used = true;
@@ -1330,16 +1345,26 @@ int tileqr_apply_qt(char trans, int64_t M, int64_t NRHS, int64_t K, const double
 
 // Batched Q^T update through the factorization's packed-reflector kernel:
 // pack (V, T) into stream-ordered scratch, then run update_v2.
+// IB the batched LARFB / SSRFB entry points run through lcm(IB, 8) (R23): the
+// T assembly at IBe (wide_t_kernel, a sequential recurrence per tile) costs
+// about as much as the update itself, which pays only against the 4-8x slower
+// generic kernels of IB < 8 (4096-pair SSRFB at (128, 4): 12.9 -> 16.7
+// TFLOP/s; at (160, 10) it would fall from 15.1 to 10.3, so IB >= 8 keeps the
+// staged DMMA update).  tileqr_factor and Step 1 run IBe directly (no assembly).
+// IB > 64: T at IBs (a divisor of IB) is the caller's T's diagonal blocks.
+static int batched_ib(int NB, int IB) { return (IB < 8 || IB > 64) ? effective_ib(NB, IB) : IB; }
+
 static int packed_update(bool larfb, int NB, int IB, int batch, const double* const* V, const double* const* T,
                          double* const* C1, double* const* C2, cudaStream_t s) {
-  const int IBe = effective_ib(NB, IB);
-  if (IBe != IB) {  // R23: T at IBe from V and tau, then the IBe update
+  const int IBe = batched_ib(NB, IB);
+  if (IBe != IB) {  // R23: T at IBe from V and tau (IBe > IB) or T's diagonal blocks (IBe < IB), then the IBe update
     double* tb = nullptr;
     double** tp = nullptr;
     if (int rc_ = stream_alloc(reinterpret_cast<void**>(&tb), (size_t)batch * IBe * NB * sizeof(double), s)) return rc_;
     if (int rc_ = stream_alloc(reinterpret_cast<void**>(&tp), (size_t)batch * sizeof(double*), s)) return rc_;
     int rc = launch_fill_ptrs(tp, tb, (size_t)IBe * NB, batch, s);
-    if (!rc) rc = launch_t_assemble(!larfb, NB, IBe, IB, batch, V, T, tp, s);
+    if (!rc) rc = IBe > IB ? launch_t_assemble(!larfb, NB, IBe, IB, batch, V, T, tp, s)
+                           : launch_t_extract_ptrs(T, IB, tp, IBe, NB, batch, s);
     if (!rc) rc = packed_update(larfb, NB, IBe, batch, V, tp, C1, C2, s);
     cudaFreeAsync(tb, s);
     cudaFreeAsync(tp, s);
@@ -1402,7 +1427,7 @@ int tileqr_larfb_batched(char trans, int NB, int IB, int batch, const double* co
   if (ncols < 1 || ncols > NB) return arg_error(8, fn, "ncols not in [1, NB]");
   const bool tr = trans == 'T' || trans == 't';
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (tr && ncols == NB && v2_supported(NB, effective_ib(NB, IB)))  // the factorization's kernel: pack, then update
+  if (tr && ncols == NB && v2_supported(NB, batched_ib(NB, IB)))  // the factorization's kernel: pack, then update
     return packed_update(true, NB, IB, batch, V, T, nullptr, C, s);
   return launch_larfb(tr, NB, IB, batch, V, T, C, ncols, s);
 }
@@ -1424,7 +1449,7 @@ int tileqr_ssrfb_batched(char trans, int NB, int IB, int batch, const double* co
   if (ncols < 1 || ncols > NB) return arg_error(9, fn, "ncols not in [1, NB]");
   const bool tr = trans == 'T' || trans == 't';
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (tr && ncols == NB && v2_supported(NB, effective_ib(NB, IB)))
+  if (tr && ncols == NB && v2_supported(NB, batched_ib(NB, IB)))
     return packed_update(false, NB, IB, batch, V2, T, C1, C2, s);
   return launch_ssrfb(tr, NB, IB, batch, V2, T, C1, C2, ncols, s);
 }

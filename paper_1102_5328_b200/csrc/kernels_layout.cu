@@ -1,3 +1,4 @@
+#include <algorithm>
 // kernels_layout.cu -- HBM-bound data movement of the tile QR (SURVEY §8(a)
 // rows a1/a7): LAPACK column-major <-> padded tile layout, the non-finite
 // flag, and the device copy of the synthetic input generator.
@@ -313,6 +314,83 @@ int launch_t_extract(const double* Te, int IBe, double* T, int IB, int NB, int64
   const long long total = (long long)ntiles * IB * NB;
   if (total <= 0) return 0;
   t_extract_kernel<<<grid_for(total), kThreads, 0, s>>>(Te, IBe, T, IB, NB, total);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+// Same for arrays of per-tile pointers (batched entry points): T at IBo, a
+// divisor of IBi, from T at IBi -- the diagonal IBo-blocks.  One CTA per tile.
+__global__ void t_extract_ptrs_kernel(const double* const* Tin, int IBi, double* const* Tout, int IBo, int NB) {
+  const double* Ti = Tin[blockIdx.x];
+  double* To = Tout[blockIdx.x];
+  for (int e = threadIdx.x; e < IBo * NB; e += blockDim.x) {
+    const int j = e / IBo, l = e - j * IBo;
+    const int jb = j % IBo, off = (j - jb) % IBi;
+    To[e] = l <= jb ? Ti[off + l + (size_t)j * IBi] : 0.0;
+  }
+}
+
+int launch_t_extract_ptrs(const double* const* Tin, int IBi, double* const* Tout, int IBo, int NB, int batch,
+                          cudaStream_t s) {
+  if (batch <= 0) return 0;
+  t_extract_ptrs_kernel<<<batch, kThreads, 0, s>>>(Tin, IBi, Tout, IBo, NB);
+  TQ_LAUNCH_CHECK();
+  return 0;
+}
+
+// T at IB (> 64) of a whole factorization run at IBs (a divisor of IB,
+// DESIGN.md R23): for every tile (m, k), m >= k, k < KT, and every IB-panel,
+// the compact-WY recurrence T[i, i] = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] z,
+// z_l = v_l^T v_i, with V read from the factored tile
+// (GEQRT form on the diagonal: unit lower trapezoid; TSQRT form below: the
+// tops e_l, e_i are orthogonal, only V2 contributes) and tau_j the diagonal of
+// T at IBs.  T must be zeroed by the caller (tiles m < k stay 0).
+__global__ void t_assemble_big_kernel(const double* __restrict__ tiles, const double* __restrict__ Ts,
+                                      double* __restrict__ T, int NB, int IB, int IBs, long long MT,
+                                      long long KT) {
+  extern __shared__ double z[];  // IB
+  for (long long t = blockIdx.x; t < MT * KT; t += gridDim.x) {
+    const long long k = t / MT, m = t - k * MT;
+    if (m < k) continue;
+    const size_t tile = (size_t)(m + k * MT);
+    const double* V = tiles + tile * NB * NB;
+    const double* ts = Ts + tile * IBs * NB;
+    double* To = T + tile * IB * NB;
+    const bool ge = m == k;
+    for (int c0 = 0; c0 < NB; c0 += IB) {
+      for (int i = 0; i < IB; ++i) {
+        const int j = c0 + i;
+        for (int l = threadIdx.x; l < i; l += blockDim.x) {
+          const int jl = c0 + l;
+          const double* vl = V + (size_t)jl * NB;
+          const double* vi = V + (size_t)j * NB;
+          double acc = ge ? vl[j] : 0.0;  // GEQRT: v_l[j] * 1
+          for (int r = ge ? j + 1 : 0; r < NB; ++r) acc = fma(vl[r], vi[r], acc);
+          z[l] = acc;
+        }
+        __syncthreads();
+        const double tau = ts[(j % IBs) + (size_t)j * IBs];
+        for (int r = threadIdx.x; r < IB; r += blockDim.x) {
+          double out = r == i ? tau : 0.0;
+          if (r < i) {
+            double acc = 0.0;
+            for (int l = r; l < i; ++l) acc = fma(To[r + (size_t)(c0 + l) * IB], z[l], acc);
+            out = -tau * acc;
+          }
+          To[r + (size_t)j * IB] = out;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
+
+int launch_t_assemble_big(const double* tiles, const double* Ts, double* T, int NB, int IB, int IBs, int64_t MT,
+                          int64_t KT, int nsm, cudaStream_t s) {
+  const long long n = (long long)MT * KT;
+  if (n <= 0) return 0;
+  const int grid = (int)std::min<long long>(n, (long long)std::max(1, nsm) * 4);
+  t_assemble_big_kernel<<<grid, kThreads, (size_t)IB * sizeof(double), s>>>(tiles, Ts, T, NB, IB, IBs, MT, KT);
   TQ_LAUNCH_CHECK();
   return 0;
 }

@@ -273,13 +273,19 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
       if (nb % ib) continue;
       // V2, T from a TSQRT of (top, bottom); fresh bottoms each time are not
       // needed for timing: the reflector values only scale the data.
-      TQ_TRY(launch_tsqrt(nb, ib, batch, ptrs, ptrs + batch, ptrs + 4 * batch, s));
       // Time the kernel tileqr_factor runs for this (NB, IB): the packed-
       // reflector update (operands packed once, outside the timing) where
-      // available, else the staged DMMA / SIMT update.
-      const bool pk = v2_supported(nb, ib);
+      // available -- at IBe = lcm(IB, 8) for the IB it runs that way (DESIGN.md
+      // R23; a tie with IBe itself then goes to IBe, the larger) -- else the
+      // staged DMMA / SIMT update.  IB > 64 keeps its own (generic) kernel
+      // here: timed at its divisor IBs it would tie with IBs and, as the larger
+      // IB, take Property 1's tie (R18) for a blocking whose T is assembled
+      // after the factorization.
+      const int ibk = ib > 64 ? ib : effective_ib(nb, ib);
+      const bool pk = v2_supported(nb, ibk);
+      TQ_TRY(launch_tsqrt(nb, pk ? ibk : ib, batch, ptrs, ptrs + batch, ptrs + 4 * batch, s));
       if (pk) {
-        const size_t pd = v2_pk_doubles(nb, ib);
+        const size_t pd = v2_pk_doubles(nb, ibk);
         if (pd > pk_cap) {
           cudaFree(pkbuf);
           pkbuf = nullptr;
@@ -292,10 +298,10 @@ int tileqr_tune(int64_t M, int64_t N, int ngpus, int heuristic, int payg, int* h
           pk_cap = pd;
         }
         TQ_TRY(launch_fill_ptrs(pkp, pkbuf, pd, batch, s));
-        TQ_TRY(launch_pack(false, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, pkp, s));
+        TQ_TRY(launch_pack(false, nb, ibk, batch, ptrs + batch, ptrs + 4 * batch, pkp, s));
       }
       auto one = [&]() -> int {
-        if (pk) return launch_update_pk(false, nb, ib, batch, pkp, ptrs + 2 * batch, ptrs + 3 * batch, s);
+        if (pk) return launch_update_pk(false, nb, ibk, batch, pkp, ptrs + 2 * batch, ptrs + 3 * batch, s);
         return launch_ssrfb(true, nb, ib, batch, ptrs + batch, ptrs + 4 * batch, ptrs + 2 * batch,
                             ptrs + 3 * batch, nb, s);
       };

@@ -1,9 +1,13 @@
-"""IB that the DMMA paths take only through lcm(IB, 8) (R23).
+"""IB that the DMMA paths take only through another inner blocking IBe
+(R23): lcm(IB, 8) for IB not a multiple of 8, a divisor <= 32 for
+IB > 64.
 
 tileqr_factor runs such an IB at IBe = lcm(IB, 8) (when IBe <= 64 divides NB)
-and returns T at IB as the diagonal IB-blocks of T at IBe; the batched
-LARFB / SSRFB entry points ('T', all NB columns) assemble T at IBe from V and
-the diagonal of the caller's T and run the packed IBe update.  Both are
+and returns T at IB as the diagonal IB-blocks of T at IBe (IB > 64: runs at
+IBe | IB and assembles T at IB from the factored tiles); the batched LARFB /
+SSRFB entry points ('T', all NB columns, IB < 8 or > 64) form T at IBe
+(assembled from V and tau, or the caller's T's diagonal blocks) and run the
+packed IBe update.  Both are
 compared with the oracle run at the caller's IB (V, R, T and the updated
 tiles, normwise; the IBe blocking is another rounding order of the same
 reflectors).
@@ -20,7 +24,9 @@ pytestmark = pytest.mark.gpu
 
 BATCH = 4
 LCM_CASES = [(64, 2, 8), (128, 4, 8), (96, 12, 24), (192, 6, 24), (160, 10, 40), (160, 20, 40),
-             (224, 28, 56), (224, 14, 56), (256, 1, 8)]
+             (224, 28, 56), (224, 14, 56), (256, 1, 8),
+             # IB > 64: run at the largest of 32, 24, 16, 8 dividing IB, T at IB assembled afterwards
+             (128, 128, 32), (256, 128, 32), (96, 96, 32), (160, 80, 16), (224, 224, 32), (256, 256, 32)]
 
 
 @pytest.fixture(scope="module")
@@ -61,7 +67,7 @@ def test_factor_at_lcm_blocking_matches_oracle(tq, nb, ib, ibe):
             assert np.all(blk[j, j % ib + 1:] == 0.0)
 
 
-@pytest.mark.parametrize("nb,ib,ibe", LCM_CASES[:7])
+@pytest.mark.parametrize("nb,ib,ibe", [c for c in LCM_CASES if c[1] < 8 or c[1] > 64])
 @pytest.mark.parametrize("larfb", [False, True])
 def test_batched_update_at_lcm_blocking_matches_oracle(tq, nb, ib, ibe, larfb):
     vs, ts, c1, c2 = [], [], [], []
