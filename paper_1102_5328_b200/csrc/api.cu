@@ -1180,7 +1180,8 @@ int tileqr_factor(int64_t M, int64_t N, double* A, int64_t lda, int NB, int IB, 
     TQ_CUDA(cudaMemsetAsync(T, 0, (size_t)ws->MT * ws->NT * IB * NB * sizeof(double), s));
     int nsm = 148;
     TQ_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    if ((rc = launch_t_assemble_big(ws->tiles, ws->Tws, T, NB, IB, IBe, ws->MT, std::min(ws->MT, ws->NT), nsm, s)))
+    const int64_t KT = std::min(ws->MT, ws->NT);
+    if ((rc = launch_t_assemble_big(ws->tiles, ws->Tws, T, NB, IB, IBe, ws->MT, KT, KT, 1, 0, nsm, s)))
       return rc;
   }
   TQ_CUDA(cudaEventRecord(ws->last_use, s));

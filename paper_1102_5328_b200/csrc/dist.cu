@@ -438,11 +438,33 @@ int tileqr_dist_factor(int64_t M, int64_t N, double* A_local, int NB, int IB, do
     if (rc) return rc;
   }
   if (M == 0 || N == 0) return 0;
-  {
-    int nl = 0;
-    tileqr_dist_local_cols(N, NB, &nl);
-    if (nl > 0 && !A_local) return -3;
-    if (nl > 0 && !T_local) return -6;
+  int nloc0 = 0;
+  tileqr_dist_local_cols(N, NB, &nloc0);
+  if (nloc0 > 0 && !A_local) return -3;
+  if (nloc0 > 0 && !T_local) return -6;
+  // the inner blocking tileqr_factor runs (R23), so that the result
+  // is bitwise the single-GPU one: the factorization at IBe into a scratch T,
+  // then T at IB (its diagonal blocks, or assembled from the local V tiles)
+  if (const int IBe = effective_ib(NB, IB); IBe != IB) {
+    const int64_t MTl = (M + NB - 1) / NB, KT = std::min(MTl, (N + NB - 1) / NB);
+    double* te = nullptr;
+    if (int rc = stream_alloc(reinterpret_cast<void**>(&te), (size_t)std::max(1, nloc0) * MTl * IBe * NB * sizeof(double), s))
+      return rc;
+    int rc = tileqr_dist_factor(M, N, A_local, NB, IBe, te, d_info, stream);
+    if (!rc && IBe > IB) rc = launch_t_extract(te, IBe, T_local, IB, NB, MTl * nloc0, s);
+    if (!rc && IBe < IB) {
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      if (cudaMemsetAsync(T_local, 0, (size_t)MTl * nloc0 * IB * NB * sizeof(double), s) != cudaSuccess) {
+        rc = TILEQR_ERR_CUDA;
+        set_error("tileqr_dist_factor: memset failed");
+      } else {
+        rc = launch_t_assemble_big(A_local, te, T_local, NB, IB, IBe, MTl, nloc0, KT, g_d.nranks, g_d.rank, nsm, s);
+      }
+    }
+    cudaFreeAsync(te, s);
+    return rc;
   }
   if (dist_dataflow(NB, IB)) return dd_factor(M, N, A_local, NB, IB, T_local, d_info, s);
   if (M != N) {

@@ -42,7 +42,7 @@ int effective_ib(int NB, int IB);
 int launch_t_extract_ptrs(const double* const* Tin, int IBi, double* const* Tout, int IBo, int NB, int batch,
                           cudaStream_t s);
 int launch_t_assemble_big(const double* tiles, const double* Ts, double* T, int NB, int IB, int IBs, int64_t MT,
-                          int64_t KT, int nsm, cudaStream_t s);
+                          int64_t NTl, int64_t KT, int P, int r, int nsm, cudaStream_t s);
 int launch_t_extract(const double* Te, int IBe, double* T, int IB, int NB, int64_t ntiles, cudaStream_t s);
 int launch_tiles_to_layout(int64_t M, int64_t N, double* A, int64_t lda, int NB, int64_t MT,
                            int64_t NT, const double* tiles, cudaStream_t s);

@@ -1,4 +1,3 @@
-#include <algorithm>
 // kernels_layout.cu -- HBM-bound data movement of the tile QR (SURVEY §8(a)
 // rows a1/a7): LAPACK column-major <-> padded tile layout, the non-finite
 // flag, and the device copy of the synthetic input generator.
@@ -10,6 +9,8 @@
 // 256-B runs: one thread per element pair, grid-stride, 16-B accesses on the
 // tile side when NB is even.
 #include <math.h>
+
+#include <algorithm>
 
 #include "internal.h"
 
@@ -344,15 +345,17 @@ int launch_t_extract_ptrs(const double* const* Tin, int IBi, double* const* Tout
 // z_l = v_l^T v_i, with V read from the factored tile
 // (GEQRT form on the diagonal: unit lower trapezoid; TSQRT form below: the
 // tops e_l, e_i are orthogonal, only V2 contributes) and tau_j the diagonal of
-// T at IBs.  T must be zeroed by the caller (tiles m < k stay 0).
+// T at IBs.  T must be zeroed by the caller (tiles m < k stay 0).  Multi-rank
+// (P > 1): the tiles and T are rank r's local tile columns jl (global column
+// r + jl*P).
 __global__ void t_assemble_big_kernel(const double* __restrict__ tiles, const double* __restrict__ Ts,
                                       double* __restrict__ T, int NB, int IB, int IBs, long long MT,
-                                      long long KT) {
+                                      long long NTl, long long KT, int P, int r) {
   extern __shared__ double z[];  // IB
-  for (long long t = blockIdx.x; t < MT * KT; t += gridDim.x) {
-    const long long k = t / MT, m = t - k * MT;
-    if (m < k) continue;
-    const size_t tile = (size_t)(m + k * MT);
+  for (long long t = blockIdx.x; t < MT * NTl; t += gridDim.x) {
+    const long long jl = t / MT, m = t - jl * MT, k = r + jl * P;
+    if (k >= KT || m < k) continue;
+    const size_t tile = (size_t)t;
     const double* V = tiles + tile * NB * NB;
     const double* ts = Ts + tile * IBs * NB;
     double* To = T + tile * IB * NB;
@@ -386,11 +389,12 @@ __global__ void t_assemble_big_kernel(const double* __restrict__ tiles, const do
 }
 
 int launch_t_assemble_big(const double* tiles, const double* Ts, double* T, int NB, int IB, int IBs, int64_t MT,
-                          int64_t KT, int nsm, cudaStream_t s) {
-  const long long n = (long long)MT * KT;
+                          int64_t NTl, int64_t KT, int P, int r, int nsm, cudaStream_t s) {
+  const long long n = (long long)MT * NTl;
   if (n <= 0) return 0;
   const int grid = (int)std::min<long long>(n, (long long)std::max(1, nsm) * 4);
-  t_assemble_big_kernel<<<grid, kThreads, (size_t)IB * sizeof(double), s>>>(tiles, Ts, T, NB, IB, IBs, MT, KT);
+  t_assemble_big_kernel<<<grid, kThreads, (size_t)IB * sizeof(double), s>>>(tiles, Ts, T, NB, IB, IBs, MT, NTl,
+                                                                            KT, P, r);
   TQ_LAUNCH_CHECK();
   return 0;
 }

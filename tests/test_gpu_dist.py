@@ -73,7 +73,7 @@ def from_locals(bufs, nb, world, mt, nt):
 
 @pytest.mark.parametrize("sched", ["dataflow", "levels"])
 @pytest.mark.parametrize("n,nb,ib", [(512, 128, 32), (600, 128, 16), (700, 64, 16), (300, 96, 12),
-                                     (800, 256, 16), (500, 160, 32)])
+                                     (800, 256, 16), (500, 160, 32), (600, 128, 128), (500, 64, 2)])
 def test_dist_world1_bitwise_equals_factor(tq, monkeypatch, sched, n, nb, ib):
     if sched == "levels":
         monkeypatch.setenv("TILEQR_DIST_SCHED", "levels")
