@@ -73,6 +73,16 @@ for sm, its in per_sm.items():
             it = ch[idx[ci]] if idx[ci] < len(ch) else None
             st.append("-" if it is None or it[0] > mid else ("U" if it[2] in upd else "P"))
         tsplit["".join(sorted(st))] += t1 - t0
+dur = collections.defaultdict(list)
+for sm, its in per_sm.items():
+    for it in its:
+        if it[2] == "ssrfb":
+            dur[it[4]].append(1e3 * (it[1] - it[0]))
+for k in sorted(dur):
+    v = sorted(dur[k])
+    q = lambda f: v[min(len(v) - 1, int(f * len(v)))]
+    print(f"SSRFB duration (us), C2 staged={k}: n={len(v)} p10 {q(0.1):.1f} p50 {q(0.5):.1f} p90 {q(0.9):.1f} "
+          f"p99 {q(0.99):.1f} mean {sum(v) / len(v):.2f}")
 print("SSRFB item duration (us) by the SM's other CTA [fast hand-off flag]:")
 for k in sorted(cat):
     v = sorted(cat[k])
