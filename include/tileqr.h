@@ -107,6 +107,11 @@ int tileqr_lookup(int64_t M, int64_t N, int ngpus, int* h_NB, int* h_IB);
  *   d_info [out] device int (may be NULL): 0 = ok, 1 = A held a non-finite
  *      entry (the factorization still runs; its output is then unspecified).
  *   Workspace: (MT*NB) x (NT*NB) doubles plus task lists, cached.
+ *   Inner blocking (R23): an IB that is not a multiple of 8 runs
+ *   at IBe = lcm(IB, 8) when IBe <= 64 divides NB, an IB > 64 at the largest
+ *   of 32, 24, 16, 8 dividing it; R and V are the IB-blocked reflectors (to
+ *   rounding) and T is returned at IB (diagonal blocks of T at IBe, or
+ *   assembled from the factored tiles).
  *   Errors: -1 M<0, -2 N<0, -3 A==NULL (M,N>0), -4 lda<max(1,M), -5 NB,
  *   -6 IB, -7 T==NULL.  Quick return for M == 0 or N == 0.
  * ------------------------------------------------------------------------ */
