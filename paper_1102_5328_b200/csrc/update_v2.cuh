@@ -231,6 +231,18 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
   constexpr int RB = NB / 8;
   constexpr int NBK = P::NBK;
   constexpr bool SPLIT = NBK * MB < 4;  // two partial sums per step-A block when chains are few
+  // C2 stored during the last panel's step C, one group of ES row blocks at a
+  // time (NB >= 96; same-box A/B, r02as: 10000^2 (128, 16) -0.35 %, 4096^2
+  // -1.0 %; NB = 64 +0.3 %, not used there)
+#ifndef TILEQR_ES_GROUP
+#define TILEQR_ES_GROUP 4
+#endif
+  constexpr int ES = TILEQR_ES_GROUP;
+#ifdef TILEQR_NO_C2_EARLY_STORE
+  constexpr bool ESTORE = false;
+#else
+  constexpr bool ESTORE = !TT && NB >= 96;
+#endif
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int t = lane & 3, g = lane >> 2;
   const int wc0 = col0 + warp * 8 * MB;  // first column of this warp
@@ -404,6 +416,37 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
         w[mb][nb][1] = -w[mb][nb][1];
       }
     const int fg = pk_f(g);
+    if (ESTORE && p == P::NP - 1) {
+      // last panel: row blocks in groups of ES, each group's C2 rows stored
+      // right after their last DMMA (the stores drain under the next groups'
+      // DMMAs instead of after the loop); every accumulator sees the same
+      // (nb, s) order as below, so the results are bitwise the same
+#pragma unroll
+      for (int r0 = 0; r0 < RB; r0 += ES) {
+#pragma unroll
+        for (int nb = 0; nb < NBK; ++nb)
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const double* pc = Vq + g * P::GW + ((cb + 8 * nb + 2 * t + s) ^ fg);
+#pragma unroll
+            for (int rb = r0; rb < r0 + ES && rb < RB; ++rb) {
+              if (rb < rb0) continue;
+              if (RL && rb >= rbe) continue;
+              const double bf = pc[8 * rb * P::GW];
+#pragma unroll
+              for (int mb = 0; mb < MB; ++mb) dmma(acc[mb][rb][0], acc[mb][rb][1], w[mb][nb][s], bf);
+            }
+          }
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          double* dst = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
+#pragma unroll
+          for (int rb = r0; rb < r0 + ES && rb < RB; ++rb)
+            if (!RL || rb < rbe)
+              *reinterpret_cast<double2*>(dst + 8 * rb) = make_double2(acc[mb][rb][0], acc[mb][rb][1]);
+        }
+      }
+    } else
 #pragma unroll
     for (int nb = 0; nb < NBK; ++nb)
 #pragma unroll
@@ -436,6 +479,7 @@ __device__ __forceinline__ void update_v2_body(const double* __restrict__ gpk, d
   }
 
   // ---- registers -> C2 ----------------------------------------------------------
+  if (ESTORE) return;  // stored during the last panel's step C
 #pragma unroll
   for (int mb = 0; mb < MB; ++mb) {
     double* dst = C2 + 2 * t + (size_t)(wc0 + 8 * mb + g) * NB;
