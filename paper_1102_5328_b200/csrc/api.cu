@@ -171,6 +171,7 @@ struct DagList {
   std::vector<int> item_level;
   std::vector<std::pair<int, int>> st_order;  // STORE groups (column, group) in claim order
   int io_tiles = 8;
+  int launch_nsm = 0;  // > 0: SM count handed to the launch (one resident CTA per SM for small DAGs)
   ~DagList() {
     cudaFree(d_items);
     cudaFree(d_ctr);
@@ -458,8 +459,22 @@ static int build_dag(FactorWS* ws, bool io) {
   int dev0 = 0, nsm0 = 0;
   TQ_CUDA(cudaGetDevice(&dev0));
   TQ_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0));
-  const int P = std::max(1, nsm0 * dag::dag_ctas_per_sm(NB));
-  double cta_gflops = 220.0 / dag::dag_ctas_per_sm(NB);             // update rate per CTA
+  // Small DAGs are bound by the panel chain, and a GEQRT/TSQRT item runs at
+  // about half speed while an update CTA shares its SM: with at most
+  // kOneCtaTiles tile updates in the widest step, one CTA per SM is resident.
+  // Same-box sweeps (profiles/r02s4_one_cta*.log): NB = 64 gains 3-8 % up to
+  // 2048^2 (961 tiles) and loses 12 % at 2500^2 (1521); NB = 128 gains 6-14 %
+  // up to 4000^2 (961) and loses 5 % at 5000^2 (1444); NB = 96 +3 % at 961,
+  // -16 % at 1681.  The results do not depend on the resident CTA count.
+  int ctas_per_sm = dag::dag_ctas_per_sm(NB);
+  {
+    long kOneCtaTiles = 1200;
+    if (const char* e = getenv("TILEQR_DAG_ONE_CTA_TILES")) kOneCtaTiles = atol(e);  // diagnostics
+    const long widest = (long)(MT - 1) * (long)(NT - 1);
+    if (!io && ctas_per_sm == 2 && widest <= kOneCtaTiles) ctas_per_sm = 1;
+  }
+  const int P = std::max(1, nsm0 * ctas_per_sm);
+  double cta_gflops = 220.0 / ctas_per_sm;                          // update rate per CTA
   if (const char* e = getenv("TILEQR_DAG_CTAGF")) cta_gflops *= atof(e);  // diagnostics
   const double dS = 4.0 * NB * NB * cols / cta_gflops;               // ns per SSRFB slab
   // measured in the dataflow kernel at NB = 128 (10000^2): TSQRT and GEQRT
@@ -468,7 +483,7 @@ static int build_dag(FactorWS* ws, bool io) {
   // -> operand loads) per item.  The values below are the best of a sweep
   // (tools/sim_sweep.sh; +-40 % moves the factorization by ~1 %)
   double sT = 3000.0, sG = 3000.0, hand = 5000.0;
-  if (dag::dag_ctas_per_sm(NB) == 1) sT = sG = 1500.0;  // a panel item has its SM alone
+  if (ctas_per_sm == 1) sT = sG = 1500.0;  // a panel item has its SM alone
   if (const char* e = getenv("TILEQR_DAG_SIM")) sscanf(e, "%lf,%lf,%lf", &sT, &sG, &hand);  // diagnostics
   const double dL = 0.77 * dS + hand, dT = sT * SC + hand, dG = sG * SC + hand;
   const double dIO = 1.0e3 + (double)kIoTiles * NB * NB * 16 / 50.0;  // ~50 GB/s per CTA
@@ -511,6 +526,13 @@ static int build_dag(FactorWS* ws, bool io) {
   auto pkp = [&](int64_t m, int64_t k) { return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr; };
   DagList& L = io ? ws->dag_io : ws->dag_plain;
   const bool rowlim = !getenv("TILEQR_DAG_NO_ROWLIM");  // diagnostics: SSRFB over the padding rows too
+  // tail retirement (dag.cuh): the last `tail` items of the claim order are
+  // flagged; experiment knob, off by default
+  int64_t retire_from = INT64_MAX;
+  if (const char* e = getenv("TILEQR_DAG_RETIRE")) {
+    const long tail = atol(e);
+    if (tail > 0) retire_from = std::max<int64_t>(0, (int64_t)sched.size() - tail);
+  }
   std::vector<dag::Item> items;
   items.reserve(sched.size());
   L.item_kind.clear();
@@ -556,6 +578,7 @@ static int build_dag(FactorWS* ws, bool io) {
     if (t.kind == dag::kLarfb || t.kind == dag::kSsrfb)  // padded columns (e_j or 0) are invariant
       it.aux[0] = (int)std::min<int64_t>(NB, std::max<int64_t>(0, N - (int64_t)t.n * NB));
     if (t.kind == dag::kSsrfb && rowlim) it.aux[1] = dag::ssrfb_rows(M, t.m, NB);
+    if (!io && (int64_t)items.size() >= retire_from) it.aux[3] = 1;  // tail item (dag.cuh: tail retirement)
     items.push_back(it);
     L.item_kind.push_back((unsigned char)t.kind);
     L.item_level.push_back(t.level);
@@ -565,6 +588,7 @@ static int build_dag(FactorWS* ws, bool io) {
   L.ntasks = (int)ntask;
   L.nio = nst;
   L.io_tiles = kIoTiles;
+  L.launch_nsm = ctas_per_sm < dag::dag_ctas_per_sm(NB) ? std::max(1, nsm0 / dag::dag_ctas_per_sm(NB)) : 0;
   L.id_ld = ntask0;
   L.id_st = ntask0 + NT;
   L.id_ar = ntask0 + NT + NT * nst;
@@ -609,7 +633,7 @@ static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStre
     const long v = atol(e);
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
-  int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, ws->nsm, prof, stream,
+  int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, L.launch_nsm > 0 ? L.launch_nsm : ws->nsm, prof, stream,
                       &ws->dag_grid, io, io ? dag::kModeIO : dag::kModePlain);
   if (rc) return rc;
   if (g_timing & 15) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));

@@ -292,6 +292,12 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
   constexpr bool C2PF = dag_c2pf<NB, KW>();
   __shared__ __align__(8) uint64_t c2bar, c2free;  // C2 staging: data landed / every warp done reading
   __shared__ int s_c2item;                          // item whose C2 slab is staged (-1: none)
+  // tail retirement (device-only factorization): the second CTA to arrive on
+  // an SM stops claiming once it has started an item of the list's tail
+  // (Item::aux[3] = 1), so the tail's items -- bound by the panel chain, not
+  // by CTA slots -- have their SM to themselves. 0: keeps claiming, 1: retires
+  // at the first tail item, 2: claims no more
+  __shared__ int s_retire;
   uint32_t c2par = 0;   // all threads: phase of c2bar for the next staged slab
   uint32_t c2fpar = 0;  // thread 0: phase of c2free for the running update item
   if constexpr (C2PF) {
@@ -302,6 +308,13 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       s_c2item = -1;
     }
     __syncthreads();
+  }
+  if constexpr (MODE == kModePlain) {
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      s_retire = atomicAdd(next + 1 + (smid & 255u), 1) >= 1 ? 1 : 0;  // next[1..256]: reserved, zeroed per run
+    }
   }
   int nxt = -1;   // thread 0: item claimed ahead (-1: none)
   int slot = 0;   // descriptor slot of the running item (all threads)
@@ -315,7 +328,8 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     if (threadIdx.x == 0) {
       int cur = nxt;
       if (cur < 0) {
-        cur = atomicAdd(next, 1);
+        if (MODE == kModePlain && s_retire == 2) cur = nitems;
+        else cur = atomicAdd(next, 1);
         if (cur < nitems) fetch_desc(cur, slot);
       }
       nxt = -1;
@@ -323,6 +337,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       if (cur < nitems) {
         cp_async_wait<0>();
         const Item& it = s_desc[slot];
+        if (MODE == kModePlain && it.aux[3] != 0 && s_retire == 1) s_retire = 2;
         int need[3], got[3];
         const int nd = it.ndep;
         if constexpr (MODE == kModeDist) {  // peer-written counters: system scope
@@ -385,6 +400,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         // items [0, ca_lo) and [ca_hi, nitems) of the list (same-box A/B at
         // 10000^2: within +-0.1 % for 300-2000 items at either end)
         if (i < ca_lo || i >= ca_hi) return;
+        if (MODE == kModePlain && s_retire == 2) return;
         nxt = atomicAdd(next, 1);
         if constexpr (PC != PD) return;  // its result is first needed one panel later
       }
