@@ -171,6 +171,7 @@ struct DagList {
   std::vector<int> item_level;
   std::vector<std::pair<int, int>> st_order;  // STORE groups (column, group) in claim order
   int io_tiles = 8;
+  bool retire = false;  // tail items flagged: run the kModePlainRetire instantiation
   int launch_nsm = 0;  // > 0: SM count handed to the launch (one resident CTA per SM for small DAGs)
   ~DagList() {
     cudaFree(d_items);
@@ -526,12 +527,27 @@ static int build_dag(FactorWS* ws, bool io) {
   auto pkp = [&](int64_t m, int64_t k) { return ws->Vpk ? ws->Vpk + (size_t)(m + k * MT) * ws->pk_dbl : nullptr; };
   DagList& L = io ? ws->dag_io : ws->dag_plain;
   const bool rowlim = !getenv("TILEQR_DAG_NO_ROWLIM");  // diagnostics: SSRFB over the padding rows too
-  // tail retirement (dag.cuh): the last `tail` items of the claim order are
-  // flagged; experiment knob, off by default
+  // Tail retirement (dag.cuh): the items of the last panel steps -- those
+  // with at most kTailTiles tile updates, where the panel chain and not the
+  // CTA slots bounds the run -- are flagged, as a count at the end of the
+  // claim order; from there on one CTA per SM keeps claiming.  Same-box sweep
+  // (profiles/r02s4_retire*.log): 6000^2 (128, 16) -3.1 %, (128, 32) -2.4 %,
+  // 10000^2 -0.1 %; a tail three times as long costs 2 % at 10000^2.
   int64_t retire_from = INT64_MAX;
-  if (const char* e = getenv("TILEQR_DAG_RETIRE")) {
-    const long tail = atol(e);
-    if (tail > 0) retire_from = std::max<int64_t>(0, (int64_t)sched.size() - tail);
+  // Only where the tail is a visible share of the run (widest step of at most
+  // kRetireMaxTiles tile updates: up to 8000^2 at NB = 128): the retirement
+  // code costs the kernel 0.2-0.4 % at 10000^2 (same-box A/B of builds,
+  // profiles/r02s4_retire_build_ab.log), more than it gains there.
+  long kRetireMaxTiles = 4000;
+  if (const char* e = getenv("TILEQR_DAG_RETIRE_MAX_TILES")) kRetireMaxTiles = atol(e);  // diagnostics
+  if (!io && dag::dag_ctas_per_sm(NB) == 2 && ctas_per_sm == 2 && (MT - 1) * (NT - 1) <= kRetireMaxTiles) {
+    long kTailTiles = 500;
+    if (const char* e = getenv("TILEQR_DAG_RETIRE_TILES")) kTailTiles = atol(e);  // diagnostics; 0: off
+    int64_t tail = 0;
+    for (int64_t i = 0; i < ntask0; ++i)
+      if ((MT - tk[i].k - 1) * (NT - tk[i].k - 1) <= kTailTiles) tail += parts(tk[i].kind);
+    if (const char* e = getenv("TILEQR_DAG_RETIRE")) tail = atol(e);  // diagnostics: the count itself
+    if (kTailTiles > 0 && tail > 0) retire_from = std::max<int64_t>(0, (int64_t)sched.size() - tail);
   }
   std::vector<dag::Item> items;
   items.reserve(sched.size());
@@ -588,6 +604,7 @@ static int build_dag(FactorWS* ws, bool io) {
   L.ntasks = (int)ntask;
   L.nio = nst;
   L.io_tiles = kIoTiles;
+  L.retire = retire_from != INT64_MAX;
   L.launch_nsm = ctas_per_sm < dag::dag_ctas_per_sm(NB) ? std::max(1, nsm0 / dag::dag_ctas_per_sm(NB)) : 0;
   L.id_ld = ntask0;
   L.id_st = ntask0 + NT;
@@ -634,7 +651,7 @@ static int run_dag_list(FactorWS* ws, DagList& L, const dag::DagIO* io, cudaStre
     if (v >= 0 && v < nitems) nitems = (int)v;
   }
   int rc = launch_dag(ws->NB, ws->IB, L.d_items, nitems, L.d_ctr, L.d_ctr + 257, L.launch_nsm > 0 ? L.launch_nsm : ws->nsm, prof, stream,
-                      &ws->dag_grid, io, io ? dag::kModeIO : dag::kModePlain);
+                      &ws->dag_grid, io, io ? dag::kModeIO : L.retire ? dag::kModePlainRetire : dag::kModePlain);
   if (rc) return rc;
   if (g_timing & 15) TQ_CUDA(cudaEventRecord(ws->dag_ev[1], stream));
   if (acc) TQ_CUDA(cudaEventRecord(ws->acc_ev[2 * ws->acc_n++ + 1], stream));

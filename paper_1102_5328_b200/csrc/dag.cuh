@@ -298,6 +298,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
   // by CTA slots -- have their SM to themselves. 0: keeps claiming, 1: retires
   // at the first tail item, 2: claims no more
   __shared__ int s_retire;
+  constexpr bool RETIRE = MODE == kModePlainRetire;  // its own instantiation: the code costs the plain kernel 0.2-0.4 % at 10000^2
   uint32_t c2par = 0;   // all threads: phase of c2bar for the next staged slab
   uint32_t c2fpar = 0;  // thread 0: phase of c2free for the running update item
   if constexpr (C2PF) {
@@ -309,7 +310,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     }
     __syncthreads();
   }
-  if constexpr (MODE == kModePlain) {
+  if constexpr (RETIRE) {
     if (threadIdx.x == 0) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -328,7 +329,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
     if (threadIdx.x == 0) {
       int cur = nxt;
       if (cur < 0) {
-        if (MODE == kModePlain && s_retire == 2) cur = nitems;
+        if (RETIRE && s_retire == 2) cur = nitems;
         else cur = atomicAdd(next, 1);
         if (cur < nitems) fetch_desc(cur, slot);
       }
@@ -337,7 +338,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
       if (cur < nitems) {
         cp_async_wait<0>();
         const Item& it = s_desc[slot];
-        if (MODE == kModePlain && it.aux[3] != 0 && s_retire == 1) s_retire = 2;
+        if (RETIRE && it.aux[3] != 0 && s_retire == 1) s_retire = 2;
         int need[3], got[3];
         const int nd = it.ndep;
         if constexpr (MODE == kModeDist) {  // peer-written counters: system scope
@@ -400,7 +401,7 @@ dag_kernel(const Item* __restrict__ items, int nitems, int* next, int* done, int
         // items [0, ca_lo) and [ca_hi, nitems) of the list (same-box A/B at
         // 10000^2: within +-0.1 % for 300-2000 items at either end)
         if (i < ca_lo || i >= ca_hi) return;
-        if (MODE == kModePlain && s_retire == 2) return;
+        if (RETIRE && s_retire == 2) return;
         nxt = atomicAdd(next, 1);
         if constexpr (PC != PD) return;  // its result is first needed one panel later
       }
@@ -563,7 +564,8 @@ int launch_dag_t(int IB, const Item* items, int nitems, int* next, int* done, in
                  unsigned long long* prof, cudaStream_t s, int* grid_out, const DagIO* io, int mode) {
   auto kern = mode == kModeIO ? dag_kernel<NB, KW, kModeIO>
             : mode == kModeDist ? dag_kernel<NB, KW, kModeDist>
-            : mode == kModeTree ? dag_kernel<NB, KW, kModeTree> : dag_kernel<NB, KW, kModePlain>;
+            : mode == kModeTree ? dag_kernel<NB, KW, kModeTree>
+            : mode == kModePlainRetire ? dag_kernel<NB, KW, kModePlainRetire> : dag_kernel<NB, KW, kModePlain>;
   const size_t bytes = DagSmem<NB, KW>::bytes;
   static_assert(DagSmem<NB, KW>::bytes <= 227 * 1024, "DAG kernel shared memory");
   TQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));

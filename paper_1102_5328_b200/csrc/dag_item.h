@@ -26,7 +26,8 @@ enum Kind { kGeqrt = 0, kTsqrt = 1, kLarfb = 2, kSsrfb = 3, kLoad = 4, kStore = 
 // Kernel instantiations of the dataflow kernel (dag.cuh): the device-only
 // factorization, the host-buffer pipeline (LOAD / STORE items) and the
 // multi-rank dataflow factorization (COPY items, system-scope signals).
-enum Mode { kModePlain = 0, kModeIO = 1, kModeDist = 2, kModeTree = 3 };
+enum Mode { kModePlain = 0, kModeIO = 1, kModeDist = 2, kModeTree = 3,
+            kModePlainRetire = 4 };  // kModePlain + tail retirement (dag.cuh), for DAGs whose tail is a visible share
 
 // One work item: a whole panel task, or a column slab of an update task.
 struct Item {
