@@ -164,6 +164,27 @@ def test_factor_1024_against_oracle(tq, nb, ib):
     assert nrel(tq.from_colmajor(A), fo) < 1e-10 and nrel(T.cpu().numpy(), to) < 1e-10
 
 
+# The dataflow kernel's resident-CTA rules (session 4):
+# widest step (MT-1)(NT-1) <= 1200 tile updates: one CTA per SM; <= 4000: two
+# per SM with the second retiring in the tail (kModePlainRetire); above: the
+# plain kernel.  One oracle comparison per regime and tile order, ragged sizes.
+@pytest.mark.parametrize("n,nb,ib", [
+    (2000, 64, 16),    # 31^2 = 961 tiles: one CTA per SM
+    (2590, 64, 16),    # 40^2 = 1600: tail retirement
+    (2590, 64, 32),
+    (4650, 128, 16),   # 36^2 = 1296: tail retirement at NB = 128
+    (4200, 64, 16),    # 65^2 = 4225: plain kernel
+])
+def test_factor_resident_cta_regimes_against_oracle(tq, n, nb, ib):
+    a = si.uniform(n, n, 1000 + n)
+    A = tq.to_colmajor(a)
+    T, info = tq.factor(A, n, n, nb, ib)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    fo, to, _ = oracle.tileqr_factor(a, nb, ib)
+    assert nrel(tq.from_colmajor(A), fo) < 1e-10 and nrel(T.cpu().numpy(), to) < 1e-10
+
+
 # ---------------------------------------------------------------------------
 # apply_qt against the oracle
 # ---------------------------------------------------------------------------
